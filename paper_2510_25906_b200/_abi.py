@@ -336,3 +336,33 @@ ABI_SYMBOLS = [
     "ucfvb_get_phase_times", "ucfvb_n_cells", "ucfvb_n_faces", "ucfvb_n_qp",
     "ucfvb_state_device_ptr", "ucfvb_stream", "ucfvb_launch_count",
 ]
+
+
+class UcfvbError(RuntimeError):
+    """Base error of the C ABI (status code in .code)."""
+
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class NonPhysicalError(UcfvbError):
+    """The reference's NonPhysicalError (euler.hpp:18-20)."""
+
+
+class InvalidArgument(UcfvbError, ValueError):
+    """std::invalid_argument / MeshError of the reference."""
+
+
+class CudaError(UcfvbError):
+    pass
+
+
+class Unsupported(UcfvbError):
+    pass
+
+
+def error_for(code, msg) -> UcfvbError:
+    cls = {NONPHYSICAL: NonPhysicalError, INVALID: InvalidArgument, CUDA_ERR: CudaError,
+           UNSUPPORTED: Unsupported}.get(code, UcfvbError)
+    return cls(code, msg)

@@ -1,0 +1,673 @@
+// GpuSolver: the device-resident replacement of ucfv::Solver
+// (/root/reference/proj/include/ucfv/solver.hpp:52-100) behind the C ABI of
+// include/ucfvb.h. One CUDA stream per handle; one RK step is captured as a
+// CUDA graph (per integrator, buffer parity and dt source) and replayed.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "layout.hpp"
+#include "solver.hpp"
+
+namespace ucfvb {
+
+#define CK(x)                                                                                        \
+  do {                                                                                               \
+    cudaError_t e_ = (x);                                                                            \
+    if (e_ != cudaSuccess)                                                                           \
+      throw ApiError(UCFVB_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                   \
+  } while (0)
+
+// ---- kernel dispatch over (K, NQ, NF) ----------------------------------------
+struct KernelSet {
+  void (*central)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
+  void (*spread)(dim3, cudaStream_t, const Layout&, const Scratch&, const double4*, int, int);
+  void (*cwenoz)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
+  void (*muscl)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
+  void (*constant)(dim3, cudaStream_t, const Layout&, const Scratch&, const double4*);
+  void (*flux)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*,
+               const RkEpilogue&, int);
+};
+
+template <int K, int NQ, int NF>
+KernelSet make_set() {
+  KernelSet s;
+  s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+                 int f) { k_central<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+  s.spread = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U, int f, int d) {
+    k_spread<NQ, NF><<<g, kBlock, 0, st>>>(L, S, U, f, d);
+  };
+  s.cwenoz = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+                int f) { k_cwenoz<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+  s.muscl = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+               int f) { k_muscl<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+  s.constant = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U) {
+    k_constant<NQ, NF><<<g, kBlock, 0, st>>>(L, S, U);
+  };
+  s.flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+              const RkEpilogue& rk, int f) { k_flux<NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, rk, f); };
+  return s;
+}
+
+static KernelSet pick_kernels(int K, int NQ, int NF) {
+#define UCFVB_CASE(k, q, f) \
+  if (K == k && NQ == q && NF == f) return make_set<k, q, f>();
+  UCFVB_CASE(2, 1, 3) UCFVB_CASE(2, 1, 4)
+  UCFVB_CASE(5, 2, 3) UCFVB_CASE(5, 2, 4)
+  UCFVB_CASE(9, 2, 3) UCFVB_CASE(9, 2, 4)
+  UCFVB_CASE(14, 3, 3) UCFVB_CASE(14, 3, 4)
+#undef UCFVB_CASE
+  throw ApiError(UCFVB_UNSUPPORTED, "solver: reconstruction order with K=" + std::to_string(K) + ", n_qp=" +
+                                        std::to_string(NQ) + " is not instantiated (orders 1-4 are)");
+}
+
+template <typename T>
+static T* dalloc(size_t n, std::vector<void*>& owned) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  CK(cudaMalloc(&p, n * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+static T* dupload(const std::vector<T>& h, std::vector<void*>& owned) {
+  T* d = dalloc<T>(h.size(), owned);
+  if (!h.empty()) CK(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+// Spiteri & Ruuth SSPRK(5,4) coefficients (time_integrator.cpp:11-29)
+namespace rk54 {
+constexpr double a10 = 0.391752226571890;
+constexpr double b20 = 0.444370493651235, b21 = 0.555629506348765, a21 = 0.368410593050371;
+constexpr double b30 = 0.620101851488403, b32 = 0.379898148511597, a32 = 0.251891774271694;
+constexpr double b40 = 0.178079954393132, b43 = 0.821920045606868, a43 = 0.544974750228521;
+constexpr double c52 = 0.517231671970585, c53 = 0.096059710526147, a53 = 0.063692468666290;
+constexpr double c54 = 0.386708617503269, a54 = 0.226007483236906;
+}  // namespace rk54
+
+struct GpuSolver::Impl {
+  HostLayout host;
+  Layout L{};
+  Physics ph{};
+  Scratch S{};
+  ucfvb_options opt{};
+  KernelSet ks{};
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int n_sm = 148;
+  std::vector<void*> owned;
+  double4* ubuf[2] = {nullptr, nullptr};
+  int cur = 0;
+  double4* work[6] = {};  // RK3: u1,u2 ; RK54: ua,ub,uc,ud,rhs3 ; [5] = compute_residual input
+  double4* rhs = nullptr;
+  DtState* ds = nullptr;
+  unsigned long long* census_dev = nullptr;
+  size_t census_cap = 0;
+  int* step_zero = nullptr;  // device int 0 (census row for advance())
+  bool stage_is_first = true;
+  bool timing = false;
+  double phase[4] = {0, 0, 0, 0};
+  cudaEvent_t ev[5] = {};
+  int64_t launches = 0;
+  // graphs: [rk][with_dt][parity]
+  cudaGraphExec_t graph[2][2][2] = {};
+  int64_t graph_launches[2][2][2] = {};
+  std::string last_error;
+
+  dim3 grid_cells() const { return dim3((L.n + kBlock - 1) / kBlock); }
+  dim3 grid_list() const {
+    const int want = (L.n + kBlock - 1) / kBlock;
+    return dim3(std::max(1, std::min(want, n_sm * 8)));
+  }
+
+  void record(int i) {
+    if (timing) CK(cudaEventRecord(ev[i], stream));
+  }
+
+  // one compute_residual stage on the stream (solver.cpp:316-379)
+  int64_t launch_stage(const double4* U, bool first, const RkEpilogue& rk, bool census) {
+    int64_t nl = 0;
+    const int taps = opt.keep_taps ? FL_TAPS : 0;
+    const int mode = opt.mode;
+    record(0);
+    if (mode == UCFVB_HYBRID) {
+      const bool detect = first || opt.detect_every_stage;
+      CK(cudaMemsetAsync(S.counts, 0, 2 * sizeof(int), stream));
+      if (detect) CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream));
+      ks.central(grid_cells(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
+      record(1);
+      ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
+      record(2);
+      ks.cwenoz(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+      ks.muscl(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+      nl += 4;
+    } else if (mode == UCFVB_LINEAR) {
+      ks.central(grid_cells(), stream, L, ph, S, U, FL_EVAL | (taps ? FL_DOFS : 0));
+      record(1);
+      record(2);
+      nl += 1;
+    } else if (mode == UCFVB_CWENOZ) {
+      ks.central(grid_cells(), stream, L, ph, S, U, FL_DOFS);
+      record(1);
+      record(2);
+      ks.cwenoz(grid_cells(), stream, L, ph, S, U, taps);
+      nl += 2;
+    } else if (mode == UCFVB_MUSCL) {
+      record(1);
+      record(2);
+      ks.muscl(grid_cells(), stream, L, ph, S, U, taps);
+      nl += 1;
+    } else {
+      record(1);
+      record(2);
+      ks.constant(grid_cells(), stream, L, S, U);
+      nl += 1;
+    }
+    record(3);
+    int ff = 0;
+    if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
+    ks.flux(grid_cells(), stream, L, ph, S, U, rk, ff);
+    record(4);
+    CK(cudaGetLastError());
+    return nl + 1;
+  }
+
+  void accumulate_phases() {
+    if (!timing) return;
+    CK(cudaEventSynchronize(ev[4]));
+    float ms[4];
+    for (int i = 0; i < 4; ++i) CK(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    for (int i = 0; i < 4; ++i) phase[i] += 1e-3 * ms[i];
+  }
+
+  static void add_term(RkEpilogue& e, const double4* t, double coef, bool dt_scaled) {
+    e.term[e.nterms] = t;
+    e.coef[e.nterms] = coef;
+    e.dt_scaled[e.nterms] = dt_scaled ? 1 : 0;
+    ++e.nterms;
+  }
+
+  // All launches of one time step (the body a graph captures). `src` is the
+  // state at t, `dst` receives the state at t+dt. With `with_dt` the step
+  // starts with k_dt (device dt, run_steps); otherwise ds->dt was set by the host.
+  int64_t launch_step(int rk, bool with_dt, const double4* src, double4* dst, bool census) {
+    int64_t nl = 0;
+    const double* dt = &ds->dt;
+    if (with_dt) {
+      k_dt<<<dim3((L.n + 255) / 256), 256, 0, stream>>>(L, src, opt.gamma, ds, S.err);
+      ++nl;
+    }
+    if (rk == UCFVB_RK3) {
+      double4 *u1 = work[0], *u2 = work[1];
+      RkEpilogue e1{};
+      e1.dt = dt;
+      e1.out = u1;
+      add_term(e1, src, 1.0, false);
+      add_term(e1, src, 0.0, false);
+      add_term(e1, nullptr, 1.0, true);
+      nl += launch_stage(src, true, e1, census);
+      RkEpilogue e2{};
+      e2.dt = dt;
+      e2.out = u2;
+      add_term(e2, src, 0.75, false);
+      add_term(e2, u1, 0.25, false);
+      add_term(e2, nullptr, 0.25, true);
+      nl += launch_stage(u1, false, e2, census);
+      RkEpilogue e3{};
+      e3.dt = dt;
+      e3.out = dst;
+      add_term(e3, src, 1.0 / 3.0, false);
+      add_term(e3, u2, 2.0 / 3.0, false);
+      add_term(e3, nullptr, 2.0 / 3.0, true);
+      nl += launch_stage(u2, false, e3, census);
+    } else {
+      using namespace rk54;
+      double4 *ua = work[0], *ub = work[1], *uc = work[2], *ud = work[3], *r3 = work[4];
+      RkEpilogue e{};
+      e.dt = dt;
+      e.out = ua;
+      add_term(e, src, 1.0, false);
+      add_term(e, src, 0.0, false);
+      add_term(e, nullptr, a10, true);
+      nl += launch_stage(src, true, e, census);
+      e = RkEpilogue{};
+      e.dt = dt;
+      e.out = ub;
+      add_term(e, src, b20, false);
+      add_term(e, ua, b21, false);
+      add_term(e, nullptr, a21, true);
+      nl += launch_stage(ua, false, e, census);
+      e = RkEpilogue{};
+      e.dt = dt;
+      e.out = uc;
+      add_term(e, src, b30, false);
+      add_term(e, ub, b32, false);
+      add_term(e, nullptr, a32, true);
+      nl += launch_stage(ub, false, e, census);
+      e = RkEpilogue{};
+      e.dt = dt;
+      e.out = ud;
+      e.rhs_out = r3;
+      add_term(e, src, b40, false);
+      add_term(e, uc, b43, false);
+      add_term(e, nullptr, a43, true);
+      nl += launch_stage(uc, false, e, census);
+      e = RkEpilogue{};
+      e.dt = dt;
+      e.out = dst;
+      add_term(e, ub, c52, false);
+      add_term(e, uc, c53, false);
+      add_term(e, r3, a53, true);
+      add_term(e, ud, c54, false);
+      add_term(e, nullptr, a54, true);
+      nl += launch_stage(ud, false, e, census);
+    }
+    return nl;
+  }
+
+  cudaGraphExec_t get_graph(int rk, bool with_dt, int parity) {
+    cudaGraphExec_t& g = graph[rk][with_dt][parity];
+    if (g) return g;
+    cudaGraph_t gr;
+    CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+    const int64_t nl = launch_step(rk, with_dt, ubuf[parity], ubuf[parity ^ 1], with_dt);
+    CK(cudaStreamEndCapture(stream, &gr));
+    CK(cudaGraphInstantiate(&g, gr, 0));
+    CK(cudaGraphDestroy(gr));
+    graph_launches[rk][with_dt][parity] = nl;
+    return g;
+  }
+
+  int err_step = 0;
+  int read_error(int* kind, int* face, int* cell) {
+    int e[4];
+    CK(cudaMemcpyAsync(e, S.err, sizeof e, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    *kind = e[0];
+    *face = e[1];
+    *cell = e[2];
+    err_step = e[3];
+    return e[0];
+  }
+
+  void reset_error() {
+    const int e[4] = {0, INT_MAX, INT_MAX, INT_MAX};
+    CK(cudaMemcpyAsync(S.err, e, sizeof e, cudaMemcpyHostToDevice, stream));
+  }
+
+  // translate the device error word into the reference's exceptions
+  void raise_device_error(int kind, int face, int cell) {
+    reset_error();
+    CK(cudaStreamSynchronize(stream));
+    if (kind & 4) throw ApiError(UCFVB_INVALID, "cwenoz: central linear weight lambda1' must exceed 1");
+    if (kind & 2)
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state in max_stable_dt at cell " + std::to_string(cell));
+    if (kind & 1) {
+      std::string where = " at face " + std::to_string(face);
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state" + where);
+    }
+  }
+
+  void check_after() {
+    int k, f, c;
+    if (read_error(&k, &f, &c)) raise_device_error(k, f, c);
+  }
+};
+
+GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, const ucfvb_options& o,
+                     const ucfvb_bc* bcs, int n_bcs, int device)
+    : p_(new Impl) {
+  Impl& I = *p_;
+  I.opt = o;
+  I.device = device;
+  // validate_margins (detector.cpp:9-16)
+  const ucfvb_margins& mg = o.margins;
+  if (mg.alpha_m < 0.0 || mg.beta_m < 0.0)
+    throw ApiError(UCFVB_INVALID, "NAD margins: alpha_m and beta_m must be non-negative");
+  if (mg.beta_w > 0.0 && (mg.beta_w > mg.beta_m || mg.alpha_w > mg.alpha_m))
+    throw ApiError(UCFVB_INVALID,
+                   "NAD margins: delta_w <= delta_m requires beta_w <= beta_m and alpha_w <= alpha_m");
+  if (mg.kappa < 0.0) throw ApiError(UCFVB_INVALID, "NAD margins: kappa must be >= 0");
+  if (o.mode < 0 || o.mode > 4) throw ApiError(UCFVB_INVALID, "solver: unknown scheme mode");
+
+  // boundary conditions by patch name (solver.cpp:46-60)
+  Physics& ph = I.ph;
+  if (m.n_patches > kMaxPatches) throw ApiError(UCFVB_UNSUPPORTED, "solver: more than 16 boundary patches");
+  for (int i = 0; i < n_bcs; ++i) {
+    int pid = -1;
+    for (int p = 0; p < m.n_patches; ++p)
+      if (bcs[i].patch && std::strcmp(m.patch_names[p], bcs[i].patch) == 0) pid = p;
+    if (pid < 0)
+      throw ApiError(UCFVB_INVALID,
+                     std::string("solver: unknown boundary patch '") + (bcs[i].patch ? bcs[i].patch : "") + "'");
+    if (bcs[i].kind < UCFVB_BC_NONE || bcs[i].kind > UCFVB_BC_FIXED)
+      throw ApiError(UCFVB_UNSUPPORTED, "solver: boundary condition kind not available on the device");
+    ph.bc[pid].kind = bcs[i].kind;
+    for (int v = 0; v < 4; ++v) ph.bc[pid].state[v] = bcs[i].state[v];
+  }
+  for (int f = 0; f < m.n_faces; ++f)
+    if (m.face_right[f] < 0 && m.face_partner[f] < 0) {
+      const int p = m.face_patch[f];
+      if (p < 0 || ph.bc[p].kind == UCFVB_BC_NONE)
+        throw ApiError(UCFVB_INVALID, "solver: boundary face " + std::to_string(f) +
+                                          " has no boundary condition (patch " +
+                                          (p >= 0 ? std::string(m.patch_names[p]) : std::string("<none>")) + ")");
+    }
+
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  I.n_sm = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
+  for (auto& e : I.ev) CK(cudaEventCreate(&e));
+
+  I.host = build_layout(m, s, o, 0);
+  const HostLayout& H = I.host;
+  I.ks = pick_kernels(H.K, H.NQ, H.NF);
+  auto& own = I.owned;
+  Layout& L = I.L;
+  L.n = H.n;
+  L.MM = H.MM;
+  L.MD = H.MD;
+  L.st_idx = dupload(H.st_idx, own);
+  L.pinv = dupload(H.pinv, own);
+  L.phi = dupload(H.phi, own);
+  L.pinv_lin = dupload(H.pinv_lin, own);
+  L.dir_idx = dupload(H.dir_idx, own);
+  L.pinv_dir = dupload(H.pinv_dir, own);
+  L.oi = dupload(H.oi, own);
+  L.nbr = dupload(H.nbr, own);
+  L.other_ref = dupload(H.other_ref, own);
+  L.self_lq = dupload(H.self_lq, own);
+  L.fgeom = dupload(H.fgeom, own);
+  L.fsgn = dupload(H.fsgn, own);
+  L.face_id = dupload(H.face_id, own);
+  L.nfc = dupload(H.nfc, own);
+  L.deact_thr = dupload(H.deact_thr, own);
+  L.eps2 = dupload(H.eps2, own);
+  L.h = dupload(H.h, own);
+  L.inv_vol = dupload(H.inv_vol, own);
+
+  ph.mp = MarginParams{mg.alpha_m, mg.beta_m, mg.alpha_w, mg.beta_w, mg.kappa, mg.deact_n};
+  ph.gamma = o.gamma;
+  ph.lambda1p = o.lambda1p;
+  ph.weno_eps = o.weno_eps;
+  ph.weno_b = o.weno_b;
+  ph.limiter = o.limiter;
+  ph.hll = o.riemann == UCFVB_HLL ? 1 : 0;
+  for (int q = 0; q < 4; ++q) ph.qw[q] = H.qw[q];
+
+  const size_t nch = static_cast<size_t>(H.n_pad / 32);
+  Scratch& S = I.S;
+  S.fv = dalloc<double4>(nch * H.Q * 32, own);
+  S.dofs = dalloc<double4>(nch * H.K * 32, own);
+  S.raw = dalloc<uint8_t>(H.n_pad, own);
+  S.labels = dalloc<uint8_t>(H.n_pad, own);
+  S.step_labels = dalloc<uint8_t>(H.n_pad, own);
+  S.list_c = dalloc<int>(H.n, own);
+  S.list_m = dalloc<int>(H.n, own);
+  S.counts = dalloc<int>(2, own);
+  S.ties = dalloc<unsigned long long>(1, own);
+  S.err = dalloc<int>(4, own);
+  I.step_zero = dalloc<int>(1, own);
+  CK(cudaMemset(I.step_zero, 0, sizeof(int)));
+  CK(cudaMemset(S.fv, 0, nch * H.Q * 32 * sizeof(double4)));
+  CK(cudaMemset(S.dofs, 0, nch * H.K * 32 * sizeof(double4)));
+  CK(cudaMemset(S.ties, 0, sizeof(unsigned long long)));
+  CK(cudaMemset(S.raw, 0, H.n_pad));
+  // labels_ start Linear (solver.cpp:72-73); forced modes label every cell once
+  const int init_label = o.mode == UCFVB_CWENOZ ? 1 : o.mode == UCFVB_MUSCL ? 2 : o.mode == UCFVB_FIRST ? 3 : 0;
+  CK(cudaMemset(S.labels, init_label, H.n_pad));
+  CK(cudaMemset(S.step_labels, 0, H.n_pad));
+  S.step = I.step_zero;
+  S.census = nullptr;
+  for (auto& b : I.ubuf) {
+    b = dalloc<double4>(H.n_pad, own);
+    CK(cudaMemset(b, 0, H.n_pad * sizeof(double4)));
+  }
+  for (auto& w : I.work) {
+    w = dalloc<double4>(H.n_pad, own);
+    CK(cudaMemset(w, 0, H.n_pad * sizeof(double4)));
+  }
+  I.rhs = dalloc<double4>(H.n_pad, own);
+  I.ds = dalloc<DtState>(1, own);
+  I.reset_error();
+  CK(cudaStreamSynchronize(I.stream));
+}
+
+GpuSolver::~GpuSolver() {
+  if (!p_) return;
+  Impl& I = *p_;
+  cudaStreamSynchronize(I.stream);
+  for (auto& a : I.graph)
+    for (auto& b : a)
+      for (auto& g : b)
+        if (g) cudaGraphExecDestroy(g);
+  for (void* p : I.owned) cudaFree(p);
+  if (I.census_dev) cudaFree(I.census_dev);
+  for (auto& e : I.ev)
+    if (e) cudaEventDestroy(e);
+  if (I.stream) cudaStreamDestroy(I.stream);
+}
+
+int GpuSolver::n_cells() const { return p_->L.n; }
+int GpuSolver::n_faces() const { return p_->host.n_faces; }
+int GpuSolver::n_qp() const { return p_->host.NQ; }
+int GpuSolver::K() const { return p_->host.K; }
+int64_t GpuSolver::launch_count() const { return p_->launches; }
+void* GpuSolver::stream() const { return p_->stream; }
+double* GpuSolver::state_device_ptr() { return reinterpret_cast<double*>(p_->ubuf[p_->cur]); }
+
+void GpuSolver::set_state(const double* u) {
+  Impl& I = *p_;
+  CK(cudaMemcpyAsync(I.ubuf[I.cur], u, sizeof(double4) * I.L.n, cudaMemcpyHostToDevice, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+}
+
+void GpuSolver::get_state(double* u) {
+  Impl& I = *p_;
+  CK(cudaMemcpyAsync(u, I.ubuf[I.cur], sizeof(double4) * I.L.n, cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+}
+
+double GpuSolver::max_stable_dt() {
+  Impl& I = *p_;
+  DtState h{};
+  h.dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);  // bits of 1e300
+  h.t = 0.0;
+  h.dt = 0.0;
+  h.step = -1;
+  h.t_end = INFINITY;
+  h.cfl = I.opt.cfl;
+  CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
+  k_dt<<<dim3((I.L.n + 255) / 256), 256, 0, I.stream>>>(I.L, I.ubuf[I.cur], I.opt.gamma, I.ds, I.S.err);
+  CK(cudaGetLastError());
+  I.launches = 1;
+  CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
+  I.check_after();
+  return h.dt;
+}
+
+void GpuSolver::advance(double dt, double t, int rk) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance: unknown integrator");
+  DtState h{};
+  h.dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);
+  h.t = t;
+  h.dt = dt;
+  h.step = 0;
+  h.t_end = INFINITY;
+  h.cfl = I.opt.cfl;
+  CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
+  I.S.step = I.step_zero;
+  I.stage_is_first = true;  // Solver::advance (solver.cpp:382)
+  if (I.opt.use_graphs && !I.timing) {
+    cudaGraphExec_t g = I.get_graph(rk, false, I.cur);
+    CK(cudaGraphLaunch(g, I.stream));
+    I.launches = I.graph_launches[rk][0][I.cur];
+  } else {
+    I.launches = I.launch_step(rk, false, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], false);
+  }
+  int k, f, c;
+  if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);  // state stays at t (reference semantics)
+  I.cur ^= 1;
+  I.stage_is_first = false;
+}
+
+void GpuSolver::compute_residual(const double* u, double t, double* out) {
+  Impl& I = *p_;
+  (void)t;
+  double4* in = I.work[5];
+  CK(cudaMemcpyAsync(in, u, sizeof(double4) * I.L.n, cudaMemcpyHostToDevice, I.stream));
+  RkEpilogue e{};
+  e.rhs_out = I.rhs;
+  e.dt = &I.ds->dt;
+  I.launches = I.launch_stage(in, I.stage_is_first, e, false);
+  I.accumulate_phases();
+  I.stage_is_first = false;
+  int k, f, c;
+  if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);
+  CK(cudaMemcpyAsync(out, I.rhs, sizeof(double4) * I.L.n, cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+}
+
+double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census_out) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "run_steps: unknown integrator");
+  if (n_steps <= 0) return t0;
+  const bool census = census_out != nullptr;
+  if (census && I.census_cap < static_cast<size_t>(n_steps)) {
+    if (I.census_dev) CK(cudaFree(I.census_dev));
+    CK(cudaMalloc(&I.census_dev, sizeof(unsigned long long) * 4 * n_steps));
+    I.census_cap = n_steps;
+  }
+  if (census) CK(cudaMemsetAsync(I.census_dev, 0, sizeof(unsigned long long) * 4 * n_steps, I.stream));
+  DtState h{};
+  h.dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);
+  h.t = t0;
+  h.dt = 0.0;
+  h.step = -1;
+  h.t_end = t_end;
+  h.cfl = I.opt.cfl;
+  CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
+  // census rows are indexed by the device step counter
+  I.S.census = census ? I.census_dev : nullptr;
+  I.S.step = &I.ds->step;
+  const bool graphs = I.opt.use_graphs && !I.timing;
+  const int cur0 = I.cur;
+  int64_t nl = 0;
+  for (int s = 0; s < n_steps; ++s) {
+    if (graphs) {
+      // graphs capture the census flag; keep separate graphs only for census runs
+      if (census) {
+        nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], true);
+      } else {
+        cudaGraphExec_t g = I.get_graph(rk, true, I.cur);
+        CK(cudaGraphLaunch(g, I.stream));
+        nl += I.graph_launches[rk][1][I.cur];
+      }
+    } else {
+      nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], census);
+    }
+    I.cur ^= 1;
+  }
+  I.launches = nl;
+  I.S.step = I.step_zero;
+  I.S.census = nullptr;
+  CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
+  int k, f, c;
+  if (I.read_error(&k, &f, &c)) {
+    // step s reads ubuf[(cur0 + s) & 1] and never overwrites it: the failing
+    // step's input is the last good state (the reference throws out of
+    // advance()/max_stable_dt() before touching state_)
+    const int failed = std::min(std::max(0, I.err_step), n_steps - 1);
+    I.cur = (cur0 + failed) & 1;
+    try {
+      I.raise_device_error(k, f, c);
+    } catch (ApiError& e) {
+      throw ApiError(e.code, "run failed at step " + std::to_string(failed) + ": " + e.what());
+    }
+  }
+  if (census) {
+    std::vector<unsigned long long> tmp(4 * static_cast<size_t>(n_steps));
+    CK(cudaMemcpy(tmp.data(), I.census_dev, tmp.size() * sizeof(tmp[0]), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < tmp.size(); ++i) census_out[i] = static_cast<int64_t>(tmp[i]);
+  }
+  I.stage_is_first = false;
+  return h.t + h.dt;
+}
+
+void GpuSolver::get_labels(uint8_t* out, bool step) {
+  Impl& I = *p_;
+  CK(cudaMemcpyAsync(out, step ? I.S.step_labels : I.S.labels, I.L.n, cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+}
+
+void GpuSolver::get_census(int64_t counts[4]) {
+  std::vector<uint8_t> lab(n_cells());
+  get_labels(lab.data(), true);
+  counts[0] = counts[1] = counts[2] = counts[3] = 0;
+  for (uint8_t l : lab) ++counts[l & 3];
+}
+
+int64_t GpuSolver::nad_ties() {
+  Impl& I = *p_;
+  unsigned long long t = 0;
+  CK(cudaMemcpy(&t, I.S.ties, sizeof t, cudaMemcpyDeviceToHost));
+  return static_cast<int64_t>(t);
+}
+
+void GpuSolver::get_face_values(double* left, double* right) {
+  Impl& I = *p_;
+  const HostLayout& H = I.host;
+  const size_t nch = static_cast<size_t>(H.n_pad / 32);
+  std::vector<double4> fv(nch * H.Q * 32);
+  CK(cudaMemcpyAsync(fv.data(), I.S.fv, fv.size() * sizeof(double4), cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+  for (int c = 0; c < H.n; ++c)
+    for (int64_t q = H.qp_ptr[c]; q < H.qp_ptr[c + 1]; ++q) {
+      const int slot = H.qp_slot[q];
+      const double4 v = fv[aos_index(c, static_cast<int>(q - H.qp_ptr[c]), H.Q)];
+      double* dst = ((slot & 1) ? right : left) + 4 * static_cast<int64_t>(slot >> 1);
+      dst[0] = v.x;
+      dst[1] = v.y;
+      dst[2] = v.z;
+      dst[3] = v.w;
+    }
+}
+
+void GpuSolver::get_dofs(double* dofs) {
+  Impl& I = *p_;
+  const HostLayout& H = I.host;
+  if (!I.opt.keep_taps && I.opt.mode != UCFVB_HYBRID)
+    throw ApiError(UCFVB_INVALID, "get_dofs: create the solver with keep_taps = 1");
+  const size_t nch = static_cast<size_t>(H.n_pad / 32);
+  std::vector<double4> d(nch * H.K * 32);
+  CK(cudaMemcpyAsync(d.data(), I.S.dofs, d.size() * sizeof(double4), cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+  for (int c = 0; c < H.n; ++c)
+    for (int k = 0; k < H.K; ++k) {
+      const double4 v = d[aos_index(c, k, H.K)];
+      double* dst = dofs + (static_cast<int64_t>(c) * H.K + k) * 4;
+      dst[0] = v.x;
+      dst[1] = v.y;
+      dst[2] = v.z;
+      dst[3] = v.w;
+    }
+}
+
+void GpuSolver::set_phase_timing(bool on) { p_->timing = on; }
+void GpuSolver::get_phase_times(double t[4]) {
+  for (int i = 0; i < 4; ++i) t[i] = p_->phase[i];
+}
+
+}  // namespace ucfvb

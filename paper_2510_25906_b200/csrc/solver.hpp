@@ -1,0 +1,49 @@
+// GpuSolver: C++ host side of the B200 stage pass, mirroring the public API of
+// ucfv::Solver (/root/reference/proj/include/ucfv/solver.hpp:52-100).
+#pragma once
+
+#include <cstdint>
+#include <memory>
+
+#include "ucfvb.h"
+
+namespace ucfvb {
+
+class GpuSolver {
+ public:
+  // Solver(mesh, opt, bcs) (solver.cpp:36-74); throws ApiError
+  GpuSolver(const ucfvb_mesh_view& mesh, const ucfvb_stencil_view& stencils, const ucfvb_options& opt,
+            const ucfvb_bc* bcs, int n_bcs, int device);
+  ~GpuSolver();
+  GpuSolver(const GpuSolver&) = delete;
+  GpuSolver& operator=(const GpuSolver&) = delete;
+
+  void set_state(const double* u);                                   // state() = u
+  void get_state(double* u);                                         // u = state()
+  double max_stable_dt();                                            // solver.cpp:103-111
+  void advance(double dt, double t, int rk);                         // solver.cpp:381-387
+  void compute_residual(const double* u, double t, double* out);     // solver.cpp:316-379
+  double run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census);  // run.cpp:97-132
+
+  void get_labels(uint8_t* out, bool step);
+  void get_census(int64_t counts[4]);
+  int64_t nad_ties();
+  void get_face_values(double* left, double* right);
+  void get_dofs(double* dofs);
+  void set_phase_timing(bool on);
+  void get_phase_times(double t[4]);
+
+  int n_cells() const;
+  int n_faces() const;
+  int n_qp() const;
+  int K() const;
+  int64_t launch_count() const;
+  void* stream() const;
+  double* state_device_ptr();
+
+ private:
+  struct Impl;
+  std::unique_ptr<Impl> p_;
+};
+
+}  // namespace ucfvb

@@ -1,0 +1,195 @@
+"""Python face of the B200 stage pass: mirrors ucfv::Solver
+(/root/reference/proj/include/ucfv/solver.hpp:52-100) over the C ABI.
+
+    solver = Solver(mesh, options, bcs)       # Solver(mesh, opt, bcs)
+    solver.state = u0                          # state() = ...
+    dt = solver.max_stable_dt()
+    solver.advance(dt, t)                      # one step (RK54 like the reference, or RK3)
+    r = solver.compute_residual(u, t)
+    solver.step_labels()
+
+Every call runs on the GPU through libucfvb.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi as A
+from .mesh import Mesh, Stencils
+
+
+def _dp(a):
+    return a.ctypes.data_as(A.c_dp)
+
+
+def make_options(**kw) -> A.Options:
+    """SolverOptions with keyword overrides (mode may be a name: 'hybrid', 'cwenoz', ...)."""
+    return A.options_from_dict(**kw)
+
+
+def make_bcs(mapping) -> list:
+    """{'left': 'outflow', 'right': ('fixed', state), 'top': 'wall'} -> [BC]."""
+    out = []
+    for patch, spec in (mapping or {}).items():
+        if isinstance(spec, str):
+            kind, state = spec, (0.0, 0.0, 0.0, 0.0)
+        else:
+            kind, state = spec[0], spec[1]
+        k = {"outflow": A.BC_OUTFLOW, "wall": A.BC_WALL, "fixed": A.BC_FIXED}[kind]
+        out.append(A.BC(patch.encode(), k, (C.c_double * 4)(*state)))
+    return out
+
+
+class Solver:
+    """Device-resident drop-in for ucfv::Solver.
+
+    mesh: a `Mesh` (or any object with `.view` -> MeshView); stencils: a
+    `Stencils` built for options.order, or None to build them here; bcs: a
+    list of A.BC or a {patch: kind} mapping.
+    """
+
+    def __init__(self, mesh, options: A.Options | None = None, bcs=None, stencils=None, device: int = 0,
+                 keep=()):
+        self._lib = A.load_library()
+        self.options = options if options is not None else A.default_options()
+        if stencils is None:
+            stencils = Stencils(mesh, self.options.order, self.options.si_exponent)
+        self.mesh = mesh
+        self.stencils = stencils
+        self._keep = keep
+        if isinstance(bcs, dict):
+            bcs = make_bcs(bcs)
+        bcs = list(bcs or [])
+        self._bcs = (A.BC * max(1, len(bcs)))(*bcs)
+        h = C.c_void_p()
+        rc = self._lib.ucfvb_create(C.byref(mesh.view), C.byref(stencils.view), C.byref(self.options), self._bcs,
+                                    len(bcs), int(device), C.byref(h))
+        if rc != A.OK:
+            raise A.error_for(rc, self._lib.ucfvb_last_error(None).decode())
+        self._h = h
+        self.n_cells = self._lib.ucfvb_n_cells(h)
+        self.n_faces = self._lib.ucfvb_n_faces(h)
+        self.n_qp = self._lib.ucfvb_n_qp(h)
+        self.K = stencils.view.K
+
+    # -- errors ------------------------------------------------------------
+    def _ck(self, rc):
+        if rc != A.OK:
+            raise A.error_for(rc, self._lib.ucfvb_last_error(self._h).decode())
+
+    # -- Solver API ----------------------------------------------------------
+    @property
+    def state(self) -> np.ndarray:
+        u = np.zeros((self.n_cells, 4))
+        self._ck(self._lib.ucfvb_get_state(self._h, _dp(u)))
+        return u
+
+    @state.setter
+    def state(self, u):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        if u.shape != (self.n_cells, 4):
+            raise ValueError(f"state must be ({self.n_cells}, 4)")
+        self._ck(self._lib.ucfvb_set_state(self._h, _dp(u)))
+
+    def set_state(self, u):
+        self.state = u
+
+    def get_state(self):
+        return self.state
+
+    def max_stable_dt(self) -> float:
+        d = C.c_double()
+        self._ck(self._lib.ucfvb_max_stable_dt(self._h, C.byref(d)))
+        return d.value
+
+    def advance(self, dt: float, t: float, rk: int = A.RK54):
+        """One step in place; rk=RK54 is Solver::advance, RK3 the BASELINE integrator."""
+        self._ck(self._lib.ucfvb_advance(self._h, float(dt), float(t), int(rk)))
+
+    def compute_residual(self, u, t: float = 0.0) -> np.ndarray:
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        out = np.zeros((self.n_cells, 4))
+        self._ck(self._lib.ucfvb_compute_residual(self._h, _dp(u), float(t), _dp(out)))
+        return out
+
+    def run_steps(self, n_steps: int, rk: int = A.RK3, t0: float = 0.0, t_end: float = float("inf"),
+                  census: bool = False):
+        """run_simulation's stepping loop on the device; returns (t, census[n_steps,4] or None)."""
+        t = C.c_double()
+        cen = np.zeros((n_steps, 4), dtype=np.int64) if census else None
+        self._ck(self._lib.ucfvb_run_steps(self._h, int(n_steps), int(rk), float(t0), float(t_end), C.byref(t),
+                                           cen.ctypes.data_as(A.c_i64p) if census else None))
+        return t.value, cen
+
+    def step_labels(self) -> np.ndarray:
+        out = np.zeros(self.n_cells, dtype=np.uint8)
+        self._ck(self._lib.ucfvb_get_step_labels(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out
+
+    def labels(self) -> np.ndarray:
+        out = np.zeros(self.n_cells, dtype=np.uint8)
+        self._ck(self._lib.ucfvb_get_labels(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8))))
+        return out
+
+    def census(self) -> np.ndarray:
+        c = np.zeros(4, dtype=np.int64)
+        self._ck(self._lib.ucfvb_get_census(self._h, c.ctypes.data_as(A.c_i64p)))
+        return c
+
+    def nad_ties(self) -> int:
+        t = C.c_int64()
+        self._ck(self._lib.ucfvb_get_nad_ties(self._h, C.byref(t)))
+        return t.value
+
+    def face_values(self):
+        L = np.zeros((self.n_faces * self.n_qp, 4))
+        R = np.zeros_like(L)
+        self._ck(self._lib.ucfvb_get_face_values(self._h, _dp(L), _dp(R)))
+        return L, R
+
+    def dofs(self) -> np.ndarray:
+        d = np.zeros((self.n_cells, self.K, 4))
+        self._ck(self._lib.ucfvb_get_dofs(self._h, _dp(d)))
+        return d
+
+    def set_phase_timing(self, on: bool = True):
+        self._ck(self._lib.ucfvb_set_phase_timing(self._h, 1 if on else 0))
+
+    def phase_times(self) -> np.ndarray:
+        p = np.zeros(4)
+        self._ck(self._lib.ucfvb_get_phase_times(self._h, _dp(p)))
+        return p
+
+    def launch_count(self) -> int:
+        return int(self._lib.ucfvb_launch_count(self._h))
+
+    def state_device_ptr(self) -> int:
+        p = A.c_dp()
+        self._ck(self._lib.ucfvb_state_device_ptr(self._h, C.byref(p)))
+        return C.cast(p, C.c_void_p).value or 0
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        self._ck(self._lib.ucfvb_stream(self._h, C.byref(s)))
+        return s.value or 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.ucfvb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class ViewHolder:
+    """Wraps a raw (MeshView or StencilView) + keep-alive objects so Solver can take views from elsewhere."""
+
+    def __init__(self, view, keep=None):
+        self.view = view
+        self.keep = keep

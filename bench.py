@@ -1,0 +1,387 @@
+#!/usr/bin/env python3
+"""Benchmark of the hybrid NAD stage pass (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 2]
+
+One bench "step" is one SSP-RK3 time step of BASELINE config 2 (262,144
+jittered triangles, p=2, shock into a sine wave; 3 stages = 786,432
+cell-stage updates): device dt (max_stable_dt) + 3 x (central LSQ + NAD +
+spread/compaction + CWENOZ + MUSCL + fallback + HLLC flux + RK update).
+`value` = cell-stage updates / s with the state resident in HBM (device
+timed with CUDA events on the solver's stream, max over ranks); `e2e` = the
+same metric through the C ABI with the state copied host->device (pinned)
+before and device->host after every step, inside the timed region.
+
+--impl reference times the reference's own CPU code (oracle/_ref: the
+unmodified /root/reference sources compiled here; single-threaded -- it has
+no parallel regions) on the same config, mesh, seed and RK3 driver.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "cell-stage updates/sec (NAD+reconstruct+flux+RK, fp64) at 1/2/4/8 B200; % roofline"
+UNIT = "cell-stage/s"
+
+CONFIGS = {
+    # name: mesh, order, ic, params, opts, bcs, description
+    "1": dict(nx=128, ny=128, rect=(0.0, 0.0, 1.0, 1.0), jitter=0.1, periodic="both", order=2, ic=0,
+              params=[10.0], opts=dict(lambda1p=1e4, cfl=0.5), bcs={},
+              desc="BASELINE config 1: periodic unit square, 128x128x2 jittered tris, p=2, isentropic vortex"),
+    "2": dict(nx=2048, ny=64, rect=(-5.0, 0.0, 5.0, 1.0), jitter=0.1, periodic="y", order=2, ic=1,
+              params=[-4.0, 3.857143, 2.629369, 0.0, 10.33333, 0.2, 5.0], opts=dict(lambda1p=1e3, cfl=0.5),
+              bcs={"left": "outflow", "right": "outflow"},
+              desc="BASELINE config 2: [-5,5]x[0,1], 2048x64x2 jittered tris, p=2, shock into sine wave, "
+                   "transmissive x, periodic y"),
+    "3": dict(nx=2048, ny=2048, rect=(0.0, 0.0, 1.0, 1.0), jitter=0.0, periodic="both", order=3, ic=2,
+              params=[0.5, 0.5, 0.01], opts=dict(lambda1p=1e3, cfl=0.5), bcs={},
+              desc="BASELINE config 3: periodic unit square, 2048x2048x2 tris, p=3, random quadrants + 1% noise"),
+}
+SEED = 1
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for i, n in enumerate(names):
+                if len(r) > 4 + i and r[4 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- roofline model
+def kernel_bytes(K, NQ, NF, MM, MD):
+    """Algorithmic HBM bytes per cell of each kernel: every
+    per-cell array each kernel must read or write once; stencil-neighbour
+    gathers of U assumed to hit in L2 (only the cell's own U is counted)."""
+    Q = NF * NQ
+    central = 32 + 4 * MM + 8 * MM * K + 8 * Q * K + 4 * NF + 1 + 8 + 32 * Q + 32 * K + 1
+    cwenoz = 4 + 32 + 1 + 4 * NF * MD + 16 * NF * MD + 8 * K * K + 32 * K + 8 * Q * K + 4 * NF + 32 * Q
+    muscl = 4 + 32 + 1 + 4 * MM + 16 * MM + 4 * NF + 16 * Q + 8 + 32 * Q
+    flux = 1 + 24 * NF + 1 * NF + (4 + 1) * NF * NQ + 32 * Q + 8 + 32 + 32 * 2 + 32
+    spread = 1 + 1 + 4 * NF + 1
+    return dict(central=central, spread=spread, cwenoz=cwenoz, muscl=muscl, flux=flux)
+
+
+def measured_peak_hbm():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- setup
+def build_case(cfg, n_threads=0):
+    from paper_2510_25906_b200.mesh import Mesh, Stencils
+    c = CONFIGS[cfg]
+    nq = (c["order"] + 2) // 2
+    t0 = time.perf_counter()
+    mesh = Mesh.structured_tri(c["nx"], c["ny"], c["rect"], jitter=c["jitter"], seed=SEED, periodic=c["periodic"],
+                               n_qp=nq)
+    st = Stencils(mesh, c["order"], n_threads=n_threads)
+    u0 = mesh.project_initial(c["ic"], c["params"], seed=SEED, degree=max(2 * c["order"], 2), n_threads=n_threads)
+    return mesh, st, u0, time.perf_counter() - t0
+
+
+def cpu_reference_run(cfg, steps, budget_s=None):
+    """The reference's own CPU path (oracle/_ref) on the same mesh, seed, RK3 driver.
+    Returns (cell-stage/s, steps timed, kind, setup seconds)."""
+    from oracle import ref as R
+    from paper_2510_25906_b200 import _abi as A
+    from paper_2510_25906_b200.solver import make_bcs
+    c = CONFIGS[cfg]
+    nq = (c["order"] + 2) // 2
+    per = {"both": 3, "y": 2, "x": 1, "none": 0}[c["periodic"]]
+    t0 = time.perf_counter()
+    rm = R.RefMesh.structured_tri(c["nx"], c["ny"], c["rect"], jitter=c["jitter"], seed=SEED, periodic=per,
+                                  n_qp=nq)
+    o = A.options_from_dict(order=c["order"], **c["opts"])
+    rs = R.RefSolver(rm, o, make_bcs(c["bcs"]))
+    u0 = rm.project_initial(c["ic"], c["params"], seed=SEED, degree=max(2 * c["order"], 2))
+    rs.set_state(u0)
+    setup = time.perf_counter() - t0
+    done, wall, t = 0, 0.0, 0.0
+    while done < steps:
+        t, w, _ = rs.run_steps(1, A.RK3, t0=t)
+        wall += w
+        done += 1
+        if budget_s is not None and wall >= budget_s:
+            break
+    n = rm.n_cells
+    return n * 3 * done / wall, done, setup, n
+
+
+# ---------------------------------------------------------------- arms
+def run_reference_arm(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle import ref as R
+    cfg = args.config
+    c = CONFIGS[cfg]
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libucfv_ref.so was not built "
+                                                              "(reference sources absent at build time)"}))
+        return
+    # warm-up steps are untimed; each timed step is one full RK3 step of the config,
+    # bounded by a wall budget so the run ends within minutes
+    budget = float(os.environ.get("UCFVB_REF_BUDGET_S", "60"))
+    rate, done, setup, n = cpu_reference_run(cfg, max(1, args.steps), budget_s=budget)
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
+        "warmup": 0, "ms_per_step": 1e3 * n * 3 / rate, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["desc"], "cells": n, "order": c["order"], "integrator": "SSP-RK3",
+                   "timed_steps": done, "requested_steps": args.steps, "setup_s": round(setup, 3)},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"{done} RK3 steps of config {cfg} ({n} cells) through the unmodified reference "
+                                   f"Solver::compute_residual (single-threaded; host has {cores} cores)"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_b200_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2510_25906_b200 import _abi as A
+    from paper_2510_25906_b200.solver import Solver, make_bcs
+
+    cfg = args.config
+    c = CONFIGS[cfg]
+    mesh, st, u0, setup_s = build_case(cfg)
+    opts = A.options_from_dict(order=c["order"], mode="hybrid", **c["opts"])
+    solver = Solver(mesh, opts, make_bcs(c["bcs"]), stencils=st, device=local)
+    n = solver.n_cells
+    stream = torch.cuda.ExternalStream(solver.stream(), device=local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value leg: state resident in HBM, K graph-replayed RK3 steps
+    solver.state = u0
+    solver.run_steps(args.warmup, A.RK3)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        t_final, _ = solver.run_steps(args.steps, A.RK3, t0=0.0)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
+    launches = solver.launch_count()
+    total_units = n * 3 * args.steps * world
+    value = total_units / (ms * 1e-3)
+
+    # census of the timed run (class mix feeds the roofline bytes)
+    solver.state = u0
+    _, census = solver.run_steps(min(args.steps, 20), A.RK3, census=True)
+    mix = census.sum(0) / census.sum()
+
+    # ---- per-kernel durations (events between kernel groups, un-graphed stages)
+    solver.state = u0
+    solver.run_steps(2, A.RK3)
+    solver.set_phase_timing(True)
+    p0 = solver.phase_times().copy()
+    n_phase_steps = 5
+    solver.run_steps(n_phase_steps, A.RK3)
+    torch.cuda.synchronize()
+    phases = (solver.phase_times() - p0) / (3 * n_phase_steps)  # seconds per stage
+    solver.set_phase_timing(False)
+
+    # ---- e2e leg: host state in pinned memory, H2D + step + D2H per step
+    host_u = torch.from_numpy(u0.copy()).pin_memory()
+    host_out = torch.empty_like(host_u).pin_memory()
+    lib = A.load_library()
+    import ctypes as C
+    hp = C.cast(host_u.data_ptr(), A.c_dp)
+    op = C.cast(host_out.data_ptr(), A.c_dp)
+    t_dev = C.c_double()
+    e2e_steps = args.steps
+    for _ in range(max(1, args.warmup)):
+        lib.ucfvb_set_state(solver._h, hp)
+        lib.ucfvb_run_steps(solver._h, 1, A.RK3, 0.0, float("inf"), C.byref(t_dev), None)
+        lib.ucfvb_get_state(solver._h, op)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        rc = lib.ucfvb_set_state(solver._h, hp)
+        rc |= lib.ucfvb_run_steps(solver._h, 1, A.RK3, 0.0, float("inf"), C.byref(t_dev), None)
+        rc |= lib.ucfvb_get_state(solver._h, op)
+        if rc:
+            raise RuntimeError(lib.ucfvb_last_error(solver._h).decode())
+        host_u.copy_(host_out)  # the next step starts from this step's result
+    e1.record(stream)
+    e1.synchronize()
+    wall_e2e = time.perf_counter() - w0
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1e3 * wall_e2e))
+    e2e_value = n * 3 * e2e_steps * world / (e2e_ms * 1e-3)
+
+    # ---- roofline of the dominant kernel
+    H = solver
+    K, NQ = st.view.K, st.view.n_qp
+    NF = 3
+    sd = st.numpy()
+    MM = int(np.max(np.diff(sd["central_ptr"]))) - 1
+    MD = int(np.max(np.diff(sd["dir_member_ptr"]))) - 1
+    kb = kernel_bytes(K, NQ, NF, MM, MD)
+    names = ["central (reconstruct)", "spread+compaction (detect)", "cwenoz+muscl (weights)", "flux+RK"]
+    phase_bytes = [kb["central"] * n, kb["spread"] * n,
+                   (kb["cwenoz"] * mix[1] + kb["muscl"] * mix[2]) * n, kb["flux"] * n]
+    dom = int(np.argmax(phases))
+    peak, peak_kind = measured_peak_hbm()
+    achieved = phase_bytes[dom] / phases[dom] / 1e9
+    stage_bytes = sum(phase_bytes)
+    stage_achieved = stage_bytes / phases.sum() / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(names[dom].split()[0])
+        except Exception:
+            traffic = None
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ref as R
+            if R.available():
+                rate, done, rsetup, _ = cpu_reference_run(cfg, 50, budget_s=float(os.environ.get("UCFVB_CPU_S", "12")))
+                cpu_baseline = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
+                                "sample": f"{done} RK3 steps of config {cfg} ({n} cells), unmodified reference "
+                                          f"sources (oracle/_ref), 1 thread (the reference has no parallel regions);"
+                                          f" setup {rsetup:.1f}s excluded; host has {os.cpu_count()} cores"}
+        except Exception as e:  # pragma: no cover
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": c["desc"], "cells": n, "order": c["order"], "K": K, "M": MM,
+                       "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (per-cell operator data %.0f MB)" % (
+                           (kb["central"] + kb["cwenoz"] + kb["flux"]) * n / 1e6),
+                       "class_mix_first_stage": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
+                                                 "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
+                       "setup_s": round(setup_s, 3)},
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 32),
+                    "d2h_bytes_per_step": int(n * 32)},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic,
+                         "bytes_per_cell": {k: int(v) for k, v in kb.items()},
+                         "stage_achieved": stage_achieved, "stage_frac": stage_achieved / peak,
+                         "phase_us": [round(1e6 * p, 2) for p in phases]},
+            "cpu_baseline": cpu_baseline,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

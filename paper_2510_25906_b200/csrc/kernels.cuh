@@ -112,112 +112,154 @@ __device__ __forceinline__ void record_error(int* err, int face, const int* step
 }
 
 // ---------------------------------------------------------------------------
+// Reconstruction kernels map FOUR lanes to one cell, lane v = lane & 3 owning
+// conserved variable v (the reference solves the four variables with the same
+// operator, reconstruct.cpp:9-28). Per-cell operator loads are broadcast to
+// the four lanes (8 cells x 8 B = 64 B per warp load in the 32-cell chunk
+// layout), face-point stores of a cell's double4 are one 32 B sector, and
+// each lane keeps only its variable's accumulators in registers.
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ double grp_get(double x, int j) {
+  return __shfl_sync(kFull, x, ((threadIdx.x & 31) & ~3) | j);
+}
+__device__ __forceinline__ bool grp_any(bool b) {
+  unsigned x = b ? 1u : 0u;
+  x |= __shfl_xor_sync(kFull, x, 1);
+  x |= __shfl_xor_sync(kFull, x, 2);
+  return x != 0;
+}
+__device__ __forceinline__ int grp_max(int s) {
+  s = max(s, __shfl_xor_sync(kFull, s, 1));
+  s = max(s, __shfl_xor_sync(kFull, s, 2));
+  return s;
+}
+
+// neighbourhood bounds of this lane's variable over {c} U face neighbours
+// (solver.cpp:120-129, 207-211)
+template <int NF>
+__device__ __forceinline__ void var_bounds(const Layout& L, const double* __restrict__ Ud, int c, int v, double u0,
+                                           double& lo, double& hi) {
+  lo = u0;
+  hi = u0;
+#pragma unroll
+  for (int j = 0; j < NF; ++j) {
+    const int nb = __ldg(L.nbr + aos(c, j, NF));
+    if (nb >= 0) {
+      const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
+      lo = smin(lo, x);
+      hi = smax(hi, x);
+    }
+  }
+}
+
+// fallback_check (solver.cpp:229-264) of a reconstructed cell, group-wide:
+// positivity of every face point (needs all four variables: shuffles) and the
+// relaxed DMP of rho (lane 0) and E (lane 3) against delta_m.
+template <int Q>
+__device__ __forceinline__ bool group_demote(const Physics& ph, int v, double lo, double hi, const double* vals,
+                                             int nq_cell) {
+  double dm, dw;
+  compute_margins(ph.mp, hi - lo, dm, dw);
+  bool bad = false;
+#pragma unroll
+  for (int lq = 0; lq < Q; ++lq) {
+    if (lq < nq_cell) {
+      double s[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) s[j] = grp_get(vals[lq], j);
+      bad |= !is_physical(s, ph.gamma);
+      if (v == 0 || v == 3) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
+    }
+  }
+  return grp_any(bad);
+}
+
+// ---------------------------------------------------------------------------
 // k_central: solve_dofs (reconstruct.cpp:9-28) with the m-loop outermost (each
-// accumulator still sums in m order), evaluate_cell (solver.cpp:76-89),
-// classify_cells raw severity (solver.cpp:113-149) and the fallback pre-check
-// a Linear cell needs (solver.cpp:229-264).
-template <int K, int NQ, int NF>
+// accumulator still sums in m order), evaluate_cell (solver.cpp:76-89), the
+// raw NAD severity (classify_cells, solver.cpp:113-149) and the fallback
+// pre-check a cell that ends Linear needs (solver.cpp:229-264).
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratch S, const double4* __restrict__ U,
                                                     int flags) {
   constexpr int Q = NF * NQ;
-  const int c = blockIdx.x * kBlock + threadIdx.x;
-  if (c >= L.n) return;
+  const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
+  const int g = blockIdx.x * kBlock + threadIdx.x;
+  const int v = g & 3;
+  const int c0 = g >> 2;
   if (*(volatile int*)S.err) return;
-  const d4 u0 = ld4(&U[c]);
-  double acc[K][NV];
+  const bool live = c0 < L.n;
+  const int c = live ? c0 : L.n - 1;  // dead groups shadow a real cell so the group shuffles stay uniform
+  const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
+  double acc[K];
 #pragma unroll
-  for (int k = 0; k < K; ++k)
-#pragma unroll
-    for (int v = 0; v < NV; ++v) acc[k][v] = 0.0;
-
-  const int MM = L.MM;
+  for (int k = 0; k < K; ++k) acc[k] = 0.0;
+  const int MM = MMT ? MMT : L.MM;
   const int* ip = L.st_idx + aos(c, 0, MM);
   const double* pp = L.pinv + aos(c, 0, MM * K);
-#pragma unroll 2
+#pragma unroll
   for (int m = 0; m < MM; ++m) {
     const int nb = __ldg(ip + m * 32);
-    const d4 um = ld4(&U[nb]);
-    double d[NV];
+    const double d = __ldg(Ud + 4 * static_cast<size_t>(nb) + v) - u0;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) d[v] = um.v[v] - u0.v[v];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const double w = __ldg(pp + (m * K + k) * 32);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) acc[k][v] += w * d[v];
-    }
+    for (int k = 0; k < K; ++k) acc[k] += __ldg(pp + (m * K + k) * 32) * d;
   }
-  if (flags & FL_DOFS) {
+  double* dofs = reinterpret_cast<double*>(S.dofs);
+  if ((flags & FL_DOFS) && live) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) st4(&S.dofs[aos(c, k, K)], acc[k]);
+    for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = acc[k];
   }
   if (!(flags & FL_EVAL)) return;
-
-  const int nf = L.nfc[c];
+  const int nf = UNI ? NF : L.nfc[c];
   const bool detect = (flags & (FL_NAD | FL_PRECHECK)) != 0;
-  // neighbourhood bounds of rho and E (solver.cpp:120-129)
-  double lo0 = u0.v[0], hi0 = u0.v[0], lo3 = u0.v[3], hi3 = u0.v[3];
-  if (detect) {
-#pragma unroll
-    for (int j = 0; j < NF; ++j) {
-      const int nb = __ldg(L.nbr + aos(c, j, NF));
-      if (nb >= 0) {
-        const double r = __ldg(&U[nb].x), e = __ldg(&U[nb].w);
-        lo0 = smin(lo0, r);
-        hi0 = smax(hi0, r);
-        lo3 = smin(lo3, e);
-        hi3 = smax(hi3, e);
-      }
-    }
-  }
-  const double du0 = hi0 - lo0, du3 = hi3 - lo3;
-  double dm0, dw0, dm3, dw3;
-  compute_margins(ph.mp, du0, dm0, dw0);
-  compute_margins(ph.mp, du3, dm3, dw3);
-  double v0 = -1e300, v3 = -1e300;
+  double lo = u0, hi = u0;
+  if (detect) var_bounds<NF>(L, Ud, c, v, u0, lo, hi);
+  const double du = hi - lo;
+  double dm, dw;
+  compute_margins(ph.mp, du, dm, dw);
+  double vmax = -1e300;
   bool bad = false;
   const double* fp = L.phi + aos(c, 0, Q * K);
+  double* fv = reinterpret_cast<double*>(S.fv);
 #pragma unroll
   for (int lq = 0; lq < Q; ++lq) {
     if (lq < nf * NQ) {
-      double val[NV] = {u0.v[0], u0.v[1], u0.v[2], u0.v[3]};
+      double val = u0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const double p = __ldg(fp + (lq * K + k) * 32);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) val[v] += acc[k][v] * p;
-      }
-      st4(&S.fv[aos(c, lq, Q)], val);
+      for (int k = 0; k < K; ++k) val += acc[k] * __ldg(fp + (lq * K + k) * 32);
+      if (live) fv[4 * aos(c, lq, Q) + v] = val;
       if (detect) {
-        const double x0 = smax(lo0 - val[0], val[0] - hi0);
-        const double x3 = smax(lo3 - val[3], val[3] - hi3);
-        v0 = smax(v0, x0);
-        v3 = smax(v3, x3);
-        bad |= (x0 > dm0) || (x3 > dm3) || !is_physical(val, ph.gamma);
+        double s[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) s[j] = grp_get(val, j);
+        bad |= !is_physical(s, ph.gamma);
+        const double x = smax(lo - val, val - hi);
+        vmax = smax(vmax, x);
+        if (v == 0 || v == 3) bad |= x > dm;
       }
     }
   }
   if (!detect) return;
   int sev = 0;
   bool tie = false;
-  if (flags & FL_NAD) {
+  if ((flags & FL_NAD) && (v == 0 || v == 3)) {
     const double thr = L.deact_thr[c];
-    if (!(du0 < thr)) {
-      sev = violation_severity(v0, dm0, dw0);
-      const double sc = smax(smax(fabs(u0.v[0]), du0), 1e-300);
-      tie |= fabs(v0 - dm0) <= 1e-12 * smax(sc, fabs(dm0)) || fabs(v0 - dw0) <= 1e-12 * smax(sc, fabs(dw0));
+    if (!(du < thr)) {  // deactivate_smooth (detector.cpp:32-35)
+      sev = violation_severity(vmax, dm, dw);
+      const double sc = smax(smax(fabs(u0), du), 1e-300);
+      tie = fabs(vmax - dm) <= 1e-12 * smax(sc, fabs(dm)) || fabs(vmax - dw) <= 1e-12 * smax(sc, fabs(dw));
     }
-    if (sev < 2 && !(du3 < thr)) {
-      const int s3 = violation_severity(v3, dm3, dw3);
-      sev = sev < s3 ? s3 : sev;
-      const double sc = smax(smax(fabs(u0.v[3]), du3), 1e-300);
-      tie |= fabs(v3 - dm3) <= 1e-12 * smax(sc, fabs(dm3)) || fabs(v3 - dw3) <= 1e-12 * smax(sc, fabs(dw3));
-    }
-    if (thr > 0.0) tie |= fabs(du0 - thr) <= 1e-12 * thr || fabs(du3 - thr) <= 1e-12 * thr;
-    const unsigned tm = __ballot_sync(__activemask(), tie);
+    if (thr > 0.0) tie |= fabs(du - thr) <= 1e-12 * thr;
+  }
+  sev = grp_max(sev);
+  bad = grp_any(bad);
+  tie = grp_any(tie);
+  if (flags & FL_NAD) {
+    const unsigned tm = __ballot_sync(kFull, tie && v == 0 && live);
     if (tm && (threadIdx.x & 31) == __ffs(tm) - 1) atomicAdd(S.ties, static_cast<unsigned long long>(__popc(tm)));
   }
-  S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
+  if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -225,7 +267,7 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
 // (detector.cpp:37-53 reads `in` only, so push == pull); Linear cells whose
 // pre-check failed become FirstOrder (fallback_check); the troubled classes
 // are compacted into lists with one atomic per warp (ballot + popc).
-template <int NQ, int NF>
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const double4* __restrict__ U, int flags,
                                                    int detect) {
   constexpr int Q = NF * NQ;
@@ -250,428 +292,346 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
     if (lab == 0 && (r & 4)) lab = 3;
     if (lab == 3) {
       const d4 u0 = ld4(&U[c]);
-      const int nf = L.nfc[c];
+      const int nf = UNI ? NF : L.nfc[c];
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq)
         if (lq < nf * NQ) st4(&S.fv[aos(c, lq, Q)], u0);
+      if (flags & FL_TAPS) {
+        const double z[NV] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int k = 0; k < K; ++k) st4(&S.dofs[aos(c, k, K)], z);
+      }
     }
     S.labels[c] = static_cast<uint8_t>(lab);
   }
-  const unsigned full = 0xffffffffu;
-  const unsigned mc = __ballot_sync(full, lab == 1);
-  const unsigned mm = __ballot_sync(full, lab == 2);
+  const unsigned mc = __ballot_sync(kFull, lab == 1);
+  const unsigned mm = __ballot_sync(kFull, lab == 2);
   const unsigned lt = (1u << lane) - 1u;
   if (mc) {
     int base = 0;
     if (lane == __ffs(mc) - 1) base = atomicAdd(&S.counts[0], __popc(mc));
-    base = __shfl_sync(full, base, __ffs(mc) - 1);
+    base = __shfl_sync(kFull, base, __ffs(mc) - 1);
     if (lab == 1) S.list_c[base + __popc(mc & lt)] = c;
   }
   if (mm) {
     int base = 0;
     if (lane == __ffs(mm) - 1) base = atomicAdd(&S.counts[1], __popc(mm));
-    base = __shfl_sync(full, base, __ffs(mm) - 1);
+    base = __shfl_sync(kFull, base, __ffs(mm) - 1);
     if (lab == 2) S.list_m[base + __popc(mm & lt)] = c;
   }
 }
 
-// fallback_check epilogue for a reconstructed (CWENOZ/MUSCL) cell: returns
-// true when the cell must drop to first order (solver.cpp:229-264).
-template <int NQ, int NF>
-__device__ __forceinline__ bool fallback_demote(const Layout& L, const Physics& ph, const double4* __restrict__ U,
-                                                int c, const d4& u0, const double (*vals)[NV], int nq_cell) {
-  double lo0 = u0.v[0], hi0 = u0.v[0], lo3 = u0.v[3], hi3 = u0.v[3];
-#pragma unroll
-  for (int j = 0; j < NF; ++j) {
-    const int nb = __ldg(L.nbr + aos(c, j, NF));
-    if (nb >= 0) {
-      const double r = __ldg(&U[nb].x), e = __ldg(&U[nb].w);
-      lo0 = smin(lo0, r);
-      hi0 = smax(hi0, r);
-      lo3 = smin(lo3, e);
-      hi3 = smax(hi3, e);
-    }
-  }
-  double dm0, dw0, dm3, dw3;
-  compute_margins(ph.mp, hi0 - lo0, dm0, dw0);
-  compute_margins(ph.mp, hi3 - lo3, dm3, dw3);
-  bool bad = false;
-#pragma unroll
-  for (int lq = 0; lq < NF * NQ; ++lq) {
-    if (lq < nq_cell) {
-      const double* val = vals[lq];
-      bad |= !is_physical(val, ph.gamma) || smax(lo0 - val[0], val[0] - hi0) > dm0 ||
-             smax(lo3 - val[3], val[3] - hi3) > dm3;
-    }
-  }
-  return bad;
-}
-
 // ---------------------------------------------------------------------------
-// k_cwenoz: one thread per listed cell, all four variables in registers.
-template <int K, int NQ, int NF>
+// k_cwenoz: directional r=1 solves (reconstruct.cpp:43-57), SI via OI, tau,
+// nonlinear weights, blend (cwenoz_blend_scalar reconstruct.cpp:99-150),
+// evaluation and fallback epilogue. The blend is per variable in the
+// reference, so lane v owns variable v end to end.
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_cwenoz(Layout L, Physics ph, Scratch S, const double4* __restrict__ U,
                                                    int flags) {
   constexpr int Q = NF * NQ;
+  constexpr int CPB = kBlock / 4;  // cells per block iteration
+  const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const bool all = (flags & FL_NAD) == 0;  // forced CWENOZ mode: every cell, no list
   const int count = all ? L.n : S.counts[0];
   if (*(volatile int*)S.err) return;
-  for (int i = blockIdx.x * kBlock + threadIdx.x; i < count; i += gridDim.x * kBlock) {
-    const int c = all ? i : S.list_c[i];
-    const d4 u0 = ld4(&U[c]);
-    const int nf = L.nfc[c];
-    // directional r=1 solves (reconstruct.cpp:43-57)
-    double dir[NF][2][NV];
-#pragma unroll
-    for (int s = 0; s < NF; ++s)
-#pragma unroll
-      for (int k = 0; k < 2; ++k)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) dir[s][k][v] = 0.0;
-    const int MD = L.MD;
+  if (!(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
+    if (count > 0 && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&S.err[0], 4);
+    return;
+  }
+  const int v = threadIdx.x & 3;
+  double* dofs = reinterpret_cast<double*>(S.dofs);
+  double* fv = reinterpret_cast<double*>(S.fv);
+  for (int base = blockIdx.x * CPB; base < count; base += gridDim.x * CPB) {
+    const int i = base + (threadIdx.x >> 2);
+    const bool live = i < count;
+    const int c = all ? (live ? i : count - 1) : S.list_c[live ? i : count - 1];
+    const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
+    const int nf = UNI ? NF : L.nfc[c];
+    double dir[NF][2];
+    const int MD = MDT ? MDT : L.MD;
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
+      dir[s][0] = 0.0;
+      dir[s][1] = 0.0;
       if (s < nf) {
+#pragma unroll
         for (int m = 0; m < MD; ++m) {
           const int nb = __ldg(L.dir_idx + aos(c, s * MD + m, NF * MD));
-          const d4 um = ld4(&U[nb]);
-          const double w0 = __ldg(L.pinv_dir + aos(c, (s * MD + m) * 2 + 0, NF * MD * 2));
-          const double w1 = __ldg(L.pinv_dir + aos(c, (s * MD + m) * 2 + 1, NF * MD * 2));
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const double d = um.v[v] - u0.v[v];
-            dir[s][0][v] += w0 * d;
-            dir[s][1][v] += w1 * d;
-          }
+          const double d = __ldg(Ud + 4 * static_cast<size_t>(nb) + v) - u0;
+          dir[s][0] += __ldg(L.pinv_dir + aos(c, (s * MD + m) * 2 + 0, NF * MD * 2)) * d;
+          dir[s][1] += __ldg(L.pinv_dir + aos(c, (s * MD + m) * 2 + 1, NF * MD * 2)) * d;
         }
       }
-    }
-    // cwenoz_blend_scalar (reconstruct.cpp:99-150) for the four variables at once
-    if (!(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
-      atomicOr(&S.err[0], 4);
-      return;
     }
     const int st = nf + 1;
     const double lam0 = 1.0 - 1.0 / ph.lambda1p;
     const double lams = (1.0 - lam0) / (st - 1);
-    double p1[K][NV];
+    double p1[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const d4 a = ld4(&S.dofs[aos(c, k, K)]);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) p1[k][v] = a.v[v];
-    }
+    for (int k = 0; k < K; ++k) p1[k] = dofs[4 * aos(c, k, K) + v];
 #pragma unroll
     for (int s = 0; s < NF; ++s)
       if (s < nf) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          p1[0][v] -= lams * dir[s][0][v];
-          p1[1][v] -= lams * dir[s][1][v];
-        }
+        p1[0] -= lams * dir[s][0];
+        p1[1] -= lams * dir[s][1];
       }
 #pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) p1[k][v] /= lam0;
-    // SI_0 = p1^T OI p1, row then dot (reconstruct.cpp:88-97)
+    for (int k = 0; k < K; ++k) p1[k] /= lam0;
+    // SI_0 = p1^T OI p1, row then dot (smoothness_indicator reconstruct.cpp:88-97)
     const double* oi = L.oi + aos(c, 0, K * K);
-    double si0[NV] = {0.0, 0.0, 0.0, 0.0};
+    double si0 = 0.0;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      double t[NV] = {0.0, 0.0, 0.0, 0.0};
+      double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < K; ++q) {
-        const double o = __ldg(oi + (k * K + q) * 32);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) t[v] += o * p1[q][v];
-      }
-#pragma unroll
-      for (int v = 0; v < NV; ++v) si0[v] += p1[k][v] * t[v];
+      for (int q = 0; q < K; ++q) t += __ldg(oi + (k * K + q) * 32) * p1[q];
+      si0 += p1[k] * t;
     }
-    const double o00 = __ldg(oi + 0 * 32), o01 = __ldg(oi + 1 * 32);
-    const double o10 = __ldg(oi + K * 32), o11 = __ldg(oi + (K + 1) * 32);
-    double tau[NV] = {0.0, 0.0, 0.0, 0.0};
-    double sis[NF][NV];
+    const double o00 = __ldg(oi), o01 = __ldg(oi + 32), o10 = __ldg(oi + K * 32), o11 = __ldg(oi + (K + 1) * 32);
+    double sis[NF];
+    double tau = 0.0;
 #pragma unroll
     for (int s = 0; s < NF; ++s)
       if (s < nf) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double a0 = dir[s][0][v], a1 = dir[s][1][v];
-          sis[s][v] = o00 * a0 * a0 + (o01 + o10) * a0 * a1 + o11 * a1 * a1;
-          tau[v] += fabs(sis[s][v] - si0[v]);
-        }
+        const double a0 = dir[s][0], a1 = dir[s][1];
+        sis[s] = o00 * a0 * a0 + (o01 + o10) * a0 * a1 + o11 * a1 * a1;
+        tau += fabs(sis[s] - si0);
       }
-    double om0[NV], oms[NF][NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      tau[v] /= (st - 1);
-      tau[v] = tau_pow(tau[v], ph.weno_b);
-      om0[v] = lam0 * (1.0 + tau[v] / (ph.weno_eps + si0[v]));
-      double wsum = om0[v];
-#pragma unroll
-      for (int s = 0; s < NF; ++s)
-        if (s < nf) {
-          oms[s][v] = lams * (1.0 + tau[v] / (ph.weno_eps + sis[s][v]));
-          wsum += oms[s][v];
-        }
-      om0[v] /= wsum;
-#pragma unroll
-      for (int s = 0; s < NF; ++s)
-        if (s < nf) oms[s][v] /= wsum;
-    }
-    // blended = omega_0 p1 + sum_s omega_s p_s (zero-padded directional dofs)
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) p1[k][v] = om0[v] * p1[k][v];
+    tau /= (st - 1);
+    tau = tau_pow(tau, ph.weno_b);
+    double om0 = lam0 * (1.0 + tau / (ph.weno_eps + si0));
+    double oms[NF];
+    double wsum = om0;
 #pragma unroll
     for (int s = 0; s < NF; ++s)
       if (s < nf) {
+        oms[s] = lams * (1.0 + tau / (ph.weno_eps + sis[s]));
+        wsum += oms[s];
+      }
+    om0 /= wsum;
 #pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          p1[0][v] += oms[s][v] * dir[s][0][v];
-          p1[1][v] += oms[s][v] * dir[s][1][v];
-        }
+    for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
+#pragma unroll
+    for (int s = 0; s < NF; ++s)
+      if (s < nf) {
+        const double w = oms[s] / wsum;
+        p1[0] += w * dir[s][0];
+        p1[1] += w * dir[s][1];
       }
     // evaluate_cell + fallback epilogue
     const double* fp = L.phi + aos(c, 0, Q * K);
-    double vals[Q][NV];
+    double vals[Q];
 #pragma unroll
     for (int lq = 0; lq < Q; ++lq) {
+      vals[lq] = u0;
       if (lq < nf * NQ) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) vals[lq][v] = u0.v[v];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const double p = __ldg(fp + (lq * K + k) * 32);
-#pragma unroll
-          for (int v = 0; v < NV; ++v) vals[lq][v] += p1[k][v] * p;
-        }
+        for (int k = 0; k < K; ++k) vals[lq] += p1[k] * __ldg(fp + (lq * K + k) * 32);
       }
     }
     bool demote = false;
-    if (flags & FL_FALLBACK) demote = fallback_demote<NQ, NF>(L, ph, U, c, u0, vals, nf * NQ);
+    if (flags & FL_FALLBACK) {
+      double lo, hi;
+      var_bounds<NF>(L, Ud, c, v, u0, lo, hi);
+      demote = group_demote<Q>(ph, v, lo, hi, vals, nf * NQ);
+    }
+    if (live) {
 #pragma unroll
-    for (int lq = 0; lq < Q; ++lq)
-      if (lq < nf * NQ) {
-        if (demote)
-          st4(&S.fv[aos(c, lq, Q)], u0);
-        else
-          st4(&S.fv[aos(c, lq, Q)], vals[lq]);
-      }
-    if (demote) S.labels[c] = 3;
-    if (flags & FL_TAPS) {
+      for (int lq = 0; lq < Q; ++lq)
+        if (lq < nf * NQ) fv[4 * aos(c, lq, Q) + v] = demote ? u0 : vals[lq];
+      if (demote && v == 0) S.labels[c] = 3;
+      if (flags & FL_TAPS) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        if (demote) {
-          const double z[NV] = {0.0, 0.0, 0.0, 0.0};
-          st4(&S.dofs[aos(c, k, K)], z);
-        } else {
-          st4(&S.dofs[aos(c, k, K)], p1[k]);
-        }
+        for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = demote ? 0.0 : p1[k];
       }
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_muscl: r=1 LSQ gradient, BJ (or Venkatakrishnan) limiter per variable,
-// limited evaluation and fallback epilogue.
-template <int K, int NQ, int NF>
+// k_muscl: r=1 LSQ gradient (solve_dofs_linear reconstruct.cpp:30-41), BJ or
+// Venkatakrishnan limiter per variable (reconstruct.cpp:59-86), limited
+// evaluation (solver.cpp:189-221) and fallback epilogue; lane v owns variable v.
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_muscl(Layout L, Physics ph, Scratch S, const double4* __restrict__ U,
                                                   int flags) {
   constexpr int Q = NF * NQ;
+  constexpr int CPB = kBlock / 4;
+  const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const bool all = (flags & FL_NAD) == 0;  // forced MUSCL mode
   const int count = all ? L.n : S.counts[1];
   if (*(volatile int*)S.err) return;
-  for (int i = blockIdx.x * kBlock + threadIdx.x; i < count; i += gridDim.x * kBlock) {
-    const int c = all ? i : S.list_m[i];
-    const d4 u0 = ld4(&U[c]);
-    const int nf = L.nfc[c];
-    double lin[2][NV];
+  const int v = threadIdx.x & 3;
+  double* dofs = reinterpret_cast<double*>(S.dofs);
+  double* fv = reinterpret_cast<double*>(S.fv);
+  const bool venkat = ph.limiter == 1;
+  for (int base = blockIdx.x * CPB; base < count; base += gridDim.x * CPB) {
+    const int i = base + (threadIdx.x >> 2);
+    const bool live = i < count;
+    const int c = all ? (live ? i : count - 1) : S.list_m[live ? i : count - 1];
+    const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
+    const int nf = UNI ? NF : L.nfc[c];
+    double l0 = 0.0, l1 = 0.0;
+    const int MM = MMT ? MMT : L.MM;
 #pragma unroll
-    for (int k = 0; k < 2; ++k)
-#pragma unroll
-      for (int v = 0; v < NV; ++v) lin[k][v] = 0.0;
-    const int MM = L.MM;
-#pragma unroll 2
     for (int m = 0; m < MM; ++m) {
       const int nb = __ldg(L.st_idx + aos(c, m, MM));
-      const d4 um = ld4(&U[nb]);
-      const double w0 = __ldg(L.pinv_lin + aos(c, m * 2 + 0, MM * 2));
-      const double w1 = __ldg(L.pinv_lin + aos(c, m * 2 + 1, MM * 2));
-#pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const double d = um.v[v] - u0.v[v];
-        lin[0][v] += w0 * d;
-        lin[1][v] += w1 * d;
-      }
+      const double d = __ldg(Ud + 4 * static_cast<size_t>(nb) + v) - u0;
+      l0 += __ldg(L.pinv_lin + aos(c, m * 2 + 0, MM * 2)) * d;
+      l1 += __ldg(L.pinv_lin + aos(c, m * 2 + 1, MM * 2)) * d;
     }
-    // neighbourhood bounds of all four variables (solver.cpp:207-211)
-    double lo[NV], hi[NV];
-#pragma unroll
-    for (int v = 0; v < NV; ++v) lo[v] = hi[v] = u0.v[v];
-#pragma unroll
-    for (int j = 0; j < NF; ++j) {
-      const int nb = __ldg(L.nbr + aos(c, j, NF));
-      if (nb >= 0) {
-        const d4 un = ld4(&U[nb]);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          lo[v] = smin(lo[v], un.v[v]);
-          hi[v] = smax(hi[v], un.v[v]);
-        }
-      }
-    }
+    double lo, hi;
+    var_bounds<NF>(L, Ud, c, v, u0, lo, hi);
     const double* fp = L.phi + aos(c, 0, Q * K);
     double p0s[Q], p1s[Q];
-    double theta[NV] = {1.0, 1.0, 1.0, 1.0};
-    const bool venkat = ph.limiter == 1;
+    double theta = 1.0;
     const double eps2 = venkat ? L.eps2[c] : 0.0;
 #pragma unroll
     for (int lq = 0; lq < Q; ++lq) {
+      p0s[lq] = 0.0;
+      p1s[lq] = 0.0;
       if (lq < nf * NQ) {
         p0s[lq] = __ldg(fp + (lq * K + 0) * 32);
         p1s[lq] = __ldg(fp + (lq * K + 1) * 32);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          const double qv = u0.v[v] + lin[0][v] * p0s[lq] + lin[1][v] * p1s[lq];
-          theta[v] = venkat ? venkat_update(theta[v], u0.v[v], lo[v], hi[v], qv, eps2)
-                            : bj_update(theta[v], u0.v[v], lo[v], hi[v], qv);
-        }
+        const double qv = u0 + l0 * p0s[lq] + l1 * p1s[lq];
+        theta = venkat ? venkat_update(theta, u0, lo, hi, qv, eps2) : bj_update(theta, u0, lo, hi, qv);
       }
     }
-    double d0[NV], d1[NV];
+    if (!venkat) theta = smax(theta, 0.0);
+    const double d0 = theta * l0, d1 = theta * l1;
+    double vals[Q];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double th = venkat ? theta[v] : smax(theta[v], 0.0);
-      d0[v] = th * lin[0][v];
-      d1[v] = th * lin[1][v];
+    for (int lq = 0; lq < Q; ++lq) {
+      double o = u0;
+      o += d0 * p0s[lq];
+      o += d1 * p1s[lq];
+      vals[lq] = o;  // dofs k >= 2 are zero: adding 0*phi leaves o unchanged
     }
-    double vals[Q][NV];
-#pragma unroll
-    for (int lq = 0; lq < Q; ++lq)
-      if (lq < nf * NQ) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          double o = u0.v[v];
-          o += d0[v] * p0s[lq];
-          o += d1[v] * p1s[lq];
-          vals[lq][v] = o;  // dofs k >= 2 are zero: adding 0*phi leaves o unchanged
-        }
-      }
     bool demote = false;
-    if (flags & FL_FALLBACK) demote = fallback_demote<NQ, NF>(L, ph, U, c, u0, vals, nf * NQ);
+    if (flags & FL_FALLBACK) {
+      // the fallback DMP uses the rho/E bounds, which lanes 0 and 3 hold already
+      demote = group_demote<Q>(ph, v, lo, hi, vals, nf * NQ);
+    }
+    if (live) {
 #pragma unroll
-    for (int lq = 0; lq < Q; ++lq)
-      if (lq < nf * NQ) {
-        if (demote)
-          st4(&S.fv[aos(c, lq, Q)], u0);
-        else
-          st4(&S.fv[aos(c, lq, Q)], vals[lq]);
-      }
-    if (demote) S.labels[c] = 3;
-    if (flags & FL_TAPS) {
+      for (int lq = 0; lq < Q; ++lq)
+        if (lq < nf * NQ) fv[4 * aos(c, lq, Q) + v] = demote ? u0 : vals[lq];
+      if (demote && v == 0) S.labels[c] = 3;
+      if (flags & FL_TAPS) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        double z[NV] = {0.0, 0.0, 0.0, 0.0};
-        if (!demote && k == 0)
-          st4(&S.dofs[aos(c, k, K)], d0);
-        else if (!demote && k == 1)
-          st4(&S.dofs[aos(c, k, K)], d1);
-        else
-          st4(&S.dofs[aos(c, k, K)], z);
+        for (int k = 0; k < K; ++k)
+          dofs[4 * aos(c, k, K) + v] = demote ? 0.0 : (k == 0 ? d0 : (k == 1 ? d1 : 0.0));
       }
     }
   }
 }
 
 // first-order cells everywhere (SchemeMode::First; evaluate_constant solver.cpp:91-101)
-template <int NQ, int NF>
+template <int NQ, int NF, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_constant(Layout L, Scratch S, const double4* __restrict__ U) {
   constexpr int Q = NF * NQ;
   const int c = blockIdx.x * kBlock + threadIdx.x;
   if (c >= L.n) return;
   const d4 u0 = ld4(&U[c]);
-  const int nf = L.nfc[c];
+  const int nf = UNI ? NF : L.nfc[c];
 #pragma unroll
   for (int lq = 0; lq < Q; ++lq)
     if (lq < nf * NQ) st4(&S.fv[aos(c, lq, Q)], u0);
 }
 
 // ---------------------------------------------------------------------------
-// k_flux: per cell, the integrated flux of each of its faces is recomputed
-// from the two sides' face-point values in the face's canonical (left ->
-// right, primary) orientation, so both owners obtain the bit-identical value
-// the reference stores once in face_flux_; the gather then adds +-flux in the
-// cell's face order and scales by 1/area (solver.cpp:294-311). No atomics, no
-// face_flux_ round trip through HBM. The RK combination is fused.
-template <int NQ, int NF>
+// k_flux: one lane per (cell, face): 32/NF cells per warp. Each lane recomputes
+// the integrated flux of its face from the two sides' face-point values in the
+// face's canonical (left -> right, primary) orientation, so both owners obtain
+// the bit-identical value the reference stores once in face_flux_
+// (solver.cpp:266-292); the cell's lanes then add +-flux in the cell's face
+// order (solver.cpp:294-311) through shuffles -- no atomics, no face_flux_
+// round trip through HBM -- and the group leader applies 1/area and the RK
+// combination.
+template <int NQ, int NF, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_flux(Layout L, Physics ph, Scratch S, const double4* __restrict__ U,
                                                  RkEpilogue rk, int flags) {
   constexpr int Q = NF * NQ;
-  const int c = blockIdx.x * kBlock + threadIdx.x;
+  constexpr int CPW = 32 / NF;  // cells per warp
   const int lane = threadIdx.x & 31;
-  bool live = c < L.n;
+  const int slot = lane / NF;
+  const int j = lane - slot * NF;
+  const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+  const int c0 = warp * CPW + slot;
+  const bool live = slot < CPW && c0 < L.n;
+  const bool leader = live && j == 0;
+  const int c = live ? c0 : L.n - 1;
   if (*(volatile int*)S.err) return;
   if (flags & (FL_CENSUS | FL_STEP_LABELS)) {
-    const int lab = live ? S.labels[c] : -1;
-    if ((flags & FL_STEP_LABELS) && live) S.step_labels[c] = static_cast<uint8_t>(lab);
+    const int lab = leader ? S.labels[c] : -1;
+    if ((flags & FL_STEP_LABELS) && leader) S.step_labels[c] = static_cast<uint8_t>(lab);
     if (flags & FL_CENSUS) {
       unsigned long long* row = S.census + 4 * static_cast<size_t>(*S.step);
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
-        const unsigned m = __ballot_sync(0xffffffffu, lab == l);
+        const unsigned m = __ballot_sync(kFull, lab == l);
         if (m && lane == __ffs(m) - 1) atomicAdd(&row[l], static_cast<unsigned long long>(__popc(m)));
       }
     }
   }
-  if (!live) return;
-  const int nf = L.nfc[c];
-  double acc[NV] = {0.0, 0.0, 0.0, 0.0};
-  const size_t base = static_cast<size_t>(c >> 5) * Q * 32 + lane;
+  const int nf = UNI ? NF : L.nfc[c];
+  double t[NV] = {0.0, 0.0, 0.0, 0.0};
+  if (j < nf) {
+    const double nx = __ldg(L.fgeom + aos(c, j * 3 + 0, NF * 3));
+    const double ny = __ldg(L.fgeom + aos(c, j * 3 + 1, NF * 3));
+    const double len = __ldg(L.fgeom + aos(c, j * 3 + 2, NF * 3));
+    const bool own_left = __ldg(L.fsgn + aos(c, j, NF)) > 0;
+    const size_t base = static_cast<size_t>(c >> 5) * Q * 32 + (c & 31);
+    int slq[NQ], ref[NQ];
 #pragma unroll
-  for (int j = 0; j < NF; ++j) {
-    if (j < nf) {
-      const double nx = __ldg(L.fgeom + aos(c, j * 3 + 0, NF * 3));
-      const double ny = __ldg(L.fgeom + aos(c, j * 3 + 1, NF * 3));
-      const double len = __ldg(L.fgeom + aos(c, j * 3 + 2, NF * 3));
-      const bool own_left = __ldg(L.fsgn + aos(c, j, NF)) > 0;
-      double total[NV] = {0.0, 0.0, 0.0, 0.0};
-      bool ok = true;
+    for (int q = 0; q < NQ; ++q) {
+      slq[q] = __ldg(L.self_lq + aos(c, j * NQ + q, Q));
+      ref[q] = __ldg(L.other_ref + aos(c, j * NQ + q, Q));
+    }
+    d4 own[NQ], oth[NQ];
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int slq = __ldg(L.self_lq + aos(c, j * NQ + q, Q));
-        const int ref = __ldg(L.other_ref + aos(c, j * NQ + q, Q));
-        const d4 own = ld4(&S.fv[base + static_cast<size_t>(slq) * 32]);
-        d4 oth;
-        if (ref >= 0) {
-          oth = ld4(&S.fv[ref]);
-        } else {
-          const BcEntry& bc = ph.bc[-ref - 1];
-          if (bc.kind == 2) {
-            mirror_state(own.v, nx, ny, oth.v);
-          } else if (bc.kind == 3) {
+    for (int q = 0; q < NQ; ++q) {
+      own[q] = ld4(&S.fv[base + static_cast<size_t>(slq[q]) * 32]);
+      // boundary faces read their own slot here and substitute the BC state below
+      oth[q] = ld4(&S.fv[ref[q] >= 0 ? static_cast<size_t>(ref[q]) : base + static_cast<size_t>(slq[q]) * 32]);
+    }
+    double total[NV] = {0.0, 0.0, 0.0, 0.0};
+    bool ok = true;
 #pragma unroll
-            for (int v = 0; v < NV; ++v) oth.v[v] = bc.state[v];
-          } else {
-            oth = own;
-          }
+    for (int q = 0; q < NQ; ++q) {
+      if (ref[q] < 0) {
+        const BcEntry& bc = ph.bc[-ref[q] - 1];
+        if (bc.kind == 2) {
+          mirror_state(own[q].v, nx, ny, oth[q].v);
+        } else if (bc.kind == 3) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v) oth[q].v[v] = bc.state[v];
         }
-        double F[NV];
-        ok &= own_left ? riemann_flux(ph.hll, own.v, oth.v, nx, ny, ph.gamma, F)
-                       : riemann_flux(ph.hll, oth.v, own.v, nx, ny, ph.gamma, F);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) total[v] += ph.qw[q] * F[v];
       }
-      if (!ok) record_error(S.err, __ldg(L.face_id + aos(c, j, NF)), S.step);
-      const double sgn = own_left ? 1.0 : -1.0;
+      double F[NV];
+      ok &= own_left ? riemann_flux(ph.hll, own[q].v, oth[q].v, nx, ny, ph.gamma, F)
+                     : riemann_flux(ph.hll, oth[q].v, own[q].v, nx, ny, ph.gamma, F);
 #pragma unroll
-      for (int v = 0; v < NV; ++v) acc[v] += sgn * (total[v] * len);
+      for (int v = 0; v < NV; ++v) total[v] += ph.qw[q] * F[v];
+    }
+    if (!ok && live) record_error(S.err, __ldg(L.face_id + aos(c, j, NF)), S.step);
+    const double sgn = own_left ? 1.0 : -1.0;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) t[v] = sgn * (total[v] * len);
+  }
+  // owner-ordered gather: acc = ((0 + t_0) + t_1) + t_2 ...
+  double acc[NV] = {0.0, 0.0, 0.0, 0.0};
+  const int g0 = slot * NF;
+#pragma unroll
+  for (int jj = 0; jj < NF; ++jj) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const double x = __shfl_sync(kFull, t[v], min(g0 + jj, 31));
+      if (jj < nf) acc[v] += x;
     }
   }
+  if (!leader) return;
   const double inv_vol = L.inv_vol[c];
   double r[NV];
 #pragma unroll
@@ -686,9 +646,9 @@ __global__ void __launch_bounds__(kBlock) k_flux(Layout L, Physics ph, Scratch S
         const double w = rk.dt_scaled[i] ? rk.coef[i] * dt : rk.coef[i];
         double x[NV];
         if (rk.term[i]) {
-          const d4 t = ld4(&rk.term[i][c]);
+          const d4 tt = ld4(&rk.term[i][c]);
 #pragma unroll
-          for (int v = 0; v < NV; ++v) x[v] = t.v[v];
+          for (int v = 0; v < NV; ++v) x[v] = tt.v[v];
         } else {
 #pragma unroll
           for (int v = 0; v < NV; ++v) x[v] = r[v];

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -34,31 +35,41 @@ struct KernelSet {
   void (*constant)(dim3, cudaStream_t, const Layout&, const Scratch&, const double4*);
   void (*flux)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*,
                const RkEpilogue&, int);
+  int cells_per_flux_block;
 };
 
-template <int K, int NQ, int NF>
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 KernelSet make_set() {
   KernelSet s;
   s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                 int f) { k_central<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+                 int f) { k_central<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
   s.spread = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U, int f, int d) {
-    k_spread<NQ, NF><<<g, kBlock, 0, st>>>(L, S, U, f, d);
+    k_spread<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, S, U, f, d);
   };
   s.cwenoz = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                int f) { k_cwenoz<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+                int f) { k_cwenoz<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
   s.muscl = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-               int f) { k_muscl<K, NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+               int f) { k_muscl<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
   s.constant = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U) {
-    k_constant<NQ, NF><<<g, kBlock, 0, st>>>(L, S, U);
+    k_constant<NQ, NF, UNI><<<g, kBlock, 0, st>>>(L, S, U);
   };
   s.flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-              const RkEpilogue& rk, int f) { k_flux<NQ, NF><<<g, kBlock, 0, st>>>(L, p, S, U, rk, f); };
+              const RkEpilogue& rk, int f) { k_flux<NQ, NF, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, rk, f); };
+  s.cells_per_flux_block = (kBlock / 32) * (32 / NF);
   return s;
 }
 
-static KernelSet pick_kernels(int K, int NQ, int NF) {
-#define UCFVB_CASE(k, q, f) \
-  if (K == k && NQ == q && NF == f) return make_set<k, q, f>();
+// Fast path: uniform face count and the nominal stencil sizes (M = 2K,
+// M_dir = 4; every BASELINE mesh) with fully unrolled gathers; anything else
+// (mixed tri/quad meshes, rank-retry stencils) runs the generic instantiation.
+static KernelSet pick_kernels(int K, int NQ, int NF, int MM, int MD, bool uniform) {
+  const char* force = std::getenv("UCFVB_FORCE_GENERIC");
+  const bool fast = uniform && MM == 2 * K && MD == 4 && !(force && force[0] == '1');
+#define UCFVB_CASE(k, q, f)                               \
+  if (K == k && NQ == q && NF == f) {                     \
+    if (fast) return make_set<k, q, f, 2 * k, 4, true>(); \
+    return make_set<k, q, f, 0, 0, false>();              \
+  }
   UCFVB_CASE(2, 1, 3) UCFVB_CASE(2, 1, 4)
   UCFVB_CASE(5, 2, 3) UCFVB_CASE(5, 2, 4)
   UCFVB_CASE(9, 2, 3) UCFVB_CASE(9, 2, 4)
@@ -124,9 +135,11 @@ struct GpuSolver::Impl {
   std::string last_error;
 
   dim3 grid_cells() const { return dim3((L.n + kBlock - 1) / kBlock); }
+  // four lanes per cell (reconstruction kernels)
+  dim3 grid_cells4() const { return dim3((4 * L.n + kBlock - 1) / kBlock); }
   dim3 grid_list() const {
-    const int want = (L.n + kBlock - 1) / kBlock;
-    return dim3(std::max(1, std::min(want, n_sm * 8)));
+    const int want = (4 * L.n + kBlock - 1) / kBlock;
+    return dim3(std::max(1, std::min(want, n_sm * 16)));
   }
 
   void record(int i) {
@@ -143,7 +156,7 @@ struct GpuSolver::Impl {
       const bool detect = first || opt.detect_every_stage;
       CK(cudaMemsetAsync(S.counts, 0, 2 * sizeof(int), stream));
       if (detect) CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream));
-      ks.central(grid_cells(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
+      ks.central(grid_cells4(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
       record(1);
       ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
       record(2);
@@ -151,20 +164,20 @@ struct GpuSolver::Impl {
       ks.muscl(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
       nl += 4;
     } else if (mode == UCFVB_LINEAR) {
-      ks.central(grid_cells(), stream, L, ph, S, U, FL_EVAL | (taps ? FL_DOFS : 0));
+      ks.central(grid_cells4(), stream, L, ph, S, U, FL_EVAL | (taps ? FL_DOFS : 0));
       record(1);
       record(2);
       nl += 1;
     } else if (mode == UCFVB_CWENOZ) {
-      ks.central(grid_cells(), stream, L, ph, S, U, FL_DOFS);
+      ks.central(grid_cells4(), stream, L, ph, S, U, FL_DOFS);
       record(1);
       record(2);
-      ks.cwenoz(grid_cells(), stream, L, ph, S, U, taps);
+      ks.cwenoz(grid_cells4(), stream, L, ph, S, U, taps);
       nl += 2;
     } else if (mode == UCFVB_MUSCL) {
       record(1);
       record(2);
-      ks.muscl(grid_cells(), stream, L, ph, S, U, taps);
+      ks.muscl(grid_cells4(), stream, L, ph, S, U, taps);
       nl += 1;
     } else {
       record(1);
@@ -175,9 +188,10 @@ struct GpuSolver::Impl {
     record(3);
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
-    ks.flux(grid_cells(), stream, L, ph, S, U, rk, ff);
+    ks.flux(dim3((L.n + ks.cells_per_flux_block - 1) / ks.cells_per_flux_block), stream, L, ph, S, U, rk, ff);
     record(4);
     CK(cudaGetLastError());
+    accumulate_phases();
     return nl + 1;
   }
 
@@ -279,7 +293,7 @@ struct GpuSolver::Impl {
     if (g) return g;
     cudaGraph_t gr;
     CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-    const int64_t nl = launch_step(rk, with_dt, ubuf[parity], ubuf[parity ^ 1], with_dt);
+    const int64_t nl = launch_step(rk, with_dt, ubuf[parity], ubuf[parity ^ 1], /*census=*/false);
     CK(cudaStreamEndCapture(stream, &gr));
     CK(cudaGraphInstantiate(&g, gr, 0));
     CK(cudaGraphDestroy(gr));
@@ -372,7 +386,9 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
 
   I.host = build_layout(m, s, o, 0);
   const HostLayout& H = I.host;
-  I.ks = pick_kernels(H.K, H.NQ, H.NF);
+  bool uniform = true;
+  for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
+  I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
   auto& own = I.owned;
   Layout& L = I.L;
   L.n = H.n;
@@ -532,7 +548,6 @@ void GpuSolver::compute_residual(const double* u, double t, double* out) {
   e.rhs_out = I.rhs;
   e.dt = &I.ds->dt;
   I.launches = I.launch_stage(in, I.stage_is_first, e, false);
-  I.accumulate_phases();
   I.stage_is_first = false;
   int k, f, c;
   if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);

@@ -17,9 +17,10 @@
 //               epilogue on the CWENOZ list (solver.cpp:167-188, reconstruct.cpp:43-150)
 //   k_muscl     r=1 solve + BJ/Venkat limiter + eval + fallback epilogue on the
 //               MUSCL list (solver.cpp:189-221, reconstruct.cpp:30-86)
-//   k_flux      per-cell HLLC/HLL at every face Gauss point, owner-ordered
-//               face-to-cell gather (no atomics) and the RK stage update
-//               (solver.cpp:266-314, time_integrator.cpp:31-38,70-73)
+//   k_face_flux HLLC/HLL at every face Gauss point, integrated face flux
+//               (solver.cpp:266-292)
+//   k_gather_rk owner-ordered face-to-cell gather (no atomics) fused with the
+//               RK stage update (solver.cpp:294-311, time_integrator.cpp:31-38,70-73)
 //   k_dt        max_stable_dt min-reduction (solver.cpp:103-111) + device-side t/dt
 #pragma once
 
@@ -30,7 +31,7 @@
 namespace ucfvb {
 
 enum : int { FL_DOFS = 1, FL_EVAL = 2, FL_NAD = 4, FL_PRECHECK = 8, FL_TAPS = 16, FL_FALLBACK = 32,
-             FL_CENSUS = 64, FL_STEP_LABELS = 128 };
+             FL_CENSUS = 64, FL_STEP_LABELS = 128, FL_CHUNKS = 256 };
 
 constexpr int kMaxPatches = 16;
 constexpr int kBlock = 128;
@@ -48,16 +49,20 @@ struct Layout {
   const int* st_idx;        // E = MM           central member cell ids
   const double* pinv;       // E = MM*K  [m][k]
   const double* phi;        // E = Q*K   [lq][k]
+  const double* phi01;      // E = Q*2   [lq][k<2] (MUSCL needs only the linear basis values)
   const double* pinv_lin;   // E = MM*2  [m][k]
   const int* dir_idx;       // E = NF*MD [s][m] member cell ids
   const double* pinv_dir;   // E = NF*MD*2 [s][m][k]
   const double* oi;         // E = K*K
   const int* nbr;           // E = NF    face neighbour (-1: none)
-  const int* other_ref;     // E = NF*NQ fv index of the other face-point value, or -(1+patch)
-  const uint8_t* self_lq;   // E = NF*NQ own local qp feeding canonical qp q
-  const double* fgeom;      // E = NF*3  canonical normal x, y, length
-  const int8_t* fsgn;       // E = NF    +1: own value is UL, -1: own value is UR
-  const int* face_id;       // E = NF    canonical face id (error reports)
+  const int* dest;          // E = Q     face-point slot (double4 index into fp) of each cell-local qp
+  const int* cface;         // E = NF    (canonical face << 1) | (cell sits on its right / periodic secondary)
+  int n_faces;
+  const double* fnx;        // [n_faces] canonical unit normal (left -> right)
+  const double* fny;
+  const double* flen;       // [n_faces] length
+  const int8_t* fkind;      // [n_faces] 0: two-sided flux face, 1: boundary condition, 2: periodic secondary (skipped)
+  const int8_t* fpatch;     // [n_faces] boundary patch
   const uint8_t* nfc;       // [n] faces per cell
   const double* deact_thr;  // [n] (kappa*h)^n or -inf
   const double* eps2;       // [n] (venkat_kappa*h)^3
@@ -75,14 +80,18 @@ struct Physics {
 };
 
 struct Scratch {
-  double4* fv;       // face-point values [chunk][Q][lane]
+  double4* fp;       // face-point values [face][q][side]: the reference's val_left_/val_right_
+                     // slots (periodic partners' values land in the primary face's right slot)
+  double4* ff;       // integrated flux per face (face_flux_)
   double4* dofs;     // [chunk][K][lane]
   uint8_t* raw;      // raw NAD label | demote-if-linear << 2
   uint8_t* labels;
   uint8_t* step_labels;
   int* list_c;
   int* list_m;
-  int* counts;       // [0] CWENOZ list length, [1] MUSCL list length
+  int* counts;       // [0] CWENOZ list length, [1] MUSCL list length, [2]/[3] chunk-list lengths
+  int2* chunks_c;    // (chunk, lane mask) of 32-cell chunks holding CWENOZ cells
+  int2* chunks_m;    // ... MUSCL cells
   unsigned long long* ties;
   unsigned long long* census;  // base of [steps][4]; row selected by *step
   const int* step;
@@ -221,14 +230,14 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
   double vmax = -1e300;
   bool bad = false;
   const double* fp = L.phi + aos(c, 0, Q * K);
-  double* fv = reinterpret_cast<double*>(S.fv);
+  double* fv = reinterpret_cast<double*>(S.fp);
 #pragma unroll
   for (int lq = 0; lq < Q; ++lq) {
     if (lq < nf * NQ) {
       double val = u0;
 #pragma unroll
       for (int k = 0; k < K; ++k) val += acc[k] * __ldg(fp + (lq * K + k) * 32);
-      if (live) fv[4 * aos(c, lq, Q) + v] = val;
+      if (live) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = val;
       if (detect) {
         double s[NV];
 #pragma unroll
@@ -295,7 +304,7 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
       const int nf = UNI ? NF : L.nfc[c];
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq)
-        if (lq < nf * NQ) st4(&S.fv[aos(c, lq, Q)], u0);
+        if (lq < nf * NQ) st4(&S.fp[__ldg(L.dest + aos(c, lq, Q))], u0);
       if (flags & FL_TAPS) {
         const double z[NV] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -307,6 +316,11 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
   const unsigned mc = __ballot_sync(kFull, lab == 1);
   const unsigned mm = __ballot_sync(kFull, lab == 2);
   const unsigned lt = (1u << lane) - 1u;
+  if (flags & FL_CHUNKS) {  // one entry per 32-cell chunk (this warp) with troubled cells
+    if (lane == 0 && mc) S.chunks_c[atomicAdd(&S.counts[2], 1)] = make_int2(c >> 5, static_cast<int>(mc));
+    if (lane == 0 && mm) S.chunks_m[atomicAdd(&S.counts[3], 1)] = make_int2(c >> 5, static_cast<int>(mm));
+    return;
+  }
   if (mc) {
     int base = 0;
     if (lane == __ffs(mc) - 1) base = atomicAdd(&S.counts[0], __popc(mc));
@@ -341,7 +355,7 @@ __global__ void __launch_bounds__(kBlock) k_cwenoz(Layout L, Physics ph, Scratch
   }
   const int v = threadIdx.x & 3;
   double* dofs = reinterpret_cast<double*>(S.dofs);
-  double* fv = reinterpret_cast<double*>(S.fv);
+  double* fv = reinterpret_cast<double*>(S.fp);
   for (int base = blockIdx.x * CPB; base < count; base += gridDim.x * CPB) {
     const int i = base + (threadIdx.x >> 2);
     const bool live = i < count;
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(kBlock) k_cwenoz(Layout L, Physics ph, Scratch
     if (live) {
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq)
-        if (lq < nf * NQ) fv[4 * aos(c, lq, Q) + v] = demote ? u0 : vals[lq];
+        if (lq < nf * NQ) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
       if (demote && v == 0) S.labels[c] = 3;
       if (flags & FL_TAPS) {
 #pragma unroll
@@ -464,7 +478,7 @@ __global__ void __launch_bounds__(kBlock) k_muscl(Layout L, Physics ph, Scratch 
   if (*(volatile int*)S.err) return;
   const int v = threadIdx.x & 3;
   double* dofs = reinterpret_cast<double*>(S.dofs);
-  double* fv = reinterpret_cast<double*>(S.fv);
+  double* fv = reinterpret_cast<double*>(S.fp);
   const bool venkat = ph.limiter == 1;
   for (int base = blockIdx.x * CPB; base < count; base += gridDim.x * CPB) {
     const int i = base + (threadIdx.x >> 2);
@@ -516,7 +530,7 @@ __global__ void __launch_bounds__(kBlock) k_muscl(Layout L, Physics ph, Scratch 
     if (live) {
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq)
-        if (lq < nf * NQ) fv[4 * aos(c, lq, Q) + v] = demote ? u0 : vals[lq];
+        if (lq < nf * NQ) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
       if (demote && v == 0) S.labels[c] = 3;
       if (flags & FL_TAPS) {
 #pragma unroll
@@ -537,36 +551,104 @@ __global__ void __launch_bounds__(kBlock) k_constant(Layout L, Scratch S, const 
   const int nf = UNI ? NF : L.nfc[c];
 #pragma unroll
   for (int lq = 0; lq < Q; ++lq)
-    if (lq < nf * NQ) st4(&S.fv[aos(c, lq, Q)], u0);
+    if (lq < nf * NQ) st4(&S.fp[__ldg(L.dest + aos(c, lq, Q))], u0);
 }
 
 // ---------------------------------------------------------------------------
-// k_flux: one lane per (cell, face): 32/NF cells per warp. Each lane recomputes
-// the integrated flux of its face from the two sides' face-point values in the
-// face's canonical (left -> right, primary) orientation, so both owners obtain
-// the bit-identical value the reference stores once in face_flux_
-// (solver.cpp:266-292); the cell's lanes then add +-flux in the cell's face
-// order (solver.cpp:294-311) through shuffles -- no atomics, no face_flux_
-// round trip through HBM -- and the group leader applies 1/area and the RK
-// combination.
-template <int NQ, int NF, bool UNI>
-__global__ void __launch_bounds__(kBlock) k_flux(Layout L, Physics ph, Scratch S, const double4* __restrict__ U,
-                                                 RkEpilogue rk, int flags) {
-  constexpr int Q = NF * NQ;
-  constexpr int CPW = 32 / NF;  // cells per warp
+// k_face_flux: assemble_fluxes pass 1 (solver.cpp:266-292). One lane per
+// (face, Gauss point), NQ consecutive lanes per face: UL/UR are read as one
+// contiguous 64 B pair from the face-major fp array, the Riemann flux is
+// weighted, and the face's lanes sum total = (0 + w_0 F_0) + w_1 F_1 ... in q
+// order; face_flux = total * length. Periodic secondaries are skipped (their
+// flux lives on the primary, solver.cpp:272); boundary faces evaluate the
+// patch's BC from UL (solver.cpp:22-34, 283).
+template <int NQ>
+__global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scratch S) {
+  constexpr int FPW = 32 / NQ;  // faces per warp
   const int lane = threadIdx.x & 31;
-  const int slot = lane / NF;
-  const int j = lane - slot * NF;
+  const int fs = lane / NQ;
+  const int q = lane - fs * NQ;
   const int warp = (blockIdx.x * kBlock + threadIdx.x) >> 5;
-  const int c0 = warp * CPW + slot;
-  const bool live = slot < CPW && c0 < L.n;
-  const bool leader = live && j == 0;
+  const int f0 = warp * FPW + fs;
+  const bool in = fs < FPW && f0 < L.n_faces;
+  const int f = in ? f0 : 0;
+  const int err0 = *(volatile int*)S.err;
+  const int kind = in ? L.fkind[f] : 2;
+  double t[NV] = {0.0, 0.0, 0.0, 0.0};
+  if (kind != 2) {
+    const double nx = L.fnx[f], ny = L.fny[f];
+    const d4 UL = ld4(&S.fp[(static_cast<size_t>(f) * NQ + q) * 2 + 0]);
+    d4 UR;
+    if (kind == 0) {
+      UR = ld4(&S.fp[(static_cast<size_t>(f) * NQ + q) * 2 + 1]);
+    } else {
+      const BcEntry& bc = ph.bc[L.fpatch[f]];
+      if (bc.kind == 2) {
+        mirror_state(UL.v, nx, ny, UR.v);
+      } else if (bc.kind == 3) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) UR.v[v] = bc.state[v];
+      } else {
+        UR = UL;
+      }
+    }
+    double F[NV];
+    if (!riemann_flux(ph.hll, UL.v, UR.v, nx, ny, ph.gamma, F) && !err0) record_error(S.err, f, S.step);
+    const double w = ph.qw[q];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) t[v] = w * F[v];
+  }
+  double total[NV] = {0.0, 0.0, 0.0, 0.0};
+  const int g0 = fs * NQ;
+#pragma unroll
+  for (int qq = 0; qq < NQ; ++qq)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) total[v] += __shfl_sync(kFull, t[v], min(g0 + qq, 31));
+  if (kind == 2 || q != 0 || err0) return;
+  const double len = L.flen[f];
+  double o[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) o[v] = total[v] * len;
+  st4(&S.ff[f], o);
+}
+
+// ---------------------------------------------------------------------------
+// k_gather_rk: assemble_fluxes pass 2 (solver.cpp:294-311) fused with the RK
+// stage combination. Four lanes per cell (lane v = variable v): acc = sum over
+// the cell's faces, in the cell's face order, of +-face_flux; residual =
+// -acc * (1/area); out = sum_i coef_i * term_i left to right (combine2,
+// time_integrator.cpp:31-38; final SSPRK(5,4) line :70-73). Owner-ordered:
+// no atomics.
+template <int NF, bool UNI>
+__global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags) {
+  const int g = blockIdx.x * kBlock + threadIdx.x;
+  const int v = g & 3;
+  const int c0 = g >> 2;
+  const int lane = threadIdx.x & 31;
+  const bool live = c0 < L.n;
   const int c = live ? c0 : L.n - 1;
-  if (*(volatile int*)S.err) return;
+  const int err0 = *(volatile int*)S.err;
+  const double* ffd = reinterpret_cast<const double*>(S.ff);
+  double term[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    term[i] = (i < rk.nterms && rk.term[i]) ? __ldg(reinterpret_cast<const double*>(rk.term[i] + c) + v) : 0.0;
+  const double inv_vol = L.inv_vol[c];
+  const int nf = UNI ? NF : L.nfc[c];
+  double acc = 0.0;
+#pragma unroll
+  for (int j = 0; j < NF; ++j) {
+    if (j < nf) {
+      const int e = __ldg(L.cface + aos(c, j, NF));
+      const double x = ffd[4 * static_cast<size_t>(e >> 1) + v];
+      acc += ((e & 1) ? -1.0 : 1.0) * x;
+    }
+  }
   if (flags & (FL_CENSUS | FL_STEP_LABELS)) {
+    const bool leader = live && v == 0;
     const int lab = leader ? S.labels[c] : -1;
-    if ((flags & FL_STEP_LABELS) && leader) S.step_labels[c] = static_cast<uint8_t>(lab);
-    if (flags & FL_CENSUS) {
+    if ((flags & FL_STEP_LABELS) && leader && !err0) S.step_labels[c] = static_cast<uint8_t>(lab);
+    if ((flags & FL_CENSUS) && !err0) {
       unsigned long long* row = S.census + 4 * static_cast<size_t>(*S.step);
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
@@ -575,89 +657,21 @@ __global__ void __launch_bounds__(kBlock) k_flux(Layout L, Physics ph, Scratch S
       }
     }
   }
-  const int nf = UNI ? NF : L.nfc[c];
-  double t[NV] = {0.0, 0.0, 0.0, 0.0};
-  if (j < nf) {
-    const double nx = __ldg(L.fgeom + aos(c, j * 3 + 0, NF * 3));
-    const double ny = __ldg(L.fgeom + aos(c, j * 3 + 1, NF * 3));
-    const double len = __ldg(L.fgeom + aos(c, j * 3 + 2, NF * 3));
-    const bool own_left = __ldg(L.fsgn + aos(c, j, NF)) > 0;
-    const size_t base = static_cast<size_t>(c >> 5) * Q * 32 + (c & 31);
-    int slq[NQ], ref[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      slq[q] = __ldg(L.self_lq + aos(c, j * NQ + q, Q));
-      ref[q] = __ldg(L.other_ref + aos(c, j * NQ + q, Q));
-    }
-    d4 own[NQ], oth[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      own[q] = ld4(&S.fv[base + static_cast<size_t>(slq[q]) * 32]);
-      // boundary faces read their own slot here and substitute the BC state below
-      oth[q] = ld4(&S.fv[ref[q] >= 0 ? static_cast<size_t>(ref[q]) : base + static_cast<size_t>(slq[q]) * 32]);
-    }
-    double total[NV] = {0.0, 0.0, 0.0, 0.0};
-    bool ok = true;
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-      if (ref[q] < 0) {
-        const BcEntry& bc = ph.bc[-ref[q] - 1];
-        if (bc.kind == 2) {
-          mirror_state(own[q].v, nx, ny, oth[q].v);
-        } else if (bc.kind == 3) {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) oth[q].v[v] = bc.state[v];
-        }
-      }
-      double F[NV];
-      ok &= own_left ? riemann_flux(ph.hll, own[q].v, oth[q].v, nx, ny, ph.gamma, F)
-                     : riemann_flux(ph.hll, oth[q].v, own[q].v, nx, ny, ph.gamma, F);
-#pragma unroll
-      for (int v = 0; v < NV; ++v) total[v] += ph.qw[q] * F[v];
-    }
-    if (!ok && live) record_error(S.err, __ldg(L.face_id + aos(c, j, NF)), S.step);
-    const double sgn = own_left ? 1.0 : -1.0;
-#pragma unroll
-    for (int v = 0; v < NV; ++v) t[v] = sgn * (total[v] * len);
-  }
-  // owner-ordered gather: acc = ((0 + t_0) + t_1) + t_2 ...
-  double acc[NV] = {0.0, 0.0, 0.0, 0.0};
-  const int g0 = slot * NF;
-#pragma unroll
-  for (int jj = 0; jj < NF; ++jj) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const double x = __shfl_sync(kFull, t[v], min(g0 + jj, 31));
-      if (jj < nf) acc[v] += x;
-    }
-  }
-  if (!leader) return;
-  const double inv_vol = L.inv_vol[c];
-  double r[NV];
-#pragma unroll
-  for (int v = 0; v < NV; ++v) r[v] = -acc[v] * inv_vol;
-  if (rk.rhs_out) st4(&rk.rhs_out[c], r);
+  if (!live || err0) return;
+  const double r = -acc * inv_vol;
+  if (rk.rhs_out) reinterpret_cast<double*>(rk.rhs_out + c)[v] = r;
   if (rk.out) {
     const double dt = rk.nterms ? *rk.dt : 0.0;
-    double o[NV];
+    double o = 0.0;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       if (i < rk.nterms) {
         const double w = rk.dt_scaled[i] ? rk.coef[i] * dt : rk.coef[i];
-        double x[NV];
-        if (rk.term[i]) {
-          const d4 tt = ld4(&rk.term[i][c]);
-#pragma unroll
-          for (int v = 0; v < NV; ++v) x[v] = tt.v[v];
-        } else {
-#pragma unroll
-          for (int v = 0; v < NV; ++v) x[v] = r[v];
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) o[v] = (i == 0) ? w * x[v] : o[v] + w * x[v];
+        const double x = rk.term[i] ? term[i] : r;
+        o = (i == 0) ? w * x : o + w * x;
       }
     }
-    st4(&rk.out[c], o);
+    reinterpret_cast<double*>(rk.out + c)[v] = o;
   }
 }
 

@@ -83,16 +83,37 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
   L.st_idx.assign(nch * MM * 32, 0);
   L.pinv.assign(nch * MM * K * 32, 0.0);
   L.phi.assign(nch * Q * K * 32, 0.0);
+  L.phi01.assign(nch * Q * 2 * 32, 0.0);
   L.pinv_lin.assign(nch * MM * 2 * 32, 0.0);
   L.dir_idx.assign(nch * NF * MD * 32, 0);
   L.pinv_dir.assign(nch * NF * MD * 2 * 32, 0.0);
   L.oi.assign(nch * K * K * 32, 0.0);
   L.nbr.assign(nch * NF * 32, -1);
-  L.other_ref.assign(nch * NF * NQ * 32, 0);
-  L.self_lq.assign(nch * NF * NQ * 32, 0);
-  L.fgeom.assign(nch * NF * 3 * 32, 0.0);
-  L.fsgn.assign(nch * NF * 32, 1);
-  L.face_id.assign(nch * NF * 32, 0);
+  // pad slots of cells with fewer faces point at a scratch slot past the faces
+  L.dest.assign(nch * Q * 32, static_cast<int32_t>(2 * static_cast<int64_t>(m.n_faces) * NQ));
+  L.cface.assign(nch * NF * 32, 0);
+  L.fnx.assign(m.n_faces, 0.0);
+  L.fny.assign(m.n_faces, 0.0);
+  L.flen.assign(m.n_faces, 0.0);
+  L.fkind.assign(m.n_faces, 0);
+  L.fpatch.assign(m.n_faces, 0);
+  for (int f = 0; f < m.n_faces; ++f) {
+    L.fnx[f] = m.face_normal[2 * f];
+    L.fny[f] = m.face_normal[2 * f + 1];
+    L.flen[f] = m.face_length[f];
+    const int partner = m.face_partner[f];
+    if (m.face_right[f] >= 0) {
+      L.fkind[f] = 0;
+    } else if (partner >= 0) {
+      L.fkind[f] = partner > f ? 0 : 2;  // the primary of a periodic pair carries the flux (solver.cpp:272)
+    } else {
+      const int patch = m.face_patch[f];
+      if (patch < 0 || patch >= 16)
+        throw ApiError(UCFVB_INVALID, "solver: boundary face " + std::to_string(f) + " has no boundary condition");
+      L.fkind[f] = 1;
+      L.fpatch[f] = static_cast<int8_t>(patch);
+    }
+  }
   L.nfc.assign(L.n_pad, 0);
   L.deact_thr.assign(L.n_pad, 0.0);
   L.eps2.assign(L.n_pad, 0.0);
@@ -101,8 +122,9 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
   L.qp_ptr.assign(s.qp_ptr, s.qp_ptr + n + 1);
   L.qp_slot.assign(s.qp_slot, s.qp_slot + s.qp_ptr[n]);
 
-  auto fv_index = [&](int cell, int lq) -> int64_t { return static_cast<int64_t>(aos_index(cell, lq, Q)); };
-  if (static_cast<int64_t>(nch) * Q * 32 >= (int64_t{1} << 31))
+  // face-point slot of (face, q, side) in the face-major fp array (double4 units)
+  auto fp_slot = [&](int f, int q, int side) -> int64_t { return (static_cast<int64_t>(f) * NQ + q) * 2 + side; };
+  if (2 * static_cast<int64_t>(m.n_faces) * NQ + 1 >= (int64_t{1} << 31))
     throw ApiError(UCFVB_UNSUPPORTED, "solver: mesh too large for 32-bit face-point indices");
 
   parallel_for(n, n_threads, [&](int64_t a, int64_t b) {
@@ -138,8 +160,10 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
       if (qc != nf * NQ || s.phi_off[c + 1] - s.phi_off[c] != static_cast<int64_t>(qc) * K)
         throw ApiError(UCFVB_INVALID, "stencil: phi table does not match the cell's faces");
       const double* ph = s.phi + s.phi_off[c];
-      for (int lq = 0; lq < qc; ++lq)
+      for (int lq = 0; lq < qc; ++lq) {
         for (int k = 0; k < K; ++k) L.phi[aos_index(c, lq * K + k, Q * K)] = ph[lq * K + k];
+        for (int k = 0; k < 2; ++k) L.phi01[aos_index(c, lq * 2 + k, Q * 2)] = ph[lq * K + k];
+      }
       // directional stencils
       const int64_t d0 = s.dir_ptr[c];
       const int nd = static_cast<int>(s.dir_ptr[c + 1] - d0);
@@ -160,7 +184,10 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
         }
       }
       for (int e = 0; e < K * K; ++e) L.oi[aos_index(c, e, K * K)] = s.oi[static_cast<int64_t>(c) * K * K + e];
-      // faces: neighbours (face_neighbors mesh.cpp:19-30) and canonical flux orientation
+      // faces: neighbours (face_neighbors mesh.cpp:19-30), where each face-point
+      // value goes (val_left_/val_right_ slot; a periodic secondary writes the
+      // primary's right slot, which is what solver.cpp:280-281 reads) and the
+      // signed canonical face of the owner-ordered gather (solver.cpp:298-307)
       for (int j = 0; j < nf; ++j) {
         const int f = m.cell_faces[m.cell_face_ptr[c] + j];
         const int right = m.face_right[f], left = m.face_left[f], partner = m.face_partner[f];
@@ -170,38 +197,22 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
         else if (partner >= 0)
           nb = m.face_left[partner];
         L.nbr[aos_index(c, j, NF)] = nb;
-        int canon = f;
-        int sgn = 1;
+        int canon = f, neg = 0;
         for (int q = 0; q < NQ; ++q) {
-          int self_lq = j * NQ + q;
-          int64_t other;
+          int64_t slot;
           if (right >= 0) {
-            const int oc = (left == c) ? right : left;
-            other = fv_index(oc, local_face_index(m, oc, f) * NQ + q);
-            sgn = (left == c) ? 1 : -1;
-          } else if (partner >= 0 && partner > f) {  // primary of a periodic pair
-            const int oc = m.face_left[partner];
-            other = fv_index(oc, local_face_index(m, oc, partner) * NQ + m.face_partner_qp[f * NQ + q]);
-          } else if (partner >= 0) {  // secondary: flux lives on the primary (solver.cpp:272, 301-306)
+            slot = fp_slot(f, q, left == c ? 0 : 1);
+            neg = left == c ? 0 : 1;
+          } else if (partner >= 0 && partner < f) {  // periodic secondary
             canon = partner;
-            sgn = -1;
-            const int oc = m.face_left[partner];
-            other = fv_index(oc, local_face_index(m, oc, partner) * NQ + q);
-            self_lq = j * NQ + m.face_partner_qp[partner * NQ + q];
-          } else {
-            const int patch = m.face_patch[f];
-            if (patch < 0 || patch >= 16)
-              throw ApiError(UCFVB_INVALID, "solver: boundary face " + std::to_string(f) + " has no boundary condition");
-            other = -(1 + patch);
+            neg = 1;
+            slot = fp_slot(partner, m.face_partner_qp[f * NQ + q], 1);
+          } else {  // periodic primary or boundary: this cell is the left side
+            slot = fp_slot(f, q, 0);
           }
-          L.other_ref[aos_index(c, j * NQ + q, NF * NQ)] = static_cast<int32_t>(other);
-          L.self_lq[aos_index(c, j * NQ + q, NF * NQ)] = static_cast<uint8_t>(self_lq);
+          L.dest[aos_index(c, j * NQ + q, Q)] = static_cast<int32_t>(slot);
         }
-        L.fgeom[aos_index(c, j * 3 + 0, NF * 3)] = m.face_normal[2 * canon];
-        L.fgeom[aos_index(c, j * 3 + 1, NF * 3)] = m.face_normal[2 * canon + 1];
-        L.fgeom[aos_index(c, j * 3 + 2, NF * 3)] = m.face_length[canon];
-        L.fsgn[aos_index(c, j, NF)] = static_cast<int8_t>(sgn);
-        L.face_id[aos_index(c, j, NF)] = canon;
+        L.cface[aos_index(c, j, NF)] = (canon << 1) | neg;
       }
     }
   });

@@ -19,10 +19,12 @@ struct ApiError : std::runtime_error {
 
 struct HostLayout {
   int n = 0, n_pad = 0, K = 0, NQ = 0, NF = 0, Q = 0, MM = 0, MD = 0;
-  std::vector<int32_t> st_idx, dir_idx, nbr, other_ref, face_id;
-  std::vector<double> pinv, phi, pinv_lin, pinv_dir, oi, fgeom;
-  std::vector<uint8_t> self_lq, nfc;
-  std::vector<int8_t> fsgn;
+  std::vector<int32_t> st_idx, dir_idx, nbr, dest, cface;
+  std::vector<double> pinv, phi, phi01, pinv_lin, pinv_dir, oi;
+  std::vector<uint8_t> nfc;
+  // face arrays (canonical orientation) and the face-major face-point slots
+  std::vector<double> fnx, fny, flen;
+  std::vector<int8_t> fkind, fpatch;
   std::vector<double> deact_thr, eps2, h, inv_vol;
   double qw[4] = {0, 0, 0, 0};
   // reference slot of each cell-local qp, for the val_left_/val_right_ tap

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "kernels_tma.cuh"
 #include "layout.hpp"
 #include "solver.hpp"
 
@@ -33,9 +34,17 @@ struct KernelSet {
   void (*cwenoz)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
   void (*muscl)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
   void (*constant)(dim3, cudaStream_t, const Layout&, const Scratch&, const double4*);
-  void (*flux)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*,
-               const RkEpilogue&, int);
-  int cells_per_flux_block;
+  void (*face_flux)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&);
+  void (*gather)(dim3, cudaStream_t, const Layout&, const Scratch&, const RkEpilogue&, int);
+  int faces_per_flux_block;
+  // TMA-staged persistent central kernel (fast path); grid filled in at create
+  bool central_tma = false;
+  int (*central_tma_setup)(int n_sm) = nullptr;  // returns the persistent grid size
+  int central_tma_grid = 0;
+  // TMA-staged persistent CWENOZ+MUSCL kernel over chunk lists (fast path)
+  void (*troubled)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int) = nullptr;
+  int (*troubled_setup)(int n_sm) = nullptr;
+  int troubled_grid = 0;
 };
 
 template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
@@ -53,9 +62,37 @@ KernelSet make_set() {
   s.constant = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U) {
     k_constant<NQ, NF, UNI><<<g, kBlock, 0, st>>>(L, S, U);
   };
-  s.flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-              const RkEpilogue& rk, int f) { k_flux<NQ, NF, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, rk, f); };
-  s.cells_per_flux_block = (kBlock / 32) * (32 / NF);
+  s.face_flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S) {
+    k_face_flux<NQ><<<g, kBlock, 0, st>>>(L, p, S);
+  };
+  s.gather = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const RkEpilogue& rk, int f) {
+    k_gather_rk<NF, UNI><<<g, kBlock, 0, st>>>(L, S, rk, f);
+  };
+  s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
+  if constexpr (MMT > 0 && UNI) {
+    using St = CentralStage<K, NQ, NF, MMT>;
+    s.central_tma = true;
+    s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+                   int f) { k_central_tma<K, NQ, NF, MMT><<<g, kBlock, St::SMEM, st>>>(L, p, S, U, f); };
+    s.central_tma_setup = [](int n_sm) -> int {
+      CK(cudaFuncSetAttribute(k_central_tma<K, NQ, NF, MMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              St::SMEM));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_central_tma<K, NQ, NF, MMT>, kBlock, St::SMEM));
+      return std::max(1, per_sm) * n_sm;
+    };
+    using Tt = TroubledStage<K, NQ, NF, MMT, MDT>;
+    s.troubled = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
+                    int f) { k_troubled_tma<K, NQ, NF, MMT, MDT><<<g, kBlock, Tt::SMEM, st>>>(L, p, S, U, f); };
+    s.troubled_setup = [](int n_sm) -> int {
+      CK(cudaFuncSetAttribute(k_troubled_tma<K, NQ, NF, MMT, MDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              Tt::SMEM));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_troubled_tma<K, NQ, NF, MMT, MDT>, kBlock,
+                                                       Tt::SMEM));
+      return std::max(1, per_sm) * n_sm;
+    };
+  }
   return s;
 }
 
@@ -137,6 +174,10 @@ struct GpuSolver::Impl {
   dim3 grid_cells() const { return dim3((L.n + kBlock - 1) / kBlock); }
   // four lanes per cell (reconstruction kernels)
   dim3 grid_cells4() const { return dim3((4 * L.n + kBlock - 1) / kBlock); }
+  dim3 grid_central() const {
+    if (ks.central_tma) return dim3(std::min(ks.central_tma_grid, (L.n + 31) / 32));
+    return grid_cells4();
+  }
   dim3 grid_list() const {
     const int want = (4 * L.n + kBlock - 1) / kBlock;
     return dim3(std::max(1, std::min(want, n_sm * 16)));
@@ -154,22 +195,30 @@ struct GpuSolver::Impl {
     record(0);
     if (mode == UCFVB_HYBRID) {
       const bool detect = first || opt.detect_every_stage;
-      CK(cudaMemsetAsync(S.counts, 0, 2 * sizeof(int), stream));
+      CK(cudaMemsetAsync(S.counts, 0, 4 * sizeof(int), stream));
       if (detect) CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream));
-      ks.central(grid_cells4(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
+      ks.central(grid_central(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
       record(1);
-      ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
-      record(2);
-      ks.cwenoz(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
-      ks.muscl(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
-      nl += 4;
+      if (ks.troubled) {
+        ks.spread(grid_cells(), stream, L, S, U, taps | FL_CHUNKS, detect ? 1 : 0);
+        record(2);
+        ks.troubled(dim3(std::min(ks.troubled_grid, (L.n + 31) / 32)), stream, L, ph, S, U,
+                    FL_NAD | FL_FALLBACK | taps);
+        nl += 3;
+      } else {
+        ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
+        record(2);
+        ks.cwenoz(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+        ks.muscl(grid_list(), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+        nl += 4;
+      }
     } else if (mode == UCFVB_LINEAR) {
-      ks.central(grid_cells4(), stream, L, ph, S, U, FL_EVAL | (taps ? FL_DOFS : 0));
+      ks.central(grid_central(), stream, L, ph, S, U, FL_EVAL | (taps ? FL_DOFS : 0));
       record(1);
       record(2);
       nl += 1;
     } else if (mode == UCFVB_CWENOZ) {
-      ks.central(grid_cells4(), stream, L, ph, S, U, FL_DOFS);
+      ks.central(grid_central(), stream, L, ph, S, U, FL_DOFS);
       record(1);
       record(2);
       ks.cwenoz(grid_cells4(), stream, L, ph, S, U, taps);
@@ -188,7 +237,9 @@ struct GpuSolver::Impl {
     record(3);
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
-    ks.flux(dim3((L.n + ks.cells_per_flux_block - 1) / ks.cells_per_flux_block), stream, L, ph, S, U, rk, ff);
+    ks.face_flux(dim3((L.n_faces + ks.faces_per_flux_block - 1) / ks.faces_per_flux_block), stream, L, ph, S);
+    ks.gather(grid_cells4(), stream, L, S, rk, ff);
+    ++nl;
     record(4);
     CK(cudaGetLastError());
     accumulate_phases();
@@ -389,6 +440,8 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   bool uniform = true;
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
   I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
+  if (I.ks.central_tma) I.ks.central_tma_grid = I.ks.central_tma_setup(I.n_sm);
+  if (I.ks.troubled) I.ks.troubled_grid = I.ks.troubled_setup(I.n_sm);
   auto& own = I.owned;
   Layout& L = I.L;
   L.n = H.n;
@@ -397,16 +450,20 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   L.st_idx = dupload(H.st_idx, own);
   L.pinv = dupload(H.pinv, own);
   L.phi = dupload(H.phi, own);
+  L.phi01 = dupload(H.phi01, own);
   L.pinv_lin = dupload(H.pinv_lin, own);
   L.dir_idx = dupload(H.dir_idx, own);
   L.pinv_dir = dupload(H.pinv_dir, own);
   L.oi = dupload(H.oi, own);
   L.nbr = dupload(H.nbr, own);
-  L.other_ref = dupload(H.other_ref, own);
-  L.self_lq = dupload(H.self_lq, own);
-  L.fgeom = dupload(H.fgeom, own);
-  L.fsgn = dupload(H.fsgn, own);
-  L.face_id = dupload(H.face_id, own);
+  L.dest = dupload(H.dest, own);
+  L.cface = dupload(H.cface, own);
+  L.n_faces = H.n_faces;
+  L.fnx = dupload(H.fnx, own);
+  L.fny = dupload(H.fny, own);
+  L.flen = dupload(H.flen, own);
+  L.fkind = dupload(H.fkind, own);
+  L.fpatch = dupload(H.fpatch, own);
   L.nfc = dupload(H.nfc, own);
   L.deact_thr = dupload(H.deact_thr, own);
   L.eps2 = dupload(H.eps2, own);
@@ -424,19 +481,24 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
 
   const size_t nch = static_cast<size_t>(H.n_pad / 32);
   Scratch& S = I.S;
-  S.fv = dalloc<double4>(nch * H.Q * 32, own);
+  const size_t n_fp = 2 * static_cast<size_t>(H.n_faces) * H.NQ + 1;  // + scratch slot for padded qps
+  S.fp = dalloc<double4>(n_fp, own);
+  S.ff = dalloc<double4>(std::max(1, H.n_faces), own);
   S.dofs = dalloc<double4>(nch * H.K * 32, own);
   S.raw = dalloc<uint8_t>(H.n_pad, own);
   S.labels = dalloc<uint8_t>(H.n_pad, own);
   S.step_labels = dalloc<uint8_t>(H.n_pad, own);
   S.list_c = dalloc<int>(H.n, own);
   S.list_m = dalloc<int>(H.n, own);
-  S.counts = dalloc<int>(2, own);
+  S.counts = dalloc<int>(4, own);
+  S.chunks_c = dalloc<int2>(nch, own);
+  S.chunks_m = dalloc<int2>(nch, own);
   S.ties = dalloc<unsigned long long>(1, own);
   S.err = dalloc<int>(4, own);
   I.step_zero = dalloc<int>(1, own);
   CK(cudaMemset(I.step_zero, 0, sizeof(int)));
-  CK(cudaMemset(S.fv, 0, nch * H.Q * 32 * sizeof(double4)));
+  CK(cudaMemset(S.fp, 0, n_fp * sizeof(double4)));
+  CK(cudaMemset(S.ff, 0, std::max(1, H.n_faces) * sizeof(double4)));
   CK(cudaMemset(S.dofs, 0, nch * H.K * 32 * sizeof(double4)));
   CK(cudaMemset(S.ties, 0, sizeof(unsigned long long)));
   CK(cudaMemset(S.raw, 0, H.n_pad));
@@ -644,14 +706,17 @@ int64_t GpuSolver::nad_ties() {
 void GpuSolver::get_face_values(double* left, double* right) {
   Impl& I = *p_;
   const HostLayout& H = I.host;
-  const size_t nch = static_cast<size_t>(H.n_pad / 32);
-  std::vector<double4> fv(nch * H.Q * 32);
-  CK(cudaMemcpyAsync(fv.data(), I.S.fv, fv.size() * sizeof(double4), cudaMemcpyDeviceToHost, I.stream));
+  const int NQ = H.NQ;
+  std::vector<double4> fp(2 * static_cast<size_t>(H.n_faces) * NQ);
+  CK(cudaMemcpyAsync(fp.data(), I.S.fp, fp.size() * sizeof(double4), cudaMemcpyDeviceToHost, I.stream));
   CK(cudaStreamSynchronize(I.stream));
+  // every cell-local qp knows both its reference slot (qp_slot) and where the
+  // device stored it (dest): invert through the cells
   for (int c = 0; c < H.n; ++c)
     for (int64_t q = H.qp_ptr[c]; q < H.qp_ptr[c + 1]; ++q) {
       const int slot = H.qp_slot[q];
-      const double4 v = fv[aos_index(c, static_cast<int>(q - H.qp_ptr[c]), H.Q)];
+      const int lq = static_cast<int>(q - H.qp_ptr[c]);
+      const double4 v = fp[H.dest[aos_index(c, lq, H.Q)]];
       double* dst = ((slot & 1) ? right : left) + 4 * static_cast<int64_t>(slot >> 1);
       dst[0] = v.x;
       dst[1] = v.y;

@@ -26,17 +26,18 @@ struct CentralStage {
   static constexpr uint32_t NBR = round16(NF * 32 * 4);
   static constexpr uint32_t DEST = round16(Q * 32 * 4);
   static constexpr uint32_t BYTES = PINV + PHI + IDX + NBR + DEST;  // one stage
-  static constexpr uint32_t SMEM = 2 * BYTES + 16;           // + 2 mbarriers
 };
 
 // k_central on the fast path: same arithmetic as k_central (kernels.cuh).
-template <int K, int NQ, int NF, int MM>
+// NS shared-memory stages form a ring; chunk it+NS-1 is in flight while chunk
+// it computes (NS = 1: no intra-block overlap, more resident blocks instead).
+template <int K, int NQ, int NF, int MM, int NS>
 __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Scratch S,
                                                         const double4* __restrict__ U, int flags) {
   using St = CentralStage<K, NQ, NF, MM>;
   constexpr int Q = St::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * St::BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NS * St::BYTES);
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const int tid = threadIdx.x;
   const int slot = tid >> 2;  // cell within the chunk
@@ -45,8 +46,7 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
   __shared__ int s_err;
   if (tid == 0) {
     s_err = *(volatile int*)S.err;
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -61,19 +61,21 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
     bulk_g2s(b + St::PINV + St::PHI + St::IDX + St::NBR, L.dest + static_cast<size_t>(chunk) * Q * 32, St::DEST,
              &bar[st]);
   };
-  if (tid == 0 && blockIdx.x < nchunks) issue(blockIdx.x, 0);
+  if (tid == 0)
+    for (int p = 0; p < NS - 1; ++p)
+      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nchunks) issue(blockIdx.x + p * gridDim.x, p);
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool detect = (flags & (FL_NAD | FL_PRECHECK)) != 0;
   int it = 0;
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
-    const int st = it & 1;
-    const int next = chunk + gridDim.x;
-    if (tid == 0 && next < nchunks) {
+    const int st = it % NS;
+    const int ahead = chunk + (NS - 1) * gridDim.x;
+    if (tid == 0 && ahead < nchunks) {
       fence_proxy_async_smem();
-      issue(next, st ^ 1);
+      issue(ahead, (it + NS - 1) % NS);
     }
-    mbar_wait(&bar[st], (it >> 1) & 1);
+    mbar_wait(&bar[st], (it / NS) & 1);
     const unsigned char* b = smem + st * St::BYTES;
     const double* sp = reinterpret_cast<const double*>(b);
     const double* sf = reinterpret_cast<const double*>(b + St::PINV);
@@ -181,7 +183,6 @@ struct TroubledStage {
   static constexpr uint32_t M_NBR = round16(NF * 32 * 4);
   static constexpr uint32_t M_BYTES = M_IDX + M_PLIN + M_PHI + M_NBR;
   static constexpr uint32_t BYTES = C_BYTES > M_BYTES ? C_BYTES : M_BYTES;
-  static constexpr uint32_t SMEM = 2 * BYTES + 16;
 };
 
 // k_troubled_tma: the CWENOZ and MUSCL reconstructions of one stage in one
@@ -190,13 +191,13 @@ struct TroubledStage {
 // the scheme is uniform per block iteration, lanes of cells outside the
 // chunk's mask idle through the (shuffle-synchronous) math and store nothing.
 // Arithmetic is identical to k_cwenoz / k_muscl (kernels.cuh).
-template <int K, int NQ, int NF, int MM, int MD>
+template <int K, int NQ, int NF, int MM, int MD, int NS>
 __global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, Scratch S,
                                                          const double4* __restrict__ U, int flags) {
   using St = TroubledStage<K, NQ, NF, MM, MD>;
   constexpr int Q = St::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * St::BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NS * St::BYTES);
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const int tid = threadIdx.x;
   const int slot = tid >> 2;
@@ -206,8 +207,7 @@ __global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, S
     s_err = *(volatile int*)S.err;
     s_nc = S.counts[2];
     s_nm = S.counts[3];
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -247,23 +247,25 @@ __global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, S
       bulk_g2s(p, L.nbr + ch * NF * 32, St::M_NBR, &bar[st]);
     }
   };
-  if (tid == 0 && static_cast<int>(blockIdx.x) < nitems) issue(blockIdx.x, 0);
+  if (tid == 0)
+    for (int p = 0; p < NS - 1; ++p)
+      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nitems) issue(blockIdx.x + p * gridDim.x, p);
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool venkat = ph.limiter == 1;
   int it = 0;
   for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
-    const int st = it & 1;
-    const int next = i + gridDim.x;
-    if (tid == 0 && next < nitems) {
+    const int st = it % NS;
+    const int ahead = i + (NS - 1) * gridDim.x;
+    if (tid == 0 && ahead < nitems) {
       fence_proxy_async_smem();
-      issue(next, st ^ 1);
+      issue(ahead, (it + NS - 1) % NS);
     }
     const int2 e = item_chunk(i);
     const bool mine = (static_cast<unsigned>(e.y) >> slot) & 1u;
     const int c = e.x * 32 + slot;  // chunks are full-size in the padded layout; cells past n are never in a mask
     const int cc = c < L.n ? c : L.n - 1;
-    mbar_wait(&bar[st], (it >> 1) & 1);
+    mbar_wait(&bar[st], (it / NS) & 1);
     const unsigned char* b = smem + st * St::BYTES;
     const double u0 = __ldg(Ud + 4 * static_cast<size_t>(cc) + v);
     double vals[Q];

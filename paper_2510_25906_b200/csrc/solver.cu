@@ -39,13 +39,46 @@ struct KernelSet {
   int faces_per_flux_block;
   // TMA-staged persistent central kernel (fast path); grid filled in at create
   bool central_tma = false;
-  int (*central_tma_setup)(int n_sm) = nullptr;  // returns the persistent grid size
+  using Launch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
+  void (*central_tma_setup)(int n_sm, int stages, int* grid, Launch* launch) = nullptr;
   int central_tma_grid = 0;
   // TMA-staged persistent CWENOZ+MUSCL kernel over chunk lists (fast path)
-  void (*troubled)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int) = nullptr;
-  int (*troubled_setup)(int n_sm) = nullptr;
+  Launch troubled = nullptr;
+  void (*troubled_setup)(int n_sm, int stages, int* grid, Launch* launch) = nullptr;
   int troubled_grid = 0;
 };
+
+using StageLaunch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
+
+template <typename St>
+constexpr uint32_t tma_smem(int stages) { return stages * St::BYTES + 8 * stages; }
+
+template <int K, int NQ, int NF, int MM, int NS>
+void central_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
+                          const double4* U, int f) {
+  k_central_tma<K, NQ, NF, MM, NS><<<g, kBlock, tma_smem<CentralStage<K, NQ, NF, MM>>(NS), st>>>(L, p, S, U, f);
+}
+
+template <int K, int NQ, int NF, int MM, int MD, int NS>
+void troubled_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
+                           const double4* U, int f) {
+  k_troubled_tma<K, NQ, NF, MM, MD, NS><<<g, kBlock, tma_smem<TroubledStage<K, NQ, NF, MM, MD>>(NS), st>>>(L, p, S, U,
+                                                                                                       f);
+}
+
+// pick the stage count (1..3), raise the dynamic smem limit, size the persistent grid
+template <typename St, typename Kfn>
+void tma_setup(int n_sm, int stages, int* grid, StageLaunch* launch, StageLaunch l1, StageLaunch l2, StageLaunch l3,
+               Kfn k1, Kfn k2, Kfn k3) {
+  stages = std::max(1, std::min(3, stages));
+  const uint32_t smem = tma_smem<St>(stages);
+  Kfn k = stages == 1 ? k1 : stages == 2 ? k2 : k3;
+  *launch = stages == 1 ? l1 : stages == 2 ? l2 : l3;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, smem));
+  *grid = std::max(1, per_sm) * n_sm;
+}
 
 template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 KernelSet make_set() {
@@ -70,27 +103,23 @@ KernelSet make_set() {
   };
   s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
   if constexpr (MMT > 0 && UNI) {
-    using St = CentralStage<K, NQ, NF, MMT>;
     s.central_tma = true;
-    s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                   int f) { k_central_tma<K, NQ, NF, MMT><<<g, kBlock, St::SMEM, st>>>(L, p, S, U, f); };
-    s.central_tma_setup = [](int n_sm) -> int {
-      CK(cudaFuncSetAttribute(k_central_tma<K, NQ, NF, MMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              St::SMEM));
-      int per_sm = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_central_tma<K, NQ, NF, MMT>, kBlock, St::SMEM));
-      return std::max(1, per_sm) * n_sm;
+    s.central_tma_setup = [](int n_sm, int stages, int* grid, void (**launch)(dim3, cudaStream_t, const Layout&,
+                                                                              const Physics&, const Scratch&,
+                                                                              const double4*, int)) {
+      tma_setup<CentralStage<K, NQ, NF, MMT>>(n_sm, stages, grid, launch, central_tma_launcher<K, NQ, NF, MMT, 1>,
+                                             central_tma_launcher<K, NQ, NF, MMT, 2>,
+                                             central_tma_launcher<K, NQ, NF, MMT, 3>, k_central_tma<K, NQ, NF, MMT, 1>,
+                                             k_central_tma<K, NQ, NF, MMT, 2>, k_central_tma<K, NQ, NF, MMT, 3>);
     };
-    using Tt = TroubledStage<K, NQ, NF, MMT, MDT>;
-    s.troubled = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                    int f) { k_troubled_tma<K, NQ, NF, MMT, MDT><<<g, kBlock, Tt::SMEM, st>>>(L, p, S, U, f); };
-    s.troubled_setup = [](int n_sm) -> int {
-      CK(cudaFuncSetAttribute(k_troubled_tma<K, NQ, NF, MMT, MDT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              Tt::SMEM));
-      int per_sm = 0;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_troubled_tma<K, NQ, NF, MMT, MDT>, kBlock,
-                                                       Tt::SMEM));
-      return std::max(1, per_sm) * n_sm;
+    s.troubled_setup = [](int n_sm, int stages, int* grid, void (**launch)(dim3, cudaStream_t, const Layout&,
+                                                                           const Physics&, const Scratch&,
+                                                                           const double4*, int)) {
+      tma_setup<TroubledStage<K, NQ, NF, MMT, MDT>>(
+          n_sm, stages, grid, launch, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 1>,
+          troubled_tma_launcher<K, NQ, NF, MMT, MDT, 2>, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 3>,
+          k_troubled_tma<K, NQ, NF, MMT, MDT, 1>, k_troubled_tma<K, NQ, NF, MMT, MDT, 2>,
+          k_troubled_tma<K, NQ, NF, MMT, MDT, 3>);
     };
   }
   return s;
@@ -440,8 +469,12 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   bool uniform = true;
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
   I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
-  if (I.ks.central_tma) I.ks.central_tma_grid = I.ks.central_tma_setup(I.n_sm);
-  if (I.ks.troubled) I.ks.troubled_grid = I.ks.troubled_setup(I.n_sm);
+  if (I.ks.central_tma) {
+    const char* e1 = std::getenv("UCFVB_TMA_STAGES_CENTRAL");
+    const char* e2 = std::getenv("UCFVB_TMA_STAGES_TROUBLED");
+    I.ks.central_tma_setup(I.n_sm, e1 ? std::atoi(e1) : 1, &I.ks.central_tma_grid, &I.ks.central);
+    I.ks.troubled_setup(I.n_sm, e2 ? std::atoi(e2) : 1, &I.ks.troubled_grid, &I.ks.troubled);
+  }
   auto& own = I.owned;
   Layout& L = I.L;
   L.n = H.n;

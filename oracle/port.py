@@ -44,6 +44,13 @@ def lib():
             "port_get_face_values": (None, [H, dp, dp]),
             "port_get_dofs": (None, [H, dp]),
             "port_get_bounds": (None, [H, dp]),
+            "port_compute_margins": (None, [C.POINTER(A.Margins), C.c_double, dp, dp]),
+            "port_classify_violation": (C.c_int, [C.c_double, C.c_double, C.c_double]),
+            "port_deactivate_smooth": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double]),
+            "port_limiter_bj": (C.c_double, [C.c_double, C.c_double, C.c_double, dp, C.c_int]),
+            "port_limiter_venkat": (C.c_double, [C.c_double, C.c_double, C.c_double, dp, C.c_int, C.c_double]),
+            "port_flux": (C.c_int, [dp, dp, C.c_double, C.c_double, C.c_double, C.c_int, dp]),
+            "port_cwenoz_blend": (C.c_int, [dp, C.c_int, dp, dp, C.c_int, C.c_double, C.c_double, C.c_double, dp]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)

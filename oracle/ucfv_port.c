@@ -765,3 +765,21 @@ void port_get_face_values(const port_solver* P, double* L, double* R) {
 }
 void port_get_dofs(const port_solver* P, double* d) { memcpy(d, P->dofs, sizeof(double) * (size_t)P->n * P->K * NV); }
 void port_get_bounds(const port_solver* P, double* b) { memcpy(b, P->bounds, sizeof(double) * (size_t)P->n * 4); }
+
+/* ---- exported point functions (known-answer tests, tests/test_kat.py) ---- */
+void port_compute_margins(const ucfvb_margins* m, double du, double* dm, double* dw) { compute_margins(m, du, dm, dw); }
+int port_classify_violation(double v, double dm, double dw) { return classify_violation(v, dm, dw); }
+int port_deactivate_smooth(double du, double h, double kappa, double n) { return deactivate_smooth(du, h, kappa, n); }
+double port_limiter_bj(double u0, double lo, double hi, const double* q, int nq) { return limiter_bj(u0, lo, hi, q, nq); }
+double port_limiter_venkat(double u0, double lo, double hi, const double* q, int nq, double eps2) {
+  return limiter_venkat(u0, lo, hi, q, nq, eps2);
+}
+int port_flux(const double* ul, const double* ur, double nx, double ny, double g, int kind, double* out) {
+  int which = 0;
+  double bad = 0.0;
+  return riemann_flux(kind, ul, ur, nx, ny, g, out, &which, &bad) ? UCFVB_NONPHYSICAL : 0;
+}
+int port_cwenoz_blend(const double* oi, int K, const double* central, const double* dir, int nd, double lambda1p,
+                      double eps, double b, double* blended) {
+  return cwenoz_blend(oi, K, central, (const double(*)[2])dir, nd, lambda1p, eps, b, blended);
+}

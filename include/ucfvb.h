@@ -245,6 +245,44 @@ int32_t ucfvb_n_cells(const ucfvb_solver* h);
 int32_t ucfvb_n_faces(const ucfvb_solver* h);
 int32_t ucfvb_n_qp(const ucfvb_solver* h);
 
+/* ---- domain decomposition (multi-GPU) --------------------
+ * A subdomain is rank r's part of a partitioned mesh: its owned cells plus
+ * the stencil-depth halo every owned residual depends on (face neighbours to
+ * depth 2 for spread + NAD, then central stencils and face neighbours of those),
+ * as a self-contained local mesh + stencil set. Local cells are ordered
+ * [owned (global order) | halo grouped by owner rank (global order)], so each
+ * peer's halo block is one contiguous receive range. Halo cells beyond the
+ * classification layers carry inert (zero-weight) stencils; faces leaving the
+ * local set belong to the local patch "__halo__" and are never integrated. */
+/* recursive coordinate bisection of cell centroids into n_parts balanced parts */
+int32_t ucfvb_partition_rcb(const ucfvb_mesh_view* mesh, int32_t n_parts, int32_t* part);
+typedef struct ucfvb_subdomain ucfvb_subdomain;
+int32_t ucfvb_subdomain_build(const ucfvb_mesh_view* mesh, const ucfvb_stencil_view* stencils,
+                              const int32_t* part, int32_t n_parts, int32_t rank, ucfvb_subdomain** out);
+int32_t ucfvb_subdomain_views(const ucfvb_subdomain* s, ucfvb_mesh_view* mesh, ucfvb_stencil_view* stencils);
+/* n_owned, n_local, n_peers */
+int32_t ucfvb_subdomain_info(const ucfvb_subdomain* s, int32_t* n_owned, int32_t* n_local, int32_t* n_peers);
+/* global cell id of every local cell [n_local] */
+int32_t ucfvb_subdomain_global_ids(const ucfvb_subdomain* s, int32_t* gid);
+/* peer i: its rank, how many owned cells go to it, and the local range
+ * [recv_begin, recv_begin + n_recv) its owned cells fill */
+int32_t ucfvb_subdomain_peer(const ucfvb_subdomain* s, int32_t i, int32_t* rank, int32_t* n_send,
+                             int32_t* n_recv, int32_t* recv_begin);
+/* local ids (owned cells) sent to peer i, in the peer's receive order */
+int32_t ucfvb_subdomain_send_list(const ucfvb_subdomain* s, int32_t i, int32_t* local_ids);
+void ucfvb_subdomain_free(ucfvb_subdomain* s);
+
+/* Solver on a subdomain (ucfvb_create on the subdomain views + the owned
+ * count): residuals, RK updates, dt and census cover owned cells only. */
+int32_t ucfvb_create_sub(const ucfvb_subdomain* sub, const ucfvb_options* opt, const ucfvb_bc* bcs,
+                         int32_t n_bcs, int32_t device, ucfvb_solver** out);
+/* Attach an NCCL communicator (unique id from ucfvb_nccl_unique_id on rank 0,
+ * broadcast by the caller): every RK stage then ends with a grouped
+ * ncclSend/ncclRecv of the stage state's halo, max_stable_dt/run_steps use a
+ * min all-reduce, and run_steps' census a sum all-reduce. */
+int32_t ucfvb_nccl_unique_id(uint8_t id[128]);
+int32_t ucfvb_attach_nccl(ucfvb_solver* h, const uint8_t id[128], int32_t rank, int32_t world);
+
 /* ---- device-resident entry points (benchmark "value" leg) ---------------- */
 /* device pointer to the [n_cells][4] state; valid until the next call */
 int32_t ucfvb_state_device_ptr(ucfvb_solver* h, double** dptr);

@@ -317,6 +317,17 @@ def _declare(lib):
         "ucfvb_state_device_ptr": (C.c_int32, [H, P(c_dp)]),
         "ucfvb_stream": (C.c_int32, [H, P(C.c_void_p)]),
         "ucfvb_launch_count": (C.c_int64, [H]),
+        "ucfvb_partition_rcb": (C.c_int32, [P(MeshView), C.c_int32, c_i32p]),
+        "ucfvb_subdomain_build": (C.c_int32, [P(MeshView), P(StencilView), c_i32p, C.c_int32, C.c_int32, P(H)]),
+        "ucfvb_subdomain_views": (C.c_int32, [H, P(MeshView), P(StencilView)]),
+        "ucfvb_subdomain_info": (C.c_int32, [H, c_i32p, c_i32p, c_i32p]),
+        "ucfvb_subdomain_global_ids": (C.c_int32, [H, c_i32p]),
+        "ucfvb_subdomain_peer": (C.c_int32, [H, C.c_int32, c_i32p, c_i32p, c_i32p, c_i32p]),
+        "ucfvb_subdomain_send_list": (C.c_int32, [H, C.c_int32, c_i32p]),
+        "ucfvb_subdomain_free": (None, [H]),
+        "ucfvb_create_sub": (C.c_int32, [H, P(Options), P(BC), C.c_int32, C.c_int32, P(H)]),
+        "ucfvb_nccl_unique_id": (C.c_int32, [P(C.c_uint8)]),
+        "ucfvb_attach_nccl": (C.c_int32, [H, P(C.c_uint8), C.c_int32, C.c_int32]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -335,6 +346,9 @@ ABI_SYMBOLS = [
     "ucfvb_get_nad_ties", "ucfvb_get_face_values", "ucfvb_get_dofs", "ucfvb_set_phase_timing",
     "ucfvb_get_phase_times", "ucfvb_n_cells", "ucfvb_n_faces", "ucfvb_n_qp",
     "ucfvb_state_device_ptr", "ucfvb_stream", "ucfvb_launch_count",
+    "ucfvb_partition_rcb", "ucfvb_subdomain_build", "ucfvb_subdomain_views", "ucfvb_subdomain_info",
+    "ucfvb_subdomain_global_ids", "ucfvb_subdomain_peer", "ucfvb_subdomain_send_list", "ucfvb_subdomain_free",
+    "ucfvb_create_sub", "ucfvb_nccl_unique_id", "ucfvb_attach_nccl",
 ]
 
 

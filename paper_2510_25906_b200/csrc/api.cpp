@@ -7,6 +7,7 @@
 #include <new>
 #include <string>
 
+#include "decompose.hpp"
 #include "layout.hpp"
 #include "setup.hpp"
 #include "solver.hpp"
@@ -14,8 +15,13 @@
 
 struct ucfvb_solver {
   ucfvb::GpuSolver* s = nullptr;
+  const ucfvb_subdomain* sub = nullptr;  // borrowed (ucfvb_create_sub); must outlive the solver
   std::string err;
 };
+
+namespace ucfvb {
+void nccl_unique_id(uint8_t id[128]);
+}
 
 namespace {
 
@@ -185,5 +191,77 @@ int32_t ucfvb_stream(ucfvb_solver* h, void** stream) {
   return guard(h, [&] { *stream = h->s->stream(); });
 }
 int64_t ucfvb_launch_count(const ucfvb_solver* h) { return h->s->launch_count(); }
+
+
+int32_t ucfvb_partition_rcb(const ucfvb_mesh_view* mesh, int32_t n_parts, int32_t* part) {
+  return guard(nullptr, [&] { ucfvb::partition_rcb(*mesh, n_parts, part); });
+}
+
+int32_t ucfvb_subdomain_build(const ucfvb_mesh_view* mesh, const ucfvb_stencil_view* stencils, const int32_t* part,
+                              int32_t n_parts, int32_t rank, ucfvb_subdomain** out) {
+  return guard(nullptr, [&] { *out = ucfvb::build_subdomain(*mesh, *stencils, part, n_parts, rank); });
+}
+
+int32_t ucfvb_subdomain_views(const ucfvb_subdomain* s, ucfvb_mesh_view* mesh, ucfvb_stencil_view* stencils) {
+  if (mesh) *mesh = s->mv;
+  if (stencils) *stencils = s->sv;
+  return UCFVB_OK;
+}
+
+int32_t ucfvb_subdomain_info(const ucfvb_subdomain* s, int32_t* n_owned, int32_t* n_local, int32_t* n_peers) {
+  if (n_owned) *n_owned = s->n_owned;
+  if (n_local) *n_local = s->n_local;
+  if (n_peers) *n_peers = static_cast<int32_t>(s->peers.size());
+  return UCFVB_OK;
+}
+
+int32_t ucfvb_subdomain_global_ids(const ucfvb_subdomain* s, int32_t* gid) {
+  std::memcpy(gid, s->gid.data(), s->gid.size() * sizeof(int32_t));
+  return UCFVB_OK;
+}
+
+int32_t ucfvb_subdomain_peer(const ucfvb_subdomain* s, int32_t i, int32_t* rank, int32_t* n_send, int32_t* n_recv,
+                             int32_t* recv_begin) {
+  if (i < 0 || i >= static_cast<int32_t>(s->peers.size())) return UCFVB_INVALID;
+  const auto& p = s->peers[i];
+  if (rank) *rank = p.rank;
+  if (n_send) *n_send = static_cast<int32_t>(p.send.size());
+  if (n_recv) *n_recv = p.n_recv;
+  if (recv_begin) *recv_begin = p.recv_begin;
+  return UCFVB_OK;
+}
+
+int32_t ucfvb_subdomain_send_list(const ucfvb_subdomain* s, int32_t i, int32_t* local_ids) {
+  if (i < 0 || i >= static_cast<int32_t>(s->peers.size())) return UCFVB_INVALID;
+  std::memcpy(local_ids, s->peers[i].send.data(), s->peers[i].send.size() * sizeof(int32_t));
+  return UCFVB_OK;
+}
+
+void ucfvb_subdomain_free(ucfvb_subdomain* s) { delete s; }
+
+int32_t ucfvb_create_sub(const ucfvb_subdomain* sub, const ucfvb_options* opt, const ucfvb_bc* bcs, int32_t n_bcs,
+                         int32_t device, ucfvb_solver** out) {
+  *out = nullptr;
+  return guard(nullptr, [&] {
+    auto* h = new ucfvb_solver;
+    try {
+      h->s = new ucfvb::GpuSolver(sub->mv, sub->sv, *opt, bcs, n_bcs, device, sub->n_owned);
+      h->sub = sub;
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int32_t ucfvb_nccl_unique_id(uint8_t id[128]) {
+  return guard(nullptr, [&] { ucfvb::nccl_unique_id(id); });
+}
+
+int32_t ucfvb_attach_nccl(ucfvb_solver* h, const uint8_t id[128], int32_t rank, int32_t world) {
+  return guard(h, [&] { h->s->attach_nccl(id, rank, world, h->sub); });
+}
+
 
 }  // extern "C"

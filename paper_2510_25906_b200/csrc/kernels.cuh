@@ -43,7 +43,8 @@ struct BcEntry {
 
 // everything a stage kernel reads; passed by value (fits the 32 KB param space)
 struct Layout {
-  int n;       // cells
+  int n;       // cells (local: owned + halo on a subdomain)
+  int n_owned; // cells whose residual / RK update / dt this solver owns
   int MM;      // padded central stencil size (excluding self)
   int MD;      // padded directional stencil size (excluding self)
   const int* st_idx;        // E = MM           central member cell ids
@@ -625,8 +626,8 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
   const int v = g & 3;
   const int c0 = g >> 2;
   const int lane = threadIdx.x & 31;
-  const bool live = c0 < L.n;
-  const int c = live ? c0 : L.n - 1;
+  const bool live = c0 < L.n_owned;
+  const int c = live ? c0 : L.n_owned - 1;
   const int err0 = *(volatile int*)S.err;
   const double* ffd = reinterpret_cast<const double*>(S.ff);
   double term[5];
@@ -687,16 +688,27 @@ struct DtState {
   double dt;    // dt of the current step
   double t_end;
   double cfl;
+  double dmin;  // this rank's min(h/speed) (all-reduced across ranks before k_dt_finalize)
 };
 
+__device__ __forceinline__ void dt_finalize(DtState* ds, double dmin) {
+  // run.cpp:97-132: t advances by the previous dt (0 before the first step)
+  ds->t = ds->t + ds->dt;
+  ds->step += 1;
+  const double dt = ds->cfl * dmin;  // solver.cpp:110
+  ds->dt = smin(dt, ds->t_end - ds->t);
+}
+
+// finalize: 1 = single rank (the last block turns the min into dt), 0 = leave
+// ds->dmin for a cross-rank min all-reduce followed by k_dt_finalize
 __global__ void __launch_bounds__(256) k_dt(Layout L, const double4* __restrict__ U, double gamma, DtState* ds,
-                                            int* err) {
+                                            int* err, int finalize) {
   __shared__ double red[8];
   __shared__ bool last;
   if (*(volatile int*)err) return;  // a previous kernel failed: freeze the run
   const int c = blockIdx.x * 256 + threadIdx.x;
   double x = 1e300;
-  if (c < L.n) {
+  if (c < L.n_owned) {
     const d4 s = ld4(&U[c]);
     double rho, u, v, p;
     if (cons_to_prim(s.v, gamma, rho, u, v, p)) {
@@ -724,14 +736,23 @@ __global__ void __launch_bounds__(256) k_dt(Layout L, const double4* __restrict_
   if (last && threadIdx.x == 0) {
     __threadfence();
     const double dmin = __longlong_as_double(static_cast<long long>(atomicAdd(&ds->dmin_bits, 0ull)));
-    // run.cpp:97-132: t advances by the previous dt (0 before the first step)
-    ds->t = ds->t + ds->dt;
-    ds->step += 1;
-    const double dt = ds->cfl * dmin;
-    ds->dt = smin(dt, ds->t_end - ds->t);
+    ds->dmin = dmin;
+    if (finalize) dt_finalize(ds, dmin);
     ds->dmin_bits = static_cast<unsigned long long>(__double_as_longlong(1e300));
     ds->blocks_done = 0;
   }
+}
+
+__global__ void k_dt_finalize(DtState* ds, const int* err) {
+  if (*(volatile const int*)err) return;
+  dt_finalize(ds, ds->dmin);
+}
+
+// pack the owned cells a peer needs into a contiguous send buffer
+__global__ void __launch_bounds__(256) k_halo_pack(const double4* __restrict__ U, const int* __restrict__ idx, int n,
+                                                   double4* __restrict__ out) {
+  const int i = blockIdx.x * 256 + threadIdx.x;
+  if (i < n) out[i] = U[idx[i]];
 }
 
 }  // namespace ucfvb

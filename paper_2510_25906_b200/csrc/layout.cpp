@@ -44,7 +44,7 @@ int local_face_index(const ucfvb_mesh_view& m, int cell, int fid) {
 }  // namespace
 
 HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, const ucfvb_options& o,
-                        int n_threads) {
+                        int n_threads, int n_owned, int halo_patch) {
   HostLayout L;
   const int n = m.n_cells;
   if (n <= 0) throw ApiError(UCFVB_INVALID, "solver: empty mesh");
@@ -55,6 +55,8 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
                                       " face quadrature points but order " + std::to_string(o.order) + " needs " +
                                       std::to_string(s.n_qp));
   L.n = n;
+  L.n_owned = n_owned;
+  if (n_owned < 1 || n_owned > n) throw ApiError(UCFVB_INVALID, "solver: owned cell count out of range");
   L.n_pad = (n + 31) / 32 * 32;
   L.K = s.K;
   L.NQ = s.n_qp;
@@ -106,6 +108,8 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
       L.fkind[f] = 0;
     } else if (partner >= 0) {
       L.fkind[f] = partner > f ? 0 : 2;  // the primary of a periodic pair carries the flux (solver.cpp:272)
+    } else if (m.face_patch[f] == halo_patch && halo_patch >= 0) {
+      L.fkind[f] = 2;  // leaves a subdomain's local set: never integrated
     } else {
       const int patch = m.face_patch[f];
       if (patch < 0 || patch >= 16)
@@ -113,6 +117,10 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
       L.fkind[f] = 1;
       L.fpatch[f] = static_cast<int8_t>(patch);
     }
+    // on a subdomain only faces touching an owned cell are integrated
+    const bool touches_owned = m.face_left[f] < n_owned || (m.face_right[f] >= 0 && m.face_right[f] < n_owned) ||
+                               (partner >= 0 && m.face_left[partner] < n_owned);
+    if (!touches_owned) L.fkind[f] = 2;
   }
   L.nfc.assign(L.n_pad, 0);
   L.deact_thr.assign(L.n_pad, 0.0);

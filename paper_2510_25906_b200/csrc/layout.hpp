@@ -18,7 +18,7 @@ struct ApiError : std::runtime_error {
 };
 
 struct HostLayout {
-  int n = 0, n_pad = 0, K = 0, NQ = 0, NF = 0, Q = 0, MM = 0, MD = 0;
+  int n = 0, n_owned = 0, n_pad = 0, K = 0, NQ = 0, NF = 0, Q = 0, MM = 0, MD = 0;
   std::vector<int32_t> st_idx, dir_idx, nbr, dest, cface;
   std::vector<double> pinv, phi, phi01, pinv_lin, pinv_dir, oi;
   std::vector<uint8_t> nfc;
@@ -35,7 +35,7 @@ struct HostLayout {
 
 // Builds the layout; throws ApiError(UCFVB_INVALID / UCFVB_UNSUPPORTED).
 HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, const ucfvb_options& o,
-                        int n_threads);
+                        int n_threads, int n_owned, int halo_patch);
 
 // parallel_for over [0, n) in contiguous ranges (std::thread; no OpenMP runtime needed)
 void parallel_for(int64_t n, int n_threads, const std::function<void(int64_t, int64_t)>& body);

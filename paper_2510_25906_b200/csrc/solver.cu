@@ -13,9 +13,13 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include "kernels.cuh"
 #include "kernels_tma.cuh"
 #include "layout.hpp"
+#include "decompose.hpp"
 #include "solver.hpp"
 
 namespace ucfvb {
@@ -26,6 +30,61 @@ namespace ucfvb {
     if (e_ != cudaSuccess)                                                                           \
       throw ApiError(UCFVB_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));                   \
   } while (0)
+
+// ---- NCCL, resolved at run time --------------------------------------------
+// The library never links NCCL: ucfvb_attach_nccl binds to the NCCL already in
+// the process (torch's, when torch.distributed initialised it) or dlopens
+// libnccl.so.2. Single-GPU use therefore has no NCCL dependency at all.
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static const Nccl& nccl() {
+  static Nccl n;
+  static bool done = false;
+  if (done) return n;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) throw ApiError(UCFVB_UNSUPPORTED, "NCCL (libnccl.so.2) is not available");
+  auto sym = [&](const char* name) {
+    void* f = dlsym(h, name);
+    if (!f) throw ApiError(UCFVB_UNSUPPORTED, std::string("NCCL symbol missing: ") + name);
+    return f;
+  };
+  n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(sym("ncclGetUniqueId"));
+  n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(sym("ncclCommInitRank"));
+  n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(sym("ncclCommDestroy"));
+  n.Send = reinterpret_cast<decltype(n.Send)>(sym("ncclSend"));
+  n.Recv = reinterpret_cast<decltype(n.Recv)>(sym("ncclRecv"));
+  n.AllReduce = reinterpret_cast<decltype(n.AllReduce)>(sym("ncclAllReduce"));
+  n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(sym("ncclGroupStart"));
+  n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(sym("ncclGroupEnd"));
+  n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(sym("ncclGetErrorString"));
+  done = true;
+  return n;
+}
+
+#define NK(x)                                                                                  \
+  do {                                                                                         \
+    ncclResult_t r_ = (x);                                                                     \
+    if (r_ != ncclSuccess) throw ApiError(UCFVB_CUDA, std::string(#x) + ": " + nccl().GetErrorString(r_)); \
+  } while (0)
+
+void nccl_unique_id(uint8_t id[128]) {
+  ncclUniqueId u;
+  NK(nccl().GetUniqueId(&u));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+}
 
 // ---- kernel dispatch over (K, NQ, NF) ----------------------------------------
 struct KernelSet {
@@ -199,6 +258,47 @@ struct GpuSolver::Impl {
   cudaGraphExec_t graph[2][2][2] = {};
   int64_t graph_launches[2][2][2] = {};
   std::string last_error;
+  // decomposition / NCCL (halo exchange after every stage)
+  struct DevPeer {
+    int rank = 0, n_send = 0, recv_begin = 0, n_recv = 0;
+    int* send_idx = nullptr;
+    size_t send_off = 0;
+  };
+  std::vector<DevPeer> peers;
+  double4* sendbuf = nullptr;
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+
+  dim3 grid_owned4() const { return dim3((4 * L.n_owned + kBlock - 1) / kBlock); }
+
+  // halo exchange of a stage state: pack per peer, then one grouped send/recv
+  int64_t exchange(double4* buf) {
+    if (!comm || peers.empty()) return 0;
+    int64_t nl = 0;
+    for (const DevPeer& p : peers)
+      if (p.n_send) {
+        k_halo_pack<<<dim3((p.n_send + 255) / 256), 256, 0, stream>>>(buf, p.send_idx, p.n_send, sendbuf + p.send_off);
+        ++nl;
+      }
+    NK(nccl().GroupStart());
+    for (const DevPeer& p : peers) {
+      if (p.n_send) NK(nccl().Send(sendbuf + p.send_off, 4 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm,
+                                   stream));
+      if (p.n_recv) NK(nccl().Recv(buf + p.recv_begin, 4 * static_cast<size_t>(p.n_recv), ncclDouble, p.rank, comm,
+                                   stream));
+    }
+    NK(nccl().GroupEnd());
+    return nl;
+  }
+
+  // this step's dt: per-rank min, then (decomposed) a min all-reduce
+  int64_t launch_dt(const double4* src) {
+    k_dt<<<dim3((L.n_owned + 255) / 256), 256, 0, stream>>>(L, src, opt.gamma, ds, S.err, comm ? 0 : 1);
+    if (!comm) return 1;
+    NK(nccl().AllReduce(&ds->dmin, &ds->dmin, 1, ncclDouble, ncclMin, comm, stream));
+    k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err);
+    return 2;
+  }
 
   dim3 grid_cells() const { return dim3((L.n + kBlock - 1) / kBlock); }
   // four lanes per cell (reconstruction kernels)
@@ -267,7 +367,7 @@ struct GpuSolver::Impl {
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
     ks.face_flux(dim3((L.n_faces + ks.faces_per_flux_block - 1) / ks.faces_per_flux_block), stream, L, ph, S);
-    ks.gather(grid_cells4(), stream, L, S, rk, ff);
+    ks.gather(grid_owned4(), stream, L, S, rk, ff);
     ++nl;
     record(4);
     CK(cudaGetLastError());
@@ -296,10 +396,7 @@ struct GpuSolver::Impl {
   int64_t launch_step(int rk, bool with_dt, const double4* src, double4* dst, bool census) {
     int64_t nl = 0;
     const double* dt = &ds->dt;
-    if (with_dt) {
-      k_dt<<<dim3((L.n + 255) / 256), 256, 0, stream>>>(L, src, opt.gamma, ds, S.err);
-      ++nl;
-    }
+    if (with_dt) nl += launch_dt(src);
     if (rk == UCFVB_RK3) {
       double4 *u1 = work[0], *u2 = work[1];
       RkEpilogue e1{};
@@ -309,6 +406,7 @@ struct GpuSolver::Impl {
       add_term(e1, src, 0.0, false);
       add_term(e1, nullptr, 1.0, true);
       nl += launch_stage(src, true, e1, census);
+      nl += exchange(u1);
       RkEpilogue e2{};
       e2.dt = dt;
       e2.out = u2;
@@ -316,6 +414,7 @@ struct GpuSolver::Impl {
       add_term(e2, u1, 0.25, false);
       add_term(e2, nullptr, 0.25, true);
       nl += launch_stage(u1, false, e2, census);
+      nl += exchange(u2);
       RkEpilogue e3{};
       e3.dt = dt;
       e3.out = dst;
@@ -323,6 +422,7 @@ struct GpuSolver::Impl {
       add_term(e3, u2, 2.0 / 3.0, false);
       add_term(e3, nullptr, 2.0 / 3.0, true);
       nl += launch_stage(u2, false, e3, census);
+      nl += exchange(dst);
     } else {
       using namespace rk54;
       double4 *ua = work[0], *ub = work[1], *uc = work[2], *ud = work[3], *r3 = work[4];
@@ -333,6 +433,7 @@ struct GpuSolver::Impl {
       add_term(e, src, 0.0, false);
       add_term(e, nullptr, a10, true);
       nl += launch_stage(src, true, e, census);
+      nl += exchange(ua);
       e = RkEpilogue{};
       e.dt = dt;
       e.out = ub;
@@ -340,6 +441,7 @@ struct GpuSolver::Impl {
       add_term(e, ua, b21, false);
       add_term(e, nullptr, a21, true);
       nl += launch_stage(ua, false, e, census);
+      nl += exchange(ub);
       e = RkEpilogue{};
       e.dt = dt;
       e.out = uc;
@@ -347,6 +449,7 @@ struct GpuSolver::Impl {
       add_term(e, ub, b32, false);
       add_term(e, nullptr, a32, true);
       nl += launch_stage(ub, false, e, census);
+      nl += exchange(uc);
       e = RkEpilogue{};
       e.dt = dt;
       e.out = ud;
@@ -355,6 +458,7 @@ struct GpuSolver::Impl {
       add_term(e, uc, b43, false);
       add_term(e, nullptr, a43, true);
       nl += launch_stage(uc, false, e, census);
+      nl += exchange(ud);
       e = RkEpilogue{};
       e.dt = dt;
       e.out = dst;
@@ -364,6 +468,7 @@ struct GpuSolver::Impl {
       add_term(e, ud, c54, false);
       add_term(e, nullptr, a54, true);
       nl += launch_stage(ud, false, e, census);
+      nl += exchange(dst);
     }
     return nl;
   }
@@ -411,6 +516,11 @@ struct GpuSolver::Impl {
     }
   }
 
+  // every rank learns that some rank failed (the kinds are OR-ed via max of bits)
+  void allreduce_error() {
+    if (comm) NK(nccl().AllReduce(S.err, S.err, 1, ncclInt32, ncclMax, comm, stream));
+  }
+
   void check_after() {
     int k, f, c;
     if (read_error(&k, &f, &c)) raise_device_error(k, f, c);
@@ -418,7 +528,7 @@ struct GpuSolver::Impl {
 };
 
 GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, const ucfvb_options& o,
-                     const ucfvb_bc* bcs, int n_bcs, int device)
+                     const ucfvb_bc* bcs, int n_bcs, int device, int n_owned)
     : p_(new Impl) {
   Impl& I = *p_;
   I.opt = o;
@@ -448,9 +558,14 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
     ph.bc[pid].kind = bcs[i].kind;
     for (int v = 0; v < 4; ++v) ph.bc[pid].state[v] = bcs[i].state[v];
   }
+  // faces leaving a subdomain's local cell set (ucfvb_subdomain_build) need no BC: never integrated
+  int halo_patch = -1;
+  for (int p = 0; p < m.n_patches; ++p)
+    if (std::strcmp(m.patch_names[p], "__halo__") == 0) halo_patch = p;
   for (int f = 0; f < m.n_faces; ++f)
     if (m.face_right[f] < 0 && m.face_partner[f] < 0) {
       const int p = m.face_patch[f];
+      if (p == halo_patch && p >= 0) continue;
       if (p < 0 || ph.bc[p].kind == UCFVB_BC_NONE)
         throw ApiError(UCFVB_INVALID, "solver: boundary face " + std::to_string(f) +
                                           " has no boundary condition (patch " +
@@ -464,7 +579,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   CK(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
   for (auto& e : I.ev) CK(cudaEventCreate(&e));
 
-  I.host = build_layout(m, s, o, 0);
+  I.host = build_layout(m, s, o, 0, n_owned < 0 ? m.n_cells : n_owned, halo_patch);
   const HostLayout& H = I.host;
   bool uniform = true;
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
@@ -478,6 +593,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   auto& own = I.owned;
   Layout& L = I.L;
   L.n = H.n;
+  L.n_owned = H.n_owned;
   L.MM = H.MM;
   L.MD = H.MD;
   L.st_idx = dupload(H.st_idx, own);
@@ -563,6 +679,7 @@ GpuSolver::~GpuSolver() {
     for (auto& b : a)
       for (auto& g : b)
         if (g) cudaGraphExecDestroy(g);
+  if (I.comm) nccl().CommDestroy(I.comm);
   for (void* p : I.owned) cudaFree(p);
   if (I.census_dev) cudaFree(I.census_dev);
   for (auto& e : I.ev)
@@ -600,9 +717,9 @@ double GpuSolver::max_stable_dt() {
   h.t_end = INFINITY;
   h.cfl = I.opt.cfl;
   CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
-  k_dt<<<dim3((I.L.n + 255) / 256), 256, 0, I.stream>>>(I.L, I.ubuf[I.cur], I.opt.gamma, I.ds, I.S.err);
+  I.launches = I.launch_dt(I.ubuf[I.cur]);
   CK(cudaGetLastError());
-  I.launches = 1;
+  I.allreduce_error();
   CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
   I.check_after();
   return h.dt;
@@ -628,6 +745,7 @@ void GpuSolver::advance(double dt, double t, int rk) {
   } else {
     I.launches = I.launch_step(rk, false, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], false);
   }
+  I.allreduce_error();
   int k, f, c;
   if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);  // state stays at t (reference semantics)
   I.cur ^= 1;
@@ -693,6 +811,10 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
   I.launches = nl;
   I.S.step = I.step_zero;
   I.S.census = nullptr;
+  if (census && I.comm)
+    NK(nccl().AllReduce(I.census_dev, I.census_dev, 4 * static_cast<size_t>(n_steps), ncclUint64, ncclSum, I.comm,
+                        I.stream));
+  I.allreduce_error();
   CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
   int k, f, c;
   if (I.read_error(&k, &f, &c)) {
@@ -726,7 +848,7 @@ void GpuSolver::get_census(int64_t counts[4]) {
   std::vector<uint8_t> lab(n_cells());
   get_labels(lab.data(), true);
   counts[0] = counts[1] = counts[2] = counts[3] = 0;
-  for (uint8_t l : lab) ++counts[l & 3];
+  for (int c = 0; c < p_->L.n_owned; ++c) ++counts[lab[c] & 3];  // owned cells (subdomains: not the halo)
 }
 
 int64_t GpuSolver::nad_ties() {
@@ -781,6 +903,42 @@ void GpuSolver::get_dofs(double* dofs) {
 void GpuSolver::set_phase_timing(bool on) { p_->timing = on; }
 void GpuSolver::get_phase_times(double t[4]) {
   for (int i = 0; i < 4; ++i) t[i] = p_->phase[i];
+}
+
+void GpuSolver::attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub) {
+  Impl& I = *p_;
+  if (!sub) throw ApiError(UCFVB_INVALID, "attach_nccl: the solver was not created on a subdomain");
+  if (I.comm) throw ApiError(UCFVB_INVALID, "attach_nccl: a communicator is already attached");
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  CK(cudaSetDevice(I.device));
+  NK(nccl().CommInitRank(&I.comm, world, u, rank));
+  I.world = world;
+  I.rank = rank;
+  size_t off = 0;
+  for (const auto& p : sub->peers) {
+    Impl::DevPeer d;
+    d.rank = p.rank;
+    d.n_send = static_cast<int>(p.send.size());
+    d.recv_begin = p.recv_begin;
+    d.n_recv = p.n_recv;
+    d.send_off = off;
+    off += p.send.size();
+    if (d.n_send) {
+      d.send_idx = dalloc<int>(p.send.size(), I.owned);
+      CK(cudaMemcpy(d.send_idx, p.send.data(), p.send.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    I.peers.push_back(d);
+  }
+  I.sendbuf = dalloc<double4>(std::max<size_t>(1, off), I.owned);
+  // graphs captured before the exchange existed are stale
+  for (auto& a : I.graph)
+    for (auto& b : a)
+      for (auto& g : b)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
 }
 
 }  // namespace ucfvb

@@ -12,8 +12,10 @@ namespace ucfvb {
 class GpuSolver {
  public:
   // Solver(mesh, opt, bcs) (solver.cpp:36-74); throws ApiError
+  // n_owned < 0: every cell is owned (single domain); otherwise the first
+  // n_owned cells of a subdomain (ucfvb_subdomain_build) are owned
   GpuSolver(const ucfvb_mesh_view& mesh, const ucfvb_stencil_view& stencils, const ucfvb_options& opt,
-            const ucfvb_bc* bcs, int n_bcs, int device);
+            const ucfvb_bc* bcs, int n_bcs, int device, int n_owned = -1);
   ~GpuSolver();
   GpuSolver(const GpuSolver&) = delete;
   GpuSolver& operator=(const GpuSolver&) = delete;
@@ -40,6 +42,8 @@ class GpuSolver {
   int64_t launch_count() const;
   void* stream() const;
   double* state_device_ptr();
+  // NCCL communicator + the subdomain's exchange plan (halo exchange after every stage)
+  void attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub);
 
  private:
   struct Impl;

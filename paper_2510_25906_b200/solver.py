@@ -51,21 +51,27 @@ class Solver:
     """
 
     def __init__(self, mesh, options: A.Options | None = None, bcs=None, stencils=None, device: int = 0,
-                 keep=()):
+                 keep=(), subdomain=None):
         self._lib = A.load_library()
         self.options = options if options is not None else A.default_options()
-        if stencils is None:
+        if subdomain is None and stencils is None:
             stencils = Stencils(mesh, self.options.order, self.options.si_exponent)
         self.mesh = mesh
         self.stencils = stencils
+        self.subdomain = subdomain
         self._keep = keep
         if isinstance(bcs, dict):
             bcs = make_bcs(bcs)
         bcs = list(bcs or [])
         self._bcs = (A.BC * max(1, len(bcs)))(*bcs)
         h = C.c_void_p()
-        rc = self._lib.ucfvb_create(C.byref(mesh.view), C.byref(stencils.view), C.byref(self.options), self._bcs,
-                                    len(bcs), int(device), C.byref(h))
+        if subdomain is not None:
+            rc = self._lib.ucfvb_create_sub(subdomain.handle, C.byref(self.options), self._bcs, len(bcs), int(device),
+                                            C.byref(h))
+            stencils = type("SV", (), {"view": subdomain.stencil_view})()
+        else:
+            rc = self._lib.ucfvb_create(C.byref(mesh.view), C.byref(stencils.view), C.byref(self.options),
+                                        self._bcs, len(bcs), int(device), C.byref(h))
         if rc != A.OK:
             raise A.error_for(rc, self._lib.ucfvb_last_error(None).decode())
         self._h = h
@@ -73,6 +79,16 @@ class Solver:
         self.n_faces = self._lib.ucfvb_n_faces(h)
         self.n_qp = self._lib.ucfvb_n_qp(h)
         self.K = stencils.view.K
+
+    @classmethod
+    def on_subdomain(cls, subdomain, options=None, bcs=None, device: int = 0):
+        """Solver over a Subdomain (decompose.py): owned cells + halo; RK updates,
+        dt and census cover owned cells; attach_nccl adds the per-stage halo exchange."""
+        return cls(subdomain, options, bcs, device=device, subdomain=subdomain)
+
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        self._ck(self._lib.ucfvb_attach_nccl(self._h, buf, int(rank), int(world)))
 
     # -- errors ------------------------------------------------------------
     def _ck(self, rc):
@@ -185,6 +201,16 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId through the native library (rank 0 creates, all ranks attach)."""
+    lib = A.load_library()
+    buf = (C.c_uint8 * 128)()
+    rc = lib.ucfvb_nccl_unique_id(buf)
+    if rc != A.OK:
+        raise A.error_for(rc, lib.ucfvb_last_error(None).decode())
+    return bytes(buf)
 
 
 class ViewHolder:

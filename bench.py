@@ -21,7 +21,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -59,52 +58,67 @@ def env_rank():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled through NVML every
+    ~2 ms during the timed region (nvidia-smi's fields, without its 0.3 s/call)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason* bits
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+        0x80: "hw_power_brake_slowdown",
+    }
 
-    def __init__(self, index=0):
+    def __init__(self, index=0, period=0.002):
         self.index = index
-        self.rows = []
+        self.period = period
+        self.samples = []
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
 
     def _run(self):
+        nv = self._nvml
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        try:
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            pass
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)), int(get_reasons(h))))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            time.sleep(self.period)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nvml = nv
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+            time.sleep(0.01)
+        except Exception:
+            self._nvml = None
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         if self._t:
-            self._t.join(timeout=6)
+            self._t.join(timeout=2)
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        mhz = [m for m, _ in self.samples]
         reasons = set()
-        for r in self.rows:
-            for i, n in enumerate(names):
-                if len(r) > 4 + i and r[4 + i].lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        for _, r in self.samples:
+            for bit, name in self.REASONS.items():
+                if r & bit:
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(mhz)), "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml"}
 
 
 # ---------------------------------------------------------------- roofline model
@@ -132,9 +146,20 @@ def measured_peak_hbm():
 
 
 # ---------------------------------------------------------------- setup
-def build_case(cfg, n_threads=0):
+def scaled_config(cfg, world):
+    """Weak scaling: the config's domain repeated `world` times along y (periodic
+    in y), so every rank owns one config-sized block of cells."""
+    c = dict(CONFIGS[cfg])
+    if world > 1:
+        x0, y0, x1, y1 = c["rect"]
+        c["rect"] = (x0, y0, x1, y0 + world * (y1 - y0))
+        c["ny"] = c["ny"] * world
+    return c
+
+
+def build_case(cfg, n_threads=0, world=1):
     from paper_2510_25906_b200.mesh import Mesh, Stencils
-    c = CONFIGS[cfg]
+    c = scaled_config(cfg, world)
     nq = (c["order"] + 2) // 2
     t0 = time.perf_counter()
     mesh = Mesh.structured_tri(c["nx"], c["ny"], c["rect"], jitter=c["jitter"], seed=SEED, periodic=c["periodic"],
@@ -216,15 +241,39 @@ def run_b200_arm(args):
 
     cfg = args.config
     c = CONFIGS[cfg]
-    mesh, st, u0, setup_s = build_case(cfg)
+    threads = max(1, (os.cpu_count() or 1) // max(1, world))
+    mesh, st, u0, setup_s = build_case(cfg, n_threads=threads, world=world)
     opts = A.options_from_dict(order=c["order"], mode="hybrid", **c["opts"])
-    solver = Solver(mesh, opts, make_bcs(c["bcs"]), stencils=st, device=local)
-    n = solver.n_cells
+    bcs = make_bcs(c["bcs"])
+    sub = None
+    if world == 1:
+        solver = Solver(mesh, opts, bcs, stencils=st, device=local)
+        n = solver.n_cells
+    else:
+        from paper_2510_25906_b200.decompose import Subdomain, partition_rcb
+        from paper_2510_25906_b200.solver import nccl_unique_id
+        t0 = time.perf_counter()
+        part = partition_rcb(mesh, world)
+        sub = Subdomain(mesh, st, part, world, rank)
+        solver = Solver.on_subdomain(sub, opts, bcs, device=local)
+        ids = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        solver.attach_nccl(ids[0], rank, world)
+        u0 = sub.local_state(u0)
+        setup_s += time.perf_counter() - t0
+        n = sub.n_owned
     stream = torch.cuda.ExternalStream(solver.stream(), device=local)
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t)
+        return float(t.item())
 
     def max_over_ranks(x):
         if world == 1:
@@ -249,7 +298,8 @@ def run_b200_arm(args):
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = solver.launch_count()
-    total_units = n * 3 * args.steps * world
+    owned_total = int(round(sum_over_ranks(n)))
+    total_units = owned_total * 3 * args.steps
     value = total_units / (ms * 1e-3)
 
     # census of the timed run (class mix feeds the roofline bytes)
@@ -269,7 +319,7 @@ def run_b200_arm(args):
     solver.set_phase_timing(False)
 
     # ---- e2e leg: host state in pinned memory, H2D + step + D2H per step
-    host_u = torch.from_numpy(u0.copy()).pin_memory()
+    host_u = torch.from_numpy(np.ascontiguousarray(u0)).pin_memory()
     host_out = torch.empty_like(host_u).pin_memory()
     lib = A.load_library()
     import ctypes as C
@@ -297,7 +347,7 @@ def run_b200_arm(args):
     e1.synchronize()
     wall_e2e = time.perf_counter() - w0
     e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1e3 * wall_e2e))
-    e2e_value = n * 3 * e2e_steps * world / (e2e_ms * 1e-3)
+    e2e_value = owned_total * 3 * e2e_steps / (e2e_ms * 1e-3)
 
     # ---- roofline of the dominant kernel
     H = solver
@@ -341,17 +391,20 @@ def run_b200_arm(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["desc"], "cells": n, "order": c["order"], "K": K, "M": MM,
+            "config": {"workload": c["desc"] + (f"; weak scaling: domain repeated {world}x in y, RCB-partitioned, "
+                                                 f"one {n}-cell block per GPU" if world > 1 else ""),
+                       "cells": owned_total, "cells_per_gpu": n, "order": c["order"], "K": K, "M": MM,
                        "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid",
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "parallelism": f"domain decomposition x{world}, NCCL halo exchange per stage" if world > 1
+                       else "single",
                        "l2": "inputs larger than L2 (per-cell operator data %.0f MB)" % (
                            (kb["central"] + kb["cwenoz"] + kb["flux"]) * n / 1e6),
                        "class_mix_first_stage": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
                                                  "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
                        "setup_s": round(setup_s, 3)},
             "clocks": clk.summary(),
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 32),
-                    "d2h_bytes_per_step": int(n * 32)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(solver.n_cells * 32 * world),
+                    "d2h_bytes_per_step": int(solver.n_cells * 32 * world)},
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,

@@ -317,9 +317,23 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
   const unsigned mc = __ballot_sync(kFull, lab == 1);
   const unsigned mm = __ballot_sync(kFull, lab == 2);
   const unsigned lt = (1u << lane) - 1u;
-  if (flags & FL_CHUNKS) {  // one entry per 32-cell chunk (this warp) with troubled cells
-    if (lane == 0 && mc) S.chunks_c[atomicAdd(&S.counts[2], 1)] = make_int2(c >> 5, static_cast<int>(mc));
-    if (lane == 0 && mm) S.chunks_m[atomicAdd(&S.counts[3], 1)] = make_int2(c >> 5, static_cast<int>(mm));
+  if (flags & FL_CHUNKS) {  // one entry per 32-cell chunk (= this warp) with troubled cells
+    // block-aggregated: one global atomic per block and class (the chunk lists
+    // are unordered; per-cell results do not depend on the order)
+    __shared__ int s_nc, s_nm, s_bc, s_bm;
+    if (threadIdx.x == 0) s_nc = s_nm = 0;
+    __syncthreads();
+    int pc = -1, pm = -1;
+    if (lane == 0 && mc) pc = atomicAdd(&s_nc, 1);
+    if (lane == 0 && mm) pm = atomicAdd(&s_nm, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_bc = s_nc ? atomicAdd(&S.counts[2], s_nc) : 0;
+      s_bm = s_nm ? atomicAdd(&S.counts[3], s_nm) : 0;
+    }
+    __syncthreads();
+    if (pc >= 0) S.chunks_c[s_bc + pc] = make_int2(c >> 5, static_cast<int>(mc));
+    if (pm >= 0) S.chunks_m[s_bm + pm] = make_int2(c >> 5, static_cast<int>(mm));
     return;
   }
   if (mc) {

@@ -17,27 +17,45 @@ namespace ucfvb {
 
 __host__ __device__ constexpr uint32_t round16(uint32_t x) { return (x + 15u) & ~15u; }
 
+// blocks per SM the shared-memory footprint allows (capped at 8): passed to
+// __launch_bounds__ so that registers never become the tighter occupancy limit
+__host__ __device__ constexpr int smem_min_blocks(uint32_t bytes) {
+  const uint32_t per_block = bytes + 1024;  // + the per-block reservation
+  const uint32_t b = (227u * 1024u) / per_block;
+  return b < 1 ? 1 : (b > 8 ? 8 : static_cast<int>(b));
+}
+
 template <int K, int NQ, int NF, int MM>
 struct CentralStage {
   static constexpr int Q = NF * NQ;
+  // group A: consumed by the LSQ solve
   static constexpr uint32_t PINV = MM * K * 32 * 8;
-  static constexpr uint32_t PHI = Q * K * 32 * 8;
   static constexpr uint32_t IDX = round16(MM * 32 * 4);
+  static constexpr uint32_t A_BYTES = PINV + IDX;
+  // group B: consumed by evaluation, NAD and the scatter
+  static constexpr uint32_t PHI = Q * K * 32 * 8;
+  static constexpr uint32_t THR = 32 * 8;
   static constexpr uint32_t NBR = round16(NF * 32 * 4);
   static constexpr uint32_t DEST = round16(Q * 32 * 4);
-  static constexpr uint32_t BYTES = PINV + PHI + IDX + NBR + DEST;  // one stage
+  static constexpr uint32_t B_BYTES = PHI + THR + NBR + DEST;
+  static constexpr uint32_t BYTES = A_BYTES + B_BYTES;  // one stage
 };
 
 // k_central on the fast path: same arithmetic as k_central (kernels.cuh).
-// NS shared-memory stages form a ring; chunk it+NS-1 is in flight while chunk
-// it computes (NS = 1: no intra-block overlap, more resident blocks instead).
+// One shared-memory stage split into two TMA groups with their own
+// mbarriers: group A (pinv, stencil ids) is refilled with the next chunk as
+// soon as the solve has consumed it, group B (phi, thresholds, neighbours,
+// face-point slots) after the evaluation -- the copies of chunk i+1 overlap
+// the second half of chunk i without doubling the footprint (NS = 2 keeps
+// two such stages).
 template <int K, int NQ, int NF, int MM, int NS>
-__global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Scratch S,
+__global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, NQ, NF, MM>::BYTES + 16 * NS))
+    k_central_tma(Layout L, Physics ph, Scratch S,
                                                         const double4* __restrict__ U, int flags) {
   using St = CentralStage<K, NQ, NF, MM>;
   constexpr int Q = St::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NS * St::BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NS * St::BYTES);  // [2*NS]: A, B per stage
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const int tid = threadIdx.x;
   const int slot = tid >> 2;  // cell within the chunk
@@ -46,47 +64,53 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
   __shared__ int s_err;
   if (tid == 0) {
     s_err = *(volatile int*)S.err;
-    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < 2 * NS; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
   }
   __syncthreads();
   if (s_err) return;  // block-uniform: the loop below has block barriers
-  auto issue = [&](int chunk, int st) {
+  auto issue_a = [&](int chunk, int st) {
     unsigned char* b = smem + st * St::BYTES;
-    mbar_arrive_expect_tx(&bar[st], St::BYTES);
-    bulk_g2s(b, L.pinv + static_cast<size_t>(chunk) * MM * K * 32, St::PINV, &bar[st]);
-    bulk_g2s(b + St::PINV, L.phi + static_cast<size_t>(chunk) * Q * K * 32, St::PHI, &bar[st]);
-    bulk_g2s(b + St::PINV + St::PHI, L.st_idx + static_cast<size_t>(chunk) * MM * 32, St::IDX, &bar[st]);
-    bulk_g2s(b + St::PINV + St::PHI + St::IDX, L.nbr + static_cast<size_t>(chunk) * NF * 32, St::NBR, &bar[st]);
-    bulk_g2s(b + St::PINV + St::PHI + St::IDX + St::NBR, L.dest + static_cast<size_t>(chunk) * Q * 32, St::DEST,
-             &bar[st]);
+    mbar_arrive_expect_tx(&bar[2 * st], St::A_BYTES);
+    bulk_g2s(b, L.pinv + static_cast<size_t>(chunk) * MM * K * 32, St::PINV, &bar[2 * st]);
+    bulk_g2s(b + St::PINV, L.st_idx + static_cast<size_t>(chunk) * MM * 32, St::IDX, &bar[2 * st]);
+  };
+  auto issue_b = [&](int chunk, int st) {
+    unsigned char* b = smem + st * St::BYTES + St::A_BYTES;
+    mbar_arrive_expect_tx(&bar[2 * st + 1], St::B_BYTES);
+    bulk_g2s(b, L.phi + static_cast<size_t>(chunk) * Q * K * 32, St::PHI, &bar[2 * st + 1]);
+    bulk_g2s(b + St::PHI, L.deact_thr + static_cast<size_t>(chunk) * 32, St::THR, &bar[2 * st + 1]);
+    bulk_g2s(b + St::PHI + St::THR, L.nbr + static_cast<size_t>(chunk) * NF * 32, St::NBR, &bar[2 * st + 1]);
+    bulk_g2s(b + St::PHI + St::THR + St::NBR, L.dest + static_cast<size_t>(chunk) * Q * 32, St::DEST,
+             &bar[2 * st + 1]);
   };
   if (tid == 0)
-    for (int p = 0; p < NS - 1; ++p)
-      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nchunks) issue(blockIdx.x + p * gridDim.x, p);
+    for (int p = 0; p < NS; ++p)
+      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nchunks) {
+        issue_a(blockIdx.x + p * gridDim.x, p);
+        issue_b(blockIdx.x + p * gridDim.x, p);
+      }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool detect = (flags & (FL_NAD | FL_PRECHECK)) != 0;
   int it = 0;
   for (int chunk = blockIdx.x; chunk < nchunks; chunk += gridDim.x, ++it) {
     const int st = it % NS;
-    const int ahead = chunk + (NS - 1) * gridDim.x;
-    if (tid == 0 && ahead < nchunks) {
-      fence_proxy_async_smem();
-      issue(ahead, (it + NS - 1) % NS);
-    }
-    mbar_wait(&bar[st], (it / NS) & 1);
+    const uint32_t par = (it / NS) & 1;
+    const int refill = chunk + NS * gridDim.x;  // the chunk this stage holds next
     const unsigned char* b = smem + st * St::BYTES;
     const double* sp = reinterpret_cast<const double*>(b);
-    const double* sf = reinterpret_cast<const double*>(b + St::PINV);
-    const int* si = reinterpret_cast<const int*>(b + St::PINV + St::PHI);
-    const int* sn = reinterpret_cast<const int*>(b + St::PINV + St::PHI + St::IDX);
-    const int* sdst = reinterpret_cast<const int*>(b + St::PINV + St::PHI + St::IDX + St::NBR);
+    const int* si = reinterpret_cast<const int*>(b + St::PINV);
+    const double* sf = reinterpret_cast<const double*>(b + St::A_BYTES);
+    const double* sthr = reinterpret_cast<const double*>(b + St::A_BYTES + St::PHI);
+    const int* sn = reinterpret_cast<const int*>(b + St::A_BYTES + St::PHI + St::THR);
+    const int* sdst = reinterpret_cast<const int*>(b + St::A_BYTES + St::PHI + St::THR + St::NBR);
 
     const int c0 = chunk * 32 + slot;
     const bool live = c0 < L.n;
     const int c = live ? c0 : L.n - 1;
     const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
+    mbar_wait(&bar[2 * st], par);
     // solve_dofs (reconstruct.cpp:9-28), m outermost, per-accumulator m order kept
     double acc[K];
 #pragma unroll
@@ -100,10 +124,16 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
 #pragma unroll
       for (int k = 0; k < K; ++k) acc[k] += sp[(m * K + k) * 32 + slot] * d;
     }
+    __syncthreads();  // group A of this stage consumed: refill it with the next chunk
+    if (tid == 0 && refill < nchunks) {
+      fence_proxy_async_smem();
+      issue_a(refill, st);
+    }
     if ((flags & FL_DOFS) && live) {
 #pragma unroll
       for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = acc[k];
     }
+    mbar_wait(&bar[2 * st + 1], par);
     if (flags & FL_EVAL) {
       double lo = u0, hi = u0;
       if (detect) {
@@ -142,7 +172,7 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
         int sev = 0;
         bool tie = false;
         if ((flags & FL_NAD) && (v == 0 || v == 3)) {
-          const double thr = L.deact_thr[c];
+          const double thr = sthr[slot];
           if (!(du < thr)) {
             sev = violation_severity(vmax, dm, dw);
             const double sc = smax(smax(fabs(u0), du), 1e-300);
@@ -160,10 +190,13 @@ __global__ void __launch_bounds__(kBlock) k_central_tma(Layout L, Physics ph, Sc
         if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
       }
     }
-    __syncthreads();  // stage `st` fully consumed before it is refilled
+    __syncthreads();  // group B consumed
+    if (tid == 0 && refill < nchunks) {
+      fence_proxy_async_smem();
+      issue_b(refill, st);
+    }
   }
 }
-
 
 template <int K, int NQ, int NF, int MM, int MD>
 struct TroubledStage {

@@ -396,9 +396,25 @@ ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_expon
     std::vector<std::vector<double>> pinv_dir;
     std::vector<int32_t> slots;
   };
-  std::vector<CellOut> outs(n);
+  S->central_ptr.assign(1, 0);
+  S->pinv_off.assign(1, 0);
+  S->pinv_lin_off.assign(1, 0);
+  S->dir_ptr.assign(1, 0);
+  S->dir_member_ptr.assign(1, 0);
+  S->pinv_dir_off.assign(1, 0);
+  S->qp_ptr.assign(1, 0);
+  S->phi_off.assign(1, 0);
+  // cells are built in blocks (parallel inside a block) and appended in cell
+  // order, so peak memory is the final arrays plus one block of scratch
+  const int64_t block = std::max<int64_t>(4096, 1 << 16);
+  std::vector<CellOut> outs;
+  for (int64_t b0 = 0; b0 < n; b0 += block) {
+  const int64_t b1 = std::min<int64_t>(n, b0 + block);
+  outs.assign(static_cast<size_t>(b1 - b0), CellOut{});
 
-  parallel_for(n, n_threads, [&](int64_t a0, int64_t a1) {
+  parallel_for(b1 - b0, n_threads, [&](int64_t a0, int64_t a1) {
+    a0 += b0;
+    a1 += b0;
     std::vector<Entry> central;
     std::vector<double> A, A1, pinv, pl, pd;
     std::vector<Vec2> ref_poly;
@@ -406,7 +422,7 @@ ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_expon
     std::vector<std::vector<int>> dirs;
     double d[64], psi[64];
     for (int c = static_cast<int>(a0); c < static_cast<int>(a1); ++c) {
-      CellOut& o = outs[c];
+      CellOut& o = outs[c - b0];
       B.member_poly(c, {c, 0, 0}, ref_poly);
       // basis means over the reference cell (build_basis, basis.cpp:125-137)
       const double rarea = polygon_signed_area(ref_poly);
@@ -501,29 +517,6 @@ ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_expon
     }
   });
 
-  // concatenate in cell order
-  S->central_ptr.assign(1, 0);
-  S->pinv_off.assign(1, 0);
-  S->pinv_lin_off.assign(1, 0);
-  S->dir_ptr.assign(1, 0);
-  S->dir_member_ptr.assign(1, 0);
-  S->pinv_dir_off.assign(1, 0);
-  S->qp_ptr.assign(1, 0);
-  S->phi_off.assign(1, 0);
-  size_t tc = 0, tp = 0, tl = 0, tph = 0, ts = 0;
-  for (const auto& o : outs) {
-    tc += o.central.size();
-    tp += o.pinv.size();
-    tl += o.pinv_lin.size();
-    tph += o.phi.size();
-    ts += o.slots.size();
-  }
-  S->central.reserve(tc);
-  S->pinv.reserve(tp);
-  S->pinv_lin.reserve(tl);
-  S->phi.reserve(tph);
-  S->qp_slot.reserve(ts);
-  S->oi.reserve(static_cast<size_t>(n) * K * K);
   for (auto& o : outs) {
     S->central.insert(S->central.end(), o.central.begin(), o.central.end());
     S->central_ptr.push_back(static_cast<int64_t>(S->central.size() / 3));
@@ -545,6 +538,7 @@ ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_expon
     S->qp_ptr.push_back(static_cast<int64_t>(S->qp_slot.size()));
     o = CellOut{};
   }
+  }  // blocks
   return S.release();
 }
 

@@ -110,7 +110,7 @@ struct KernelSet {
 using StageLaunch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
 
 template <typename St>
-constexpr uint32_t tma_smem(int stages) { return stages * St::BYTES + 8 * stages; }
+constexpr uint32_t tma_smem(int stages) { return stages * St::BYTES + 16 * stages; }
 
 template <int K, int NQ, int NF, int MM, int NS>
 void central_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
@@ -269,6 +269,8 @@ struct GpuSolver::Impl {
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
 
+  size_t l2_window_bytes = 0, l2_persist_bytes = 0;
+  bool per_cell_lists = false;  // UCFVB_TROUBLED=lists: dense per-cell class lists instead of chunk lists
   dim3 grid_owned4() const { return dim3((4 * L.n_owned + kBlock - 1) / kBlock); }
 
   // halo exchange of a stage state: pack per peer, then one grouped send/recv
@@ -328,7 +330,7 @@ struct GpuSolver::Impl {
       if (detect) CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream));
       ks.central(grid_central(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
       record(1);
-      if (ks.troubled) {
+      if (ks.troubled && !per_cell_lists) {
         ks.spread(grid_cells(), stream, L, S, U, taps | FL_CHUNKS, detect ? 1 : 0);
         record(2);
         ks.troubled(dim3(std::min(ks.troubled_grid, (L.n + 31) / 32)), stream, L, ph, S, U,
@@ -584,6 +586,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   bool uniform = true;
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
   I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
+  if (const char* tl = std::getenv("UCFVB_TROUBLED")) I.per_cell_lists = std::strcmp(tl, "lists") == 0;
   if (I.ks.central_tma) {
     const char* e1 = std::getenv("UCFVB_TMA_STAGES_CENTRAL");
     const char* e2 = std::getenv("UCFVB_TMA_STAGES_TROUBLED");
@@ -619,6 +622,14 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   L.h = dupload(H.h, own);
   L.inv_vol = dupload(H.inv_vol, own);
 
+  // the operator data now lives on the device: keep only what the taps need
+  {
+    HostLayout& Hm = I.host;
+    auto drop = [](auto& v) { std::remove_reference_t<decltype(v)>().swap(v); };
+    drop(Hm.st_idx); drop(Hm.pinv); drop(Hm.phi); drop(Hm.phi01); drop(Hm.pinv_lin); drop(Hm.dir_idx);
+    drop(Hm.pinv_dir); drop(Hm.oi); drop(Hm.nbr); drop(Hm.cface); drop(Hm.fnx); drop(Hm.fny); drop(Hm.flen);
+    drop(Hm.fkind); drop(Hm.fpatch); drop(Hm.deact_thr); drop(Hm.eps2); drop(Hm.h); drop(Hm.inv_vol);
+  }
   ph.mp = MarginParams{mg.alpha_m, mg.beta_m, mg.alpha_w, mg.beta_w, mg.kappa, mg.deact_n};
   ph.gamma = o.gamma;
   ph.lambda1p = o.lambda1p;
@@ -631,9 +642,37 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   const size_t nch = static_cast<size_t>(H.n_pad / 32);
   Scratch& S = I.S;
   const size_t n_fp = 2 * static_cast<size_t>(H.n_faces) * H.NQ + 1;  // + scratch slot for padded qps
-  S.fp = dalloc<double4>(n_fp, own);
-  S.ff = dalloc<double4>(std::max(1, H.n_faces), own);
-  S.dofs = dalloc<double4>(nch * H.K * 32, own);
+  // face points, face fluxes and dofs are produced and consumed within one
+  // stage: one allocation, so one L2 access-policy window can keep them resident
+  const size_t n_ff = std::max<size_t>(1, H.n_faces), n_dofs = nch * H.K * 32;
+  double4* stage_buf = dalloc<double4>(n_fp + n_ff + n_dofs, own);
+  S.fp = stage_buf;
+  S.ff = stage_buf + n_fp;
+  S.dofs = stage_buf + n_fp + n_ff;
+  {
+    const char* e = std::getenv("UCFVB_L2_PERSIST");
+    const bool want = !(e && e[0] == '0');
+    int max_persist = 0, max_window = 0;
+    CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+    CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
+    const size_t bytes = (n_fp + n_ff + n_dofs) * sizeof(double4);
+    if (want && max_persist > 0 && max_window > 0) {
+      size_t limit = 0;
+      CK(cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize));
+      const size_t persist = std::min<size_t>(max_persist, std::max(limit, bytes));
+      CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = stage_buf;
+      attr.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, max_window);
+      attr.accessPolicyWindow.hitRatio =
+          static_cast<float>(std::min(1.0, static_cast<double>(persist) / attr.accessPolicyWindow.num_bytes));
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      CK(cudaStreamSetAttribute(I.stream, cudaStreamAttributeAccessPolicyWindow, &attr));
+      I.l2_window_bytes = attr.accessPolicyWindow.num_bytes;
+      I.l2_persist_bytes = persist;
+    }
+  }
   S.raw = dalloc<uint8_t>(H.n_pad, own);
   S.labels = dalloc<uint8_t>(H.n_pad, own);
   S.step_labels = dalloc<uint8_t>(H.n_pad, own);

@@ -21,7 +21,9 @@
 //               (solver.cpp:266-292)
 //   k_gather_rk owner-ordered face-to-cell gather (no atomics) fused with the
 //               RK stage update (solver.cpp:294-311, time_integrator.cpp:31-38,70-73)
-//   k_dt        max_stable_dt min-reduction (solver.cpp:103-111) + device-side t/dt
+//   k_dt        max_stable_dt min-reduction (solver.cpp:103-111) for a run's first
+//               step; later steps reduce it inside the previous final k_gather_rk;
+//               k_dt_finalize turns it into the step's dt (device-side t/dt)
 #pragma once
 
 #include <cstdint>
@@ -31,7 +33,7 @@
 namespace ucfvb {
 
 enum : int { FL_DOFS = 1, FL_EVAL = 2, FL_NAD = 4, FL_PRECHECK = 8, FL_TAPS = 16, FL_FALLBACK = 32,
-             FL_CENSUS = 64, FL_STEP_LABELS = 128, FL_CHUNKS = 256 };
+             FL_CENSUS = 64, FL_STEP_LABELS = 128, FL_CHUNKS = 256, FL_DT = 512 };
 
 constexpr int kMaxPatches = 16;
 constexpr int kBlock = 128;
@@ -570,6 +572,89 @@ __global__ void __launch_bounds__(kBlock) k_constant(Layout L, Scratch S, const 
 }
 
 // ---------------------------------------------------------------------------
+// max_stable_dt support (solver.cpp:103-111) + device-side t/dt of run_steps
+struct DtState {
+  unsigned long long dmin_bits;  // running min of h/speed (positive doubles order as integers)
+  int dt_bad;   // a cell's state was non-physical when its h/speed was taken
+  int step;     // steps completed in this run (census row)
+  double t;     // time at the start of the current step
+  double dt;    // dt of the current step
+  double t_end;
+  double cfl;
+  double dmin;  // collected min(h/speed) (all-reduced across ranks before k_dt_finalize)
+};
+
+// max_stable_dt's per-cell term (solver.cpp:103-111): h_c / (|u| + |v| + a)
+__device__ __forceinline__ bool dt_term(const double* s, double gamma, double h, double& x) {
+  double rho, u, v, p;
+  if (!cons_to_prim(s, gamma, rho, u, v, p)) return false;
+  const double speed = fabs(u) + fabs(v) + sqrt(gamma * p / rho);
+  x = h / speed;
+  return true;
+}
+
+// block-wide min of x folded into ds->dmin_bits (every thread of the block must call)
+__device__ __forceinline__ void block_min_into(double x, DtState* ds) {
+  __shared__ double red[kBlock / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = smin(x, __shfl_xor_sync(0xffffffffu, x, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = red[0];
+    for (int i = 1; i < static_cast<int>(blockDim.x >> 5); ++i) b = smin(b, red[i]);
+    if (b < 1e300) atomicMin(&ds->dmin_bits, static_cast<unsigned long long>(__double_as_longlong(b)));
+  }
+}
+
+// min over owned cells of h/speed into ds->dmin_bits (the first step of a run;
+// later steps get it from the previous step's final k_gather_rk)
+__global__ void __launch_bounds__(kBlock) k_dt(Layout L, const double4* __restrict__ U, double gamma, DtState* ds,
+                                               int* err) {
+  if (*(volatile int*)err) return;  // block-uniform
+  const int c = blockIdx.x * kBlock + threadIdx.x;
+  double x = 1e300;
+  if (c < L.n_owned) {
+    const d4 s = ld4(&U[c]);
+    if (!dt_term(s.v, gamma, L.h[c], x)) {
+      x = 1e300;
+      ds->dt_bad = 1;
+      atomicMin(&err[2], c);
+    }
+  }
+  block_min_into(x, ds);
+}
+
+// collect the reduced min (and reset the accumulator)
+__device__ __forceinline__ void dt_collect(DtState* ds) {
+  ds->dmin = __longlong_as_double(static_cast<long long>(ds->dmin_bits));
+  ds->dmin_bits = static_cast<unsigned long long>(__double_as_longlong(1e300));
+}
+
+// start of a step: raise a pending dt failure (max_stable_dt throws before the
+// step touches the state) or advance t by the previous dt and set this step's
+// dt = min(cfl * dmin, t_end - t) (run.cpp:97-132, solver.cpp:110)
+__device__ __forceinline__ void dt_finalize(DtState* ds, int* err) {
+  if (ds->dt_bad) {
+    atomicOr(&err[0], 2);
+    atomicMin(&err[3], ds->step + 1);
+    return;
+  }
+  ds->t = ds->t + ds->dt;  // 0 before the first step
+  ds->step += 1;
+  const double dt = ds->cfl * ds->dmin;
+  ds->dt = smin(dt, ds->t_end - ds->t);
+}
+
+__global__ void k_dt_collect(DtState* ds) { dt_collect(ds); }
+
+__global__ void k_dt_finalize(DtState* ds, int* err, int collect) {
+  if (*(volatile int*)err) return;
+  if (collect) dt_collect(ds);
+  dt_finalize(ds, err);
+}
+
+// ---------------------------------------------------------------------------
 // k_face_flux: assemble_fluxes pass 1 (solver.cpp:266-292). One lane per
 // (face, Gauss point), NQ consecutive lanes per face: UL/UR are read as one
 // contiguous 64 B pair from the face-major fp array, the Riemann flux is
@@ -635,7 +720,8 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
 // time_integrator.cpp:31-38; final SSPRK(5,4) line :70-73). Owner-ordered:
 // no atomics.
 template <int NF, bool UNI>
-__global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags) {
+__global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags, DtState* ds,
+                                                      double gamma) {
   const int g = blockIdx.x * kBlock + threadIdx.x;
   const int v = g & 3;
   const int c0 = g >> 2;
@@ -672,12 +758,10 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
       }
     }
   }
-  if (!live || err0) return;
   const double r = -acc * inv_vol;
-  if (rk.rhs_out) reinterpret_cast<double*>(rk.rhs_out + c)[v] = r;
+  double o = 0.0;
   if (rk.out) {
     const double dt = rk.nterms ? *rk.dt : 0.0;
-    double o = 0.0;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       if (i < rk.nterms) {
@@ -686,82 +770,26 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
         o = (i == 0) ? w * x : o + w * x;
       }
     }
-    reinterpret_cast<double*>(rk.out + c)[v] = o;
+  }
+  if (live && !err0) {
+    if (rk.rhs_out) reinterpret_cast<double*>(rk.rhs_out + c)[v] = r;
+    if (rk.out) reinterpret_cast<double*>(rk.out + c)[v] = o;
+  }
+  if (flags & FL_DT) {  // max_stable_dt of the new state, for the next step (block-uniform branch)
+    double s4[NV];
+#pragma unroll
+    for (int jv = 0; jv < NV; ++jv) s4[jv] = grp_get(o, jv);
+    double x = 1e300;
+    if (v == 0 && live && !err0 && !dt_term(s4, gamma, L.h[c], x)) {
+      x = 1e300;
+      ds->dt_bad = 1;
+      atomicMin(&S.err[2], c);
+    }
+    block_min_into(x, ds);
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_dt: max_stable_dt (solver.cpp:103-111) as a min-reduction over cells; the
-// last block turns it into this step's dt = min(cfl*min, t_end - t)
-// (run.cpp:100) and advances the device clock by the previous dt.
-struct DtState {
-  unsigned long long dmin_bits;  // running min of h/speed (positive doubles order as integers)
-  unsigned int blocks_done;
-  int step;     // steps completed in this run (census row)
-  double t;     // time at the start of the current step
-  double dt;    // dt of the current step
-  double t_end;
-  double cfl;
-  double dmin;  // this rank's min(h/speed) (all-reduced across ranks before k_dt_finalize)
-};
-
-__device__ __forceinline__ void dt_finalize(DtState* ds, double dmin) {
-  // run.cpp:97-132: t advances by the previous dt (0 before the first step)
-  ds->t = ds->t + ds->dt;
-  ds->step += 1;
-  const double dt = ds->cfl * dmin;  // solver.cpp:110
-  ds->dt = smin(dt, ds->t_end - ds->t);
-}
-
-// finalize: 1 = single rank (the last block turns the min into dt), 0 = leave
-// ds->dmin for a cross-rank min all-reduce followed by k_dt_finalize
-__global__ void __launch_bounds__(256) k_dt(Layout L, const double4* __restrict__ U, double gamma, DtState* ds,
-                                            int* err, int finalize) {
-  __shared__ double red[8];
-  __shared__ bool last;
-  if (*(volatile int*)err) return;  // a previous kernel failed: freeze the run
-  const int c = blockIdx.x * 256 + threadIdx.x;
-  double x = 1e300;
-  if (c < L.n_owned) {
-    const d4 s = ld4(&U[c]);
-    double rho, u, v, p;
-    if (cons_to_prim(s.v, gamma, rho, u, v, p)) {
-      const double speed = fabs(u) + fabs(v) + sqrt(gamma * p / rho);
-      x = L.h[c] / speed;
-    } else {
-      atomicOr(&err[0], 2);
-      atomicMin(&err[2], c);
-      atomicMin(&err[3], ds->step + 1);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = smin(x, __shfl_xor_sync(0xffffffffu, x, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = red[0];
-    for (int i = 1; i < 8; ++i) b = smin(b, red[i]);
-    atomicMin(&ds->dmin_bits, static_cast<unsigned long long>(__double_as_longlong(b)));
-    __threadfence();
-    const unsigned done = atomicAdd(&ds->blocks_done, 1u);
-    last = (done == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    const double dmin = __longlong_as_double(static_cast<long long>(atomicAdd(&ds->dmin_bits, 0ull)));
-    ds->dmin = dmin;
-    if (finalize) dt_finalize(ds, dmin);
-    ds->dmin_bits = static_cast<unsigned long long>(__double_as_longlong(1e300));
-    ds->blocks_done = 0;
-  }
-}
-
-__global__ void k_dt_finalize(DtState* ds, const int* err) {
-  if (*(volatile const int*)err) return;
-  dt_finalize(ds, ds->dmin);
-}
-
 // pack the owned cells a peer needs into a contiguous send buffer
 __global__ void __launch_bounds__(256) k_halo_pack(const double4* __restrict__ U, const int* __restrict__ idx, int n,
                                                    double4* __restrict__ out) {

@@ -94,7 +94,7 @@ struct KernelSet {
   void (*muscl)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
   void (*constant)(dim3, cudaStream_t, const Layout&, const Scratch&, const double4*);
   void (*face_flux)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&);
-  void (*gather)(dim3, cudaStream_t, const Layout&, const Scratch&, const RkEpilogue&, int);
+  void (*gather)(dim3, cudaStream_t, const Layout&, const Scratch&, const RkEpilogue&, int, DtState*, double);
   int faces_per_flux_block;
   // TMA-staged persistent central kernel (fast path); grid filled in at create
   bool central_tma = false;
@@ -157,9 +157,8 @@ KernelSet make_set() {
   s.face_flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S) {
     k_face_flux<NQ><<<g, kBlock, 0, st>>>(L, p, S);
   };
-  s.gather = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const RkEpilogue& rk, int f) {
-    k_gather_rk<NF, UNI><<<g, kBlock, 0, st>>>(L, S, rk, f);
-  };
+  s.gather = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const RkEpilogue& rk, int f, DtState* ds,
+                 double gamma) { k_gather_rk<NF, UNI><<<g, kBlock, 0, st>>>(L, S, rk, f, ds, gamma); };
   s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
   if constexpr (MMT > 0 && UNI) {
     s.central_tma = true;
@@ -293,12 +292,20 @@ struct GpuSolver::Impl {
     return nl;
   }
 
-  // this step's dt: per-rank min, then (decomposed) a min all-reduce
-  int64_t launch_dt(const double4* src) {
-    k_dt<<<dim3((L.n_owned + 255) / 256), 256, 0, stream>>>(L, src, opt.gamma, ds, S.err, comm ? 0 : 1);
-    if (!comm) return 1;
+  // min(h/speed) over the owned cells of `src` into ds->dmin_bits
+  int64_t launch_dt_reduce(const double4* src) {
+    k_dt<<<dim3((L.n_owned + kBlock - 1) / kBlock), kBlock, 0, stream>>>(L, src, opt.gamma, ds, S.err);
+    return 1;
+  }
+  // turn the reduced min into this step's dt (on subdomains after a min all-reduce)
+  int64_t launch_dt_finalize() {
+    if (!comm) {
+      k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err, 1);
+      return 1;
+    }
+    k_dt_collect<<<1, 1, 0, stream>>>(ds);
     NK(nccl().AllReduce(&ds->dmin, &ds->dmin, 1, ncclDouble, ncclMin, comm, stream));
-    k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err);
+    k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err, 0);
     return 2;
   }
 
@@ -319,7 +326,8 @@ struct GpuSolver::Impl {
   }
 
   // one compute_residual stage on the stream (solver.cpp:316-379)
-  int64_t launch_stage(const double4* U, bool first, const RkEpilogue& rk, bool census) {
+  // dt_next: this stage's output starts the next step; reduce its max_stable_dt term
+  int64_t launch_stage(const double4* U, bool first, const RkEpilogue& rk, bool census, bool dt_next = false) {
     int64_t nl = 0;
     const int taps = opt.keep_taps ? FL_TAPS : 0;
     const int mode = opt.mode;
@@ -369,7 +377,7 @@ struct GpuSolver::Impl {
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
     ks.face_flux(dim3((L.n_faces + ks.faces_per_flux_block - 1) / ks.faces_per_flux_block), stream, L, ph, S);
-    ks.gather(grid_owned4(), stream, L, S, rk, ff);
+    ks.gather(grid_owned4(), stream, L, S, rk, ff | (dt_next ? FL_DT : 0), ds, opt.gamma);
     ++nl;
     record(4);
     CK(cudaGetLastError());
@@ -398,7 +406,7 @@ struct GpuSolver::Impl {
   int64_t launch_step(int rk, bool with_dt, const double4* src, double4* dst, bool census) {
     int64_t nl = 0;
     const double* dt = &ds->dt;
-    if (with_dt) nl += launch_dt(src);
+    if (with_dt) nl += launch_dt_finalize();  // dmin of src: k_dt (first step) or the previous final gather
     if (rk == UCFVB_RK3) {
       double4 *u1 = work[0], *u2 = work[1];
       RkEpilogue e1{};
@@ -423,7 +431,7 @@ struct GpuSolver::Impl {
       add_term(e3, src, 1.0 / 3.0, false);
       add_term(e3, u2, 2.0 / 3.0, false);
       add_term(e3, nullptr, 2.0 / 3.0, true);
-      nl += launch_stage(u2, false, e3, census);
+      nl += launch_stage(u2, false, e3, census, with_dt);
       nl += exchange(dst);
     } else {
       using namespace rk54;
@@ -469,7 +477,7 @@ struct GpuSolver::Impl {
       add_term(e, r3, a53, true);
       add_term(e, ud, c54, false);
       add_term(e, nullptr, a54, true);
-      nl += launch_stage(ud, false, e, census);
+      nl += launch_stage(ud, false, e, census, with_dt);
       nl += exchange(dst);
     }
     return nl;
@@ -756,7 +764,7 @@ double GpuSolver::max_stable_dt() {
   h.t_end = INFINITY;
   h.cfl = I.opt.cfl;
   CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
-  I.launches = I.launch_dt(I.ubuf[I.cur]);
+  I.launches = I.launch_dt_reduce(I.ubuf[I.cur]) + I.launch_dt_finalize();
   CK(cudaGetLastError());
   I.allreduce_error();
   CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
@@ -831,7 +839,8 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
   I.S.step = &I.ds->step;
   const bool graphs = I.opt.use_graphs && !I.timing;
   const int cur0 = I.cur;
-  int64_t nl = 0;
+  // the first step's max_stable_dt term; each step's final gather reduces the next one
+  int64_t nl = I.launch_dt_reduce(I.ubuf[I.cur]);
   for (int s = 0; s < n_steps; ++s) {
     if (graphs) {
       // graphs capture the census flag; keep separate graphs only for census runs

@@ -234,13 +234,15 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
   bool bad = false;
   const double* fp = L.phi + aos(c, 0, Q * K);
   double* fv = reinterpret_cast<double*>(S.fp);
+  double vals[Q];
 #pragma unroll
   for (int lq = 0; lq < Q; ++lq) {
+    vals[lq] = u0;
     if (lq < nf * NQ) {
       double val = u0;
 #pragma unroll
       for (int k = 0; k < K; ++k) val += acc[k] * __ldg(fp + (lq * K + k) * 32);
-      if (live) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = val;
+      vals[lq] = val;
       if (detect) {
         double s[NV];
 #pragma unroll
@@ -252,10 +254,9 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
       }
     }
   }
-  if (!detect) return;
   int sev = 0;
   bool tie = false;
-  if ((flags & FL_NAD) && (v == 0 || v == 3)) {
+  if (detect && (flags & FL_NAD) && (v == 0 || v == 3)) {
     const double thr = L.deact_thr[c];
     if (!(du < thr)) {  // deactivate_smooth (detector.cpp:32-35)
       sev = violation_severity(vmax, dm, dw);
@@ -264,14 +265,22 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
     }
     if (thr > 0.0) tie |= fabs(du - thr) <= 1e-12 * thr;
   }
-  sev = grp_max(sev);
-  bad = grp_any(bad);
-  tie = grp_any(tie);
-  if (flags & FL_NAD) {
-    const unsigned tm = __ballot_sync(kFull, tie && v == 0 && live);
-    if (tm && (threadIdx.x & 31) == __ffs(tm) - 1) atomicAdd(S.ties, static_cast<unsigned long long>(__popc(tm)));
+  if (detect) {
+    sev = grp_max(sev);
+    bad = grp_any(bad);
+    tie = grp_any(tie);
+    if (flags & FL_NAD) {
+      const unsigned tm = __ballot_sync(kFull, tie && v == 0 && live);
+      if (tm && (threadIdx.x & 31) == __ffs(tm) - 1) atomicAdd(S.ties, static_cast<unsigned long long>(__popc(tm)));
+    }
+    if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
   }
-  if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
+  // a raw label >= CWENOZ survives the spread: the troubled kernels rewrite these face points
+  if (live && !((flags & FL_NAD) && sev >= 1)) {
+#pragma unroll
+    for (int lq = 0; lq < Q; ++lq)
+      if (lq < nf * NQ) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = vals[lq];
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -152,12 +152,14 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
       compute_margins(ph.mp, du, dm, dw);
       double vmax = -1e300;
       bool bad = false;
+      bool store = true;
+      double vals[Q];
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) {
         double val = u0;
 #pragma unroll
         for (int k = 0; k < K; ++k) val += acc[k] * sf[(lq * K + k) * 32 + slot];
-        if (live) fv[4 * static_cast<size_t>(sdst[lq * 32 + slot]) + v] = val;
+        vals[lq] = val;
         if (detect) {
           double s4[NV];
 #pragma unroll
@@ -188,6 +190,13 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
           if (tm && (tid & 31) == __ffs(tm) - 1) atomicAdd(S.ties, static_cast<unsigned long long>(__popc(tm)));
         }
         if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
+        // a raw label >= CWENOZ survives the spread (it only raises labels): the
+        // troubled kernel rewrites this cell's face points, so the candidates are dead
+        store = !((flags & FL_NAD) && sev >= 1);
+      }
+      if (live && store) {
+#pragma unroll
+        for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(sdst[lq * 32 + slot]) + v] = vals[lq];
       }
     }
     __syncthreads();  // group B consumed

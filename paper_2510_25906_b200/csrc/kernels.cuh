@@ -147,6 +147,41 @@ __device__ __forceinline__ int grp_max(int s) {
   return s;
 }
 
+__device__ __forceinline__ double pick4(double a, double b, double c, double d, int i) {
+  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
+}
+
+// is_physical (euler.hpp:34-36) of the cell's Q face points without the 4x
+// redundancy: lane v holds variable v of every point; a 4x4 transpose through
+// rotated shuffles hands lane v all four variables of points v, v+4, ... and
+// each lane checks only those. Returns this lane's verdict (OR over the group
+// with grp_any).
+template <int Q>
+__device__ __forceinline__ bool group_nonphysical(const double* vals, int nq_cell, double gamma) {
+  const int v = threadIdx.x & 3;
+  const int base = (threadIdx.x & 31) & ~3;
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < (Q + 3) / 4; ++r) {
+    double t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // step k: send point 4r + ((v - k) & 3), receive variable (v + k) & 3 of point 4r + v
+      const int si = (v - k) & 3;
+      double send = 1.0;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i == si && 4 * r + i < Q) send = vals[4 * r + i];
+      t[k] = __shfl_sync(kFull, send, base | ((v + k) & 3));
+    }
+    double st[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) st[j] = pick4(t[0], t[1], t[2], t[3], (j - v) & 3);
+    if (4 * r + v < nq_cell) bad |= !is_physical(st, gamma);
+  }
+  return bad;
+}
+
 // neighbourhood bounds of this lane's variable over {c} U face neighbours
 // (solver.cpp:120-129, 207-211)
 template <int NF>
@@ -244,16 +279,13 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
       for (int k = 0; k < K; ++k) val += acc[k] * __ldg(fp + (lq * K + k) * 32);
       vals[lq] = val;
       if (detect) {
-        double s[NV];
-#pragma unroll
-        for (int j = 0; j < NV; ++j) s[j] = grp_get(val, j);
-        bad |= !is_physical(s, ph.gamma);
         const double x = smax(lo - val, val - hi);
         vmax = smax(vmax, x);
         if (v == 0 || v == 3) bad |= x > dm;
       }
     }
   }
+  if (detect) bad |= group_nonphysical<Q>(vals, nf * NQ, ph.gamma);
   int sev = 0;
   bool tie = false;
   if (detect && (flags & FL_NAD) && (v == 0 || v == 3)) {

@@ -161,16 +161,13 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
         for (int k = 0; k < K; ++k) val += acc[k] * sf[(lq * K + k) * 32 + slot];
         vals[lq] = val;
         if (detect) {
-          double s4[NV];
-#pragma unroll
-          for (int jv = 0; jv < NV; ++jv) s4[jv] = grp_get(val, jv);
-          bad |= !is_physical(s4, ph.gamma);
           const double x = smax(lo - val, val - hi);
           vmax = smax(vmax, x);
           if (v == 0 || v == 3) bad |= x > dm;
         }
       }
       if (detect) {
+        bad |= group_nonphysical<Q>(vals, Q, ph.gamma);
         int sev = 0;
         bool tie = false;
         if ((flags & FL_NAD) && (v == 0 || v == 3)) {

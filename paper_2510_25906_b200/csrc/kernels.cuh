@@ -66,6 +66,7 @@ struct Layout {
   const double* flen;       // [n_faces] length
   const int8_t* fkind;      // [n_faces] 0: two-sided flux face, 1: boundary condition, 2: periodic secondary (skipped)
   const int8_t* fpatch;     // [n_faces] boundary patch
+  const int* fslot;         // [n_faces][2] residual slot (aos(cell, j, NF)) of the left / right owner, -1 none
   const uint8_t* nfc;       // [n] faces per cell
   const double* deact_thr;  // [n] (kappa*h)^n or -inf
   const double* eps2;       // [n] (venkat_kappa*h)^3
@@ -85,7 +86,7 @@ struct Physics {
 struct Scratch {
   double4* fp;       // face-point values [face][q][side]: the reference's val_left_/val_right_
                      // slots (periodic partners' values land in the primary face's right slot)
-  double4* ff;       // integrated flux per face (face_flux_)
+  double4* rs;       // +-face_flux_ per cell-face slot [chunk][NF][lane] (the gather's terms, in face order)
   double4* dofs;     // [chunk][K][lane]
   uint8_t* raw;      // raw NAD label | demote-if-linear << 2
   uint8_t* labels;
@@ -747,10 +748,15 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
     for (int v = 0; v < NV; ++v) total[v] += __shfl_sync(kFull, t[v], min(g0 + qq, 31));
   if (kind == 2 || q != 0 || err0) return;
   const double len = L.flen[f];
-  double o[NV];
+  double o[NV], m[NV];
 #pragma unroll
-  for (int v = 0; v < NV; ++v) o[v] = total[v] * len;
-  st4(&S.ff[f], o);
+  for (int v = 0; v < NV; ++v) {
+    o[v] = total[v] * len;  // face_flux_ (solver.cpp:292)
+    m[v] = -1.0 * o[v];     // sgn * face_flux_ for the right / periodic-secondary owner (solver.cpp:301-306)
+  }
+  const int sl = L.fslot[2 * f], sr = L.fslot[2 * f + 1];
+  if (sl >= 0) st4(&S.rs[sl], o);
+  if (sr >= 0) st4(&S.rs[sr], m);
 }
 
 // ---------------------------------------------------------------------------
@@ -770,22 +776,19 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
   const bool live = c0 < L.n_owned;
   const int c = live ? c0 : L.n_owned - 1;
   const int err0 = *(volatile int*)S.err;
-  const double* ffd = reinterpret_cast<const double*>(S.ff);
+  const double* rsd = reinterpret_cast<const double*>(S.rs);
   double term[5];
 #pragma unroll
   for (int i = 0; i < 5; ++i)
     term[i] = (i < rk.nterms && rk.term[i]) ? __ldg(reinterpret_cast<const double*>(rk.term[i] + c) + v) : 0.0;
   const double inv_vol = L.inv_vol[c];
   const int nf = UNI ? NF : L.nfc[c];
+  // acc += sgn * face_flux_ in the cell's face order; the signed terms were
+  // scattered into this cell's slots by k_face_flux (coalesced reads here)
   double acc = 0.0;
 #pragma unroll
-  for (int j = 0; j < NF; ++j) {
-    if (j < nf) {
-      const int e = __ldg(L.cface + aos(c, j, NF));
-      const double x = ffd[4 * static_cast<size_t>(e >> 1) + v];
-      acc += ((e & 1) ? -1.0 : 1.0) * x;
-    }
-  }
+  for (int j = 0; j < NF; ++j)
+    if (j < nf) acc += rsd[4 * aos(c, j, NF) + v];
   if (flags & (FL_CENSUS | FL_STEP_LABELS)) {
     const bool leader = live && v == 0;
     const int lab = leader ? S.labels[c] : -1;

@@ -98,6 +98,7 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
   L.fny.assign(m.n_faces, 0.0);
   L.flen.assign(m.n_faces, 0.0);
   L.fkind.assign(m.n_faces, 0);
+  L.fslot.assign(2 * static_cast<size_t>(m.n_faces), -1);
   L.fpatch.assign(m.n_faces, 0);
   for (int f = 0; f < m.n_faces; ++f) {
     L.fnx[f] = m.face_normal[2 * f];
@@ -221,6 +222,8 @@ HostLayout build_layout(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, c
           L.dest[aos_index(c, j * NQ + q, Q)] = static_cast<int32_t>(slot);
         }
         L.cface[aos_index(c, j, NF)] = (canon << 1) | neg;
+        // the canonical face's flux lands in this cell's slot j with the gather's sign
+        L.fslot[2 * static_cast<size_t>(canon) + neg] = static_cast<int32_t>(aos_index(c, j, NF));
       }
     }
   });

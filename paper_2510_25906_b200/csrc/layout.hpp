@@ -25,6 +25,7 @@ struct HostLayout {
   // face arrays (canonical orientation) and the face-major face-point slots
   std::vector<double> fnx, fny, flen;
   std::vector<int8_t> fkind, fpatch;
+  std::vector<int32_t> fslot;  // [n_faces][2] residual slots of the face's owners
   std::vector<double> deact_thr, eps2, h, inv_vol;
   double qw[4] = {0, 0, 0, 0};
   // reference slot of each cell-local qp, for the val_left_/val_right_ tap

@@ -624,6 +624,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   L.flen = dupload(H.flen, own);
   L.fkind = dupload(H.fkind, own);
   L.fpatch = dupload(H.fpatch, own);
+  L.fslot = dupload(H.fslot, own);
   L.nfc = dupload(H.nfc, own);
   L.deact_thr = dupload(H.deact_thr, own);
   L.eps2 = dupload(H.eps2, own);
@@ -636,7 +637,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
     auto drop = [](auto& v) { std::remove_reference_t<decltype(v)>().swap(v); };
     drop(Hm.st_idx); drop(Hm.pinv); drop(Hm.phi); drop(Hm.phi01); drop(Hm.pinv_lin); drop(Hm.dir_idx);
     drop(Hm.pinv_dir); drop(Hm.oi); drop(Hm.nbr); drop(Hm.cface); drop(Hm.fnx); drop(Hm.fny); drop(Hm.flen);
-    drop(Hm.fkind); drop(Hm.fpatch); drop(Hm.deact_thr); drop(Hm.eps2); drop(Hm.h); drop(Hm.inv_vol);
+    drop(Hm.fkind); drop(Hm.fpatch); drop(Hm.fslot); drop(Hm.deact_thr); drop(Hm.eps2); drop(Hm.h); drop(Hm.inv_vol);
   }
   ph.mp = MarginParams{mg.alpha_m, mg.beta_m, mg.alpha_w, mg.beta_w, mg.kappa, mg.deact_n};
   ph.gamma = o.gamma;
@@ -652,10 +653,10 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   const size_t n_fp = 2 * static_cast<size_t>(H.n_faces) * H.NQ + 1;  // + scratch slot for padded qps
   // face points, face fluxes and dofs are produced and consumed within one
   // stage: one allocation, so one L2 access-policy window can keep them resident
-  const size_t n_ff = std::max<size_t>(1, H.n_faces), n_dofs = nch * H.K * 32;
+  const size_t n_ff = nch * H.NF * 32, n_dofs = nch * H.K * 32;
   double4* stage_buf = dalloc<double4>(n_fp + n_ff + n_dofs, own);
   S.fp = stage_buf;
-  S.ff = stage_buf + n_fp;
+  S.rs = stage_buf + n_fp;
   S.dofs = stage_buf + n_fp + n_ff;
   {
     const char* e = std::getenv("UCFVB_L2_PERSIST");
@@ -694,7 +695,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   I.step_zero = dalloc<int>(1, own);
   CK(cudaMemset(I.step_zero, 0, sizeof(int)));
   CK(cudaMemset(S.fp, 0, n_fp * sizeof(double4)));
-  CK(cudaMemset(S.ff, 0, std::max(1, H.n_faces) * sizeof(double4)));
+  CK(cudaMemset(S.rs, 0, n_ff * sizeof(double4)));
   CK(cudaMemset(S.dofs, 0, nch * H.K * 32 * sizeof(double4)));
   CK(cudaMemset(S.ties, 0, sizeof(unsigned long long)));
   CK(cudaMemset(S.raw, 0, H.n_pad));

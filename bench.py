@@ -124,15 +124,22 @@ class ClockSampler:
 # ---------------------------------------------------------------- roofline model
 def kernel_bytes(K, NQ, NF, MM, MD):
     """Algorithmic HBM bytes per cell of each kernel: every
-    per-cell array each kernel must read or write once; stencil-neighbour
-    gathers of U assumed to hit in L2 (only the cell's own U is counted)."""
+    array the kernel must read or write, once; stencil-neighbour gathers of U
+    counted as L2 hits (only the cell's own U is counted). Face points are
+    double4 (32 B), indices int32, labels uint8."""
     Q = NF * NQ
-    central = 32 + 4 * MM + 8 * MM * K + 8 * Q * K + 4 * NF + 1 + 8 + 32 * Q + 32 * K + 1
-    cwenoz = 4 + 32 + 1 + 4 * NF * MD + 16 * NF * MD + 8 * K * K + 32 * K + 8 * Q * K + 4 * NF + 32 * Q
-    muscl = 4 + 32 + 1 + 4 * MM + 16 * MM + 4 * NF + 16 * Q + 8 + 32 * Q
-    flux = 1 + 24 * NF + 1 * NF + (4 + 1) * NF * NQ + 32 * Q + 8 + 32 + 32 * 2 + 32
-    spread = 1 + 1 + 4 * NF + 1
-    return dict(central=central, spread=spread, cwenoz=cwenoz, muscl=muscl, flux=flux)
+    central = (32 + 4 * MM + 8 * MM * K      # U, stencil ids, pinv        (TMA group A)
+               + 8 * Q * K + 8 + 4 * NF + 4 * Q  # phi, threshold, nbrs, slots (TMA group B)
+               + 32 * Q + 32 * K + 1)         # candidate face points, dofs, raw label
+    cwenoz = (32 + 4 * NF * MD + 16 * NF * MD + 8 * K * K + 8 * Q * K + 4 * NF + 32 * K  # U, dir ids/pinv, OI, phi, nbrs, dofs
+              + 4 * Q + 32 * Q + 8)           # slots, face points, chunk entry/label
+    muscl = 32 + 4 * MM + 16 * MM + 16 * Q + 4 * NF + 4 * Q + 32 * Q + 8
+    faces_per_cell = NF / 2.0
+    flux = faces_per_cell * (2 * NQ * 32 + 24 + 2 + 8 + 2 * 32)  # both sides' points, geometry, kind, slots, +-flux
+    gather = 32 * NF + 2 * 32 + 8 + 32 + 8                       # residual slots, RK terms, 1/area, output, h (dt)
+    spread = 1 + 4 * NF + 1 + 1
+    return dict(central=int(central), spread=spread, cwenoz=int(cwenoz), muscl=int(muscl),
+                flux=int(flux + gather))
 
 
 def measured_peak_hbm():

@@ -1,0 +1,118 @@
+"""BASELINE.json configurations at full size on the GPU.
+
+* Config 2 (262,144 cells): against the compiled reference (oracle/_ref) on the
+  same mesh/seed -- one stage (labels identical, residual within 1e-10) and
+  two SSP-RK3 steps (census identical, L1 within 1e-8).
+* Config 3 (8,388,608 cells, p=3): size-independent properties -- discrete
+  conservation on the fully periodic domain, run-to-run bit-determinism, and
+  (at quarter scale) a 4-subdomain decomposition reproducing the single-domain
+  state bit-for-bit.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref as R
+from paper_2510_25906_b200 import _abi as A
+from paper_2510_25906_b200.decompose import Subdomain, partition_rcb
+from paper_2510_25906_b200.mesh import Mesh, Stencils
+from paper_2510_25906_b200.solver import Solver, make_bcs
+from tests.cases import case, scaled_err
+from tests.decomp_driver import local_exchange, run_rk3
+
+pytestmark = pytest.mark.gpu
+
+
+def product_case(name, scale=1):
+    mk, order, ic, prm, opts, bcs = case(name, scale)
+    nq = (order + 2) // 2
+    mesh = Mesh.structured_tri(mk["nx"], mk["ny"], mk["rect"], jitter=mk["jitter"], seed=1, periodic=mk["periodic"],
+                               n_qp=nq)
+    st = Stencils(mesh, order)
+    u0 = mesh.project_initial(ic, prm, seed=1, degree=max(2 * order, 2))
+    return mk, order, ic, prm, opts, bcs, mesh, st, u0
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not shipped")
+def test_config2_full_size_against_reference():
+    mk, order, ic, prm, opts, bcs, mesh, st, u0 = product_case("config2")
+    o = A.options_from_dict(order=order, **opts)
+    rm = R.RefMesh.structured_tri(mk["nx"], mk["ny"], mk["rect"], jitter=mk["jitter"], seed=1, periodic=2, n_qp=2)
+    rs = R.RefSolver(rm, o, make_bcs(bcs))
+    g = Solver(mesh, o, make_bcs(bcs), stencils=st)
+    r_ref = rs.compute_residual(u0, 0.0, 1)
+    r_gpu = g.compute_residual(u0, 0.0)
+    np.testing.assert_array_equal(g.labels(), rs.labels())
+    assert g.nad_ties() == 0
+    assert scaled_err(r_gpu, r_ref) <= 1e-10
+    rs.set_state(u0)
+    g.state = u0
+    _, _, cen_ref = rs.run_steps(2, A.RK3, census=True)
+    _, cen_gpu = g.run_steps(2, A.RK3, census=True)
+    np.testing.assert_array_equal(cen_gpu, cen_ref)
+    ug, ur = g.state, rs.get_state()
+    assert np.sum(np.abs(ug - ur)) / np.sum(np.abs(ur)) <= 1e-8
+
+
+def test_config3_full_size_conservation_and_determinism():
+    mk, order, ic, prm, opts, bcs, mesh, st, u0 = product_case("config3")
+    assert mesh.n_cells == 8_388_608
+    o = A.options_from_dict(order=order, **opts)
+    g = Solver(mesh, o, stencils=st)
+    area = np.ctypeslib.as_array(mesh.view.cell_area, shape=(mesh.n_cells,)).copy()
+    g.state = u0
+    t1, cen = g.run_steps(2, A.RK3, census=True)
+    u1 = g.state
+    # discrete conservation on the periodic domain (telescoping face fluxes)
+    tot0 = (u0 * area[:, None]).sum(0)
+    tot1 = (u1 * area[:, None]).sum(0)
+    scale = np.abs(u0 * area[:, None]).sum(0)
+    assert np.all(np.abs(tot1 - tot0) <= 1e-12 * scale)
+    assert cen.sum(1).tolist() == [mesh.n_cells] * 2
+    # bit-determinism: the same run again
+    g.state = u0
+    t2, cen2 = g.run_steps(2, A.RK3, census=True)
+    assert t2 == t1
+    np.testing.assert_array_equal(cen2, cen)
+    np.testing.assert_array_equal(g.state, u1)
+
+
+def test_config3_quarter_scale_decomposition_bit_exact():
+    mk, order, ic, prm, opts, bcs, mesh, st, u0 = product_case("config3", scale=4)
+    o = A.options_from_dict(order=order, **opts)
+    single = Solver(mesh, o, stencils=st)
+    single.state = u0
+    t_ref = 0.0
+    for _ in range(2):
+        dt = single.max_stable_dt()
+        single.advance(dt, t_ref, A.RK3)
+        t_ref += dt
+    ref = single.state
+    del single
+    n = 4
+    part = partition_rcb(mesh, n)
+    subs = [Subdomain(mesh, st, part, n, r) for r in range(n)]
+
+    class Rank:
+        def __init__(self, sub):
+            self.g = Solver.on_subdomain(sub, o)
+            self.sub = sub
+            self.last_census = np.zeros(4, dtype=np.int64)
+
+        def max_stable_dt(self, u):
+            self.g.state = u
+            return self.g.max_stable_dt()
+
+        def residual(self, u, t, first):
+            return self.g.compute_residual(u, t)
+
+        def record_census(self):
+            self.last_census = np.bincount(self.g.labels()[: self.sub.n_owned], minlength=4)
+
+    ranks = [Rank(s) for s in subs]
+    states = [s.local_state(u0) for s in subs]
+    t, _ = run_rk3(ranks, subs, states, 2, local_exchange, min)
+    assert t == t_ref
+    out = np.zeros_like(u0)
+    for s, u in zip(subs, states):
+        out[s.gid[: s.n_owned]] = u[: s.n_owned]
+    np.testing.assert_array_equal(out, ref)

@@ -36,6 +36,13 @@ enum : int { FL_DOFS = 1, FL_EVAL = 2, FL_NAD = 4, FL_PRECHECK = 8, FL_TAPS = 16
              FL_CENSUS = 64, FL_STEP_LABELS = 128, FL_CHUNKS = 256, FL_DT = 512 };
 
 constexpr int kMaxPatches = 16;
+
+// Programmatic dependent launch: every stage kernel is launched while its
+// predecessor drains (cudaLaunchAttributeProgrammaticStreamSerialization, no
+// explicit trigger, so the predecessor's blocks have all exited when we run).
+// Work on static data may precede pdl_wait(); anything the predecessor wrote
+// (and the error word) is read only after it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 constexpr int kBlock = 128;
 
 struct BcEntry {
@@ -236,6 +243,11 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
   const int g = blockIdx.x * kBlock + threadIdx.x;
   const int v = g & 3;
   const int c0 = g >> 2;
+  pdl_wait();
+  if (g == 0) {  // this stage's class-list counters and tie count (read only by later kernels)
+    for (int i = 0; i < 4; ++i) S.counts[i] = 0;
+    if (flags & FL_NAD) *S.ties = 0;
+  }
   if (*(volatile int*)S.err) return;
   const bool live = c0 < L.n;
   const int c = live ? c0 : L.n - 1;  // dead groups shadow a real cell so the group shuffles stay uniform
@@ -327,6 +339,7 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
   constexpr int Q = NF * NQ;
   const int c = blockIdx.x * kBlock + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  pdl_wait();
   int lab = -1;
   if (c < L.n && !*(volatile int*)S.err) {
     const int r = S.raw[c];
@@ -406,6 +419,7 @@ __global__ void __launch_bounds__(kBlock) k_cwenoz(Layout L, Physics ph, Scratch
   constexpr int CPB = kBlock / 4;  // cells per block iteration
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const bool all = (flags & FL_NAD) == 0;  // forced CWENOZ mode: every cell, no list
+  pdl_wait();
   const int count = all ? L.n : S.counts[0];
   if (*(volatile int*)S.err) return;
   if (!(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
@@ -533,6 +547,7 @@ __global__ void __launch_bounds__(kBlock) k_muscl(Layout L, Physics ph, Scratch 
   constexpr int CPB = kBlock / 4;
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const bool all = (flags & FL_NAD) == 0;  // forced MUSCL mode
+  pdl_wait();
   const int count = all ? L.n : S.counts[1];
   if (*(volatile int*)S.err) return;
   const int v = threadIdx.x & 3;
@@ -605,6 +620,7 @@ template <int NQ, int NF, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_constant(Layout L, Scratch S, const double4* __restrict__ U) {
   constexpr int Q = NF * NQ;
   const int c = blockIdx.x * kBlock + threadIdx.x;
+  pdl_wait();
   if (c >= L.n) return;
   const d4 u0 = ld4(&U[c]);
   const int nf = UNI ? NF : L.nfc[c];
@@ -653,6 +669,7 @@ __device__ __forceinline__ void block_min_into(double x, DtState* ds) {
 // later steps get it from the previous step's final k_gather_rk)
 __global__ void __launch_bounds__(kBlock) k_dt(Layout L, const double4* __restrict__ U, double gamma, DtState* ds,
                                                int* err) {
+  pdl_wait();
   if (*(volatile int*)err) return;  // block-uniform
   const int c = blockIdx.x * kBlock + threadIdx.x;
   double x = 1e300;
@@ -688,9 +705,13 @@ __device__ __forceinline__ void dt_finalize(DtState* ds, int* err) {
   ds->dt = smin(dt, ds->t_end - ds->t);
 }
 
-__global__ void k_dt_collect(DtState* ds) { dt_collect(ds); }
+__global__ void k_dt_collect(DtState* ds) {
+  pdl_wait();
+  dt_collect(ds);
+}
 
 __global__ void k_dt_finalize(DtState* ds, int* err, int collect) {
+  pdl_wait();
   if (*(volatile int*)err) return;
   if (collect) dt_collect(ds);
   dt_finalize(ds, err);
@@ -714,11 +735,12 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
   const int f0 = warp * FPW + fs;
   const bool in = fs < FPW && f0 < L.n_faces;
   const int f = in ? f0 : 0;
-  const int err0 = *(volatile int*)S.err;
   const int kind = in ? L.fkind[f] : 2;
+  const double nx = L.fnx[f], ny = L.fny[f];  // static geometry: fetched while the predecessor drains
+  pdl_wait();
+  const int err0 = *(volatile int*)S.err;
   double t[NV] = {0.0, 0.0, 0.0, 0.0};
   if (kind != 2) {
-    const double nx = L.fnx[f], ny = L.fny[f];
     const d4 UL = ld4(&S.fp[(static_cast<size_t>(f) * NQ + q) * 2 + 0]);
     d4 UR;
     if (kind == 0) {
@@ -775,13 +797,16 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
   const int lane = threadIdx.x & 31;
   const bool live = c0 < L.n_owned;
   const int c = live ? c0 : L.n_owned - 1;
-  const int err0 = *(volatile int*)S.err;
   const double* rsd = reinterpret_cast<const double*>(S.rs);
+  // RK terms were written by earlier stages (complete before our predecessor
+  // started) and 1/area is static: both are fetched while the face kernel drains
   double term[5];
 #pragma unroll
   for (int i = 0; i < 5; ++i)
     term[i] = (i < rk.nterms && rk.term[i]) ? __ldg(reinterpret_cast<const double*>(rk.term[i] + c) + v) : 0.0;
   const double inv_vol = L.inv_vol[c];
+  pdl_wait();
+  const int err0 = *(volatile int*)S.err;
   const int nf = UNI ? NF : L.nfc[c];
   // acc += sgn * face_flux_ in the cell's face order; the signed terms were
   // scattered into this cell's slots by k_face_flux (coalesced reads here)
@@ -838,6 +863,7 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
 __global__ void __launch_bounds__(256) k_halo_pack(const double4* __restrict__ U, const int* __restrict__ idx, int n,
                                                    double4* __restrict__ out) {
   const int i = blockIdx.x * 256 + threadIdx.x;
+  pdl_wait();
   if (i < n) out[i] = U[idx[i]];
 }
 

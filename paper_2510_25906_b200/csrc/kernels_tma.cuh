@@ -63,12 +63,9 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
   const int nchunks = (L.n + 31) >> 5;
   __shared__ int s_err;
   if (tid == 0) {
-    s_err = *(volatile int*)S.err;
     for (int i = 0; i < 2 * NS; ++i) mbar_init(&bar[i], 1);
     mbar_fence_init();
   }
-  __syncthreads();
-  if (s_err) return;  // block-uniform: the loop below has block barriers
   auto issue_a = [&](int chunk, int st) {
     unsigned char* b = smem + st * St::BYTES;
     mbar_arrive_expect_tx(&bar[2 * st], St::A_BYTES);
@@ -84,12 +81,31 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
     bulk_g2s(b + St::PHI + St::THR + St::NBR, L.dest + static_cast<size_t>(chunk) * Q * 32, St::DEST,
              &bar[2 * st + 1]);
   };
+  // the operator data is static: the first chunks' bulk copies are in flight
+  // before the wait for the previous kernel (programmatic dependent launch)
   if (tid == 0)
     for (int p = 0; p < NS; ++p)
       if (static_cast<int>(blockIdx.x + p * gridDim.x) < nchunks) {
         issue_a(blockIdx.x + p * gridDim.x, p);
         issue_b(blockIdx.x + p * gridDim.x, p);
       }
+  pdl_wait();
+  if (tid == 0) {
+    s_err = *(volatile int*)S.err;
+    if (blockIdx.x == 0) {  // this stage's class-list counters and tie count
+      for (int i = 0; i < 4; ++i) S.counts[i] = 0;
+      if (flags & FL_NAD) *S.ties = 0;
+    }
+  }
+  __syncthreads();
+  if (s_err) {  // block-uniform; drain the copies in flight before leaving
+    for (int p = 0; p < NS; ++p)
+      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nchunks) {
+        mbar_wait(&bar[2 * p], 0);
+        mbar_wait(&bar[2 * p + 1], 0);
+      }
+    return;
+  }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool detect = (flags & (FL_NAD | FL_PRECHECK)) != 0;
@@ -242,6 +258,7 @@ __global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, S
   const int slot = tid >> 2;
   const int v = tid & 3;
   __shared__ int s_err, s_nc, s_nm;
+  pdl_wait();
   if (tid == 0) {
     s_err = *(volatile int*)S.err;
     s_nc = S.counts[2];

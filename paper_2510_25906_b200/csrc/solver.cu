@@ -86,6 +86,33 @@ void nccl_unique_id(uint8_t id[128]) {
   std::memcpy(id, &u, 128);
 }
 
+// Stage kernels are launched with programmatic stream serialization (PDL):
+// the next kernel's blocks start while the previous one drains and wait in
+// griddepcontrol.wait before touching its outputs. UCFVB_PDL=0 disables it.
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("UCFVB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // ---- kernel dispatch over (K, NQ, NF) ----------------------------------------
 struct KernelSet {
   void (*central)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
@@ -115,14 +142,15 @@ constexpr uint32_t tma_smem(int stages) { return stages * St::BYTES + 16 * stage
 template <int K, int NQ, int NF, int MM, int NS>
 void central_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                           const double4* U, int f) {
-  k_central_tma<K, NQ, NF, MM, NS><<<g, kBlock, tma_smem<CentralStage<K, NQ, NF, MM>>(NS), st>>>(L, p, S, U, f);
+  launch_k(k_central_tma<K, NQ, NF, MM, NS>, g, dim3(kBlock), tma_smem<CentralStage<K, NQ, NF, MM>>(NS), st, L, p, S,
+           U, f);
 }
 
 template <int K, int NQ, int NF, int MM, int MD, int NS>
 void troubled_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                            const double4* U, int f) {
-  k_troubled_tma<K, NQ, NF, MM, MD, NS><<<g, kBlock, tma_smem<TroubledStage<K, NQ, NF, MM, MD>>(NS), st>>>(L, p, S, U,
-                                                                                                       f);
+  launch_k(k_troubled_tma<K, NQ, NF, MM, MD, NS>, g, dim3(kBlock), tma_smem<TroubledStage<K, NQ, NF, MM, MD>>(NS), st,
+           L, p, S, U, f);
 }
 
 // pick the stage count (1..3), raise the dynamic smem limit, size the persistent grid
@@ -143,22 +171,22 @@ template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
 KernelSet make_set() {
   KernelSet s;
   s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                 int f) { k_central<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+                 int f) { launch_k(k_central<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, p, S, U, f); };
   s.spread = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U, int f, int d) {
-    k_spread<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, S, U, f, d);
+    launch_k(k_spread<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, S, U, f, d);
   };
   s.cwenoz = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-                int f) { k_cwenoz<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+                int f) { launch_k(k_cwenoz<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, p, S, U, f); };
   s.muscl = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
-               int f) { k_muscl<K, NQ, NF, MMT, MDT, UNI><<<g, kBlock, 0, st>>>(L, p, S, U, f); };
+               int f) { launch_k(k_muscl<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, p, S, U, f); };
   s.constant = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U) {
-    k_constant<NQ, NF, UNI><<<g, kBlock, 0, st>>>(L, S, U);
+    launch_k(k_constant<NQ, NF, UNI>, g, kBlock, 0, st, L, S, U);
   };
   s.face_flux = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S) {
-    k_face_flux<NQ><<<g, kBlock, 0, st>>>(L, p, S);
+    launch_k(k_face_flux<NQ>, g, kBlock, 0, st, L, p, S);
   };
   s.gather = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const RkEpilogue& rk, int f, DtState* ds,
-                 double gamma) { k_gather_rk<NF, UNI><<<g, kBlock, 0, st>>>(L, S, rk, f, ds, gamma); };
+                 double gamma) { launch_k(k_gather_rk<NF, UNI>, g, kBlock, 0, st, L, S, rk, f, ds, gamma); };
   s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
   if constexpr (MMT > 0 && UNI) {
     s.central_tma = true;
@@ -278,7 +306,7 @@ struct GpuSolver::Impl {
     int64_t nl = 0;
     for (const DevPeer& p : peers)
       if (p.n_send) {
-        k_halo_pack<<<dim3((p.n_send + 255) / 256), 256, 0, stream>>>(buf, p.send_idx, p.n_send, sendbuf + p.send_off);
+        launch_k(k_halo_pack, dim3((p.n_send + 255) / 256), 256, 0, stream, buf, p.send_idx, p.n_send, sendbuf + p.send_off);
         ++nl;
       }
     NK(nccl().GroupStart());
@@ -294,18 +322,18 @@ struct GpuSolver::Impl {
 
   // min(h/speed) over the owned cells of `src` into ds->dmin_bits
   int64_t launch_dt_reduce(const double4* src) {
-    k_dt<<<dim3((L.n_owned + kBlock - 1) / kBlock), kBlock, 0, stream>>>(L, src, opt.gamma, ds, S.err);
+    launch_k(k_dt, dim3((L.n_owned + kBlock - 1) / kBlock), kBlock, 0, stream, L, src, opt.gamma, ds, S.err);
     return 1;
   }
   // turn the reduced min into this step's dt (on subdomains after a min all-reduce)
   int64_t launch_dt_finalize() {
     if (!comm) {
-      k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err, 1);
+      launch_k(k_dt_finalize, 1, 1, 0, stream, ds, S.err, 1);
       return 1;
     }
-    k_dt_collect<<<1, 1, 0, stream>>>(ds);
+    launch_k(k_dt_collect, 1, 1, 0, stream, ds);
     NK(nccl().AllReduce(&ds->dmin, &ds->dmin, 1, ncclDouble, ncclMin, comm, stream));
-    k_dt_finalize<<<1, 1, 0, stream>>>(ds, S.err, 0);
+    launch_k(k_dt_finalize, 1, 1, 0, stream, ds, S.err, 0);
     return 2;
   }
 
@@ -334,8 +362,6 @@ struct GpuSolver::Impl {
     record(0);
     if (mode == UCFVB_HYBRID) {
       const bool detect = first || opt.detect_every_stage;
-      CK(cudaMemsetAsync(S.counts, 0, 4 * sizeof(int), stream));
-      if (detect) CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream));
       ks.central(grid_central(), stream, L, ph, S, U, FL_EVAL | FL_DOFS | (detect ? FL_NAD : FL_PRECHECK));
       record(1);
       if (ks.troubled && !per_cell_lists) {

@@ -221,6 +221,42 @@ int32_t ucfvb_compute_residual(ucfvb_solver* h, const double* u, double t, doubl
 int32_t ucfvb_run_steps(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end,
                         double* t_out, int64_t* census_out);
 
+/* ucfvb_run_steps plus each step's dt (run.cpp:99-112 CensusRow::dt): dt_out
+ * (nullable) receives [n_steps] doubles; step k's end time is t0 + dt_0 + ...
+ * + dt_k summed in step order, exactly as run_simulation's `t += dt`. */
+int32_t ucfvb_run_steps_log(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end,
+                            double* t_out, int64_t* census_out, double* dt_out);
+
+/* run_simulation's loop with its own termination (run.cpp:96-132): steps
+ * `dt = min(max_stable_dt, t_end - t); advance` while t < t_end - 1e-14 t_end,
+ * at most max_steps, device-resident (batches of graph launches, the loop
+ * condition is evaluated on the device). n_steps_out receives the steps taken;
+ * census_out [max_steps][4] / dt_out [max_steps] (nullable) their rows. */
+int32_t ucfvb_run_until(ucfvb_solver* h, int32_t max_steps, int32_t rk, double t0, double t_end, double* t_out,
+                        int32_t* n_steps_out, int64_t* census_out, double* dt_out);
+
+/* CensusRow / TimingRow (run.hpp:15-25) */
+typedef struct ucfvb_census_row {
+  int32_t step;
+  double t, dt;
+  int64_t counts[4]; /* Linear, CWENOZ, MUSCL, FirstOrder */
+} ucfvb_census_row;
+typedef struct ucfvb_timing_row {
+  int32_t step;
+  double wall;
+  double reconstruct, detect, weights, flux; /* per-step PhaseTimes deltas, seconds */
+} ucfvb_timing_row;
+
+/* Run outputs, byte-identical to the reference writers (every double "%.17g"):
+ * write_field_snapshot (run.cpp:160-190; legacy-VTK ASCII with density,
+ * pressure, velocity and the scheme label; state [n_cells][4], labels from
+ * ucfvb_get_step_labels), write_census_csv (run.cpp:192-202),
+ * write_timing_csv (run.cpp:204-213). Host-only: no device needed. */
+int32_t ucfvb_write_field_snapshot(const ucfvb_mesh_view* mesh, const double* state, const uint8_t* labels,
+                                   double gamma, const char* path);
+int32_t ucfvb_write_census_csv(const ucfvb_census_row* rows, int32_t n_rows, int64_t n_cells, const char* path);
+int32_t ucfvb_write_timing_csv(const ucfvb_timing_row* rows, int32_t n_rows, const char* path);
+
 /* Solver::step_labels (solver.hpp:66) and the current-stage labels */
 int32_t ucfvb_get_step_labels(ucfvb_solver* h, uint8_t* labels);
 int32_t ucfvb_get_labels(ucfvb_solver* h, uint8_t* labels);

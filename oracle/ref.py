@@ -55,6 +55,11 @@ def lib():
             "ref_advance": (C.c_int, [H, C.c_double, C.c_double, C.c_int]),
             "ref_run_steps": (C.c_int, [H, C.c_int, C.c_int, C.c_double, C.c_double, dp,
                                         C.POINTER(C.c_int64), dp]),
+            "ref_run_steps_log": (C.c_int, [H, C.c_int, C.c_int, C.c_double, C.c_double, dp,
+                                            C.POINTER(C.c_int64), dp]),
+            "ref_write_field_snapshot": (C.c_int, [H, dp, C.POINTER(C.c_uint8), C.c_double, C.c_char_p]),
+            "ref_write_census_csv": (C.c_int, [C.POINTER(A.CensusRow), C.c_int, C.c_int, C.c_char_p]),
+            "ref_write_timing_csv": (C.c_int, [C.POINTER(A.TimingRow), C.c_int, C.c_char_p]),
             "ref_get_labels": (C.c_int, [H, C.POINTER(C.c_uint8), C.c_int]),
             "ref_get_face_values": (C.c_int, [H, dp, dp]),
             "ref_get_dofs": (C.c_int, [H, dp]),
@@ -197,6 +202,24 @@ class RefSolver:
                                 C.byref(w)))
         return t.value, w.value, (cen if census else None)
 
+    def run_log(self, n_steps, rk=A.RK3, t0=0.0, t_end=float("inf")):
+        """(t, census[n,4], dt[n]) of n reference steps."""
+        t = C.c_double()
+        cen = np.zeros((n_steps, 4), dtype=np.int64)
+        dts = np.zeros(n_steps)
+        _ck(lib().ref_run_steps_log(self.h, n_steps, rk, t0, t_end, C.byref(t),
+                                    cen.ctypes.data_as(C.POINTER(C.c_int64)), dts.ctypes.data_as(C.POINTER(C.c_double))))
+        return t.value, cen, dts
+
+    def run_until(self, t_end, rk=A.RK3, t0=0.0):
+        """run_simulation's loop (run.cpp:96): step while t < t_end - 1e-14 t_end."""
+        t, cens, dts = t0, [], []
+        while t < t_end - 1e-14 * t_end:
+            t, c, d = self.run_log(1, rk, t, t_end)
+            cens.append(c[0])
+            dts.append(d[0])
+        return t, np.array(cens, dtype=np.int64).reshape(-1, 4), np.array(dts)
+
     def labels(self, step=False):
         out = np.zeros(self.n_cells, dtype=np.uint8)
         _ck(lib().ref_get_labels(self.h, out.ctypes.data_as(C.POINTER(C.c_uint8)), 1 if step else 0))
@@ -227,3 +250,27 @@ class RefSolver:
         if getattr(self, "h", None) and _lib is not None:
             _lib.ref_solver_free(self.h)
             self.h = None
+
+
+def write_field_snapshot(mesh: "RefMesh", state, labels, gamma, path):
+    u = np.ascontiguousarray(state, dtype=np.float64)
+    lab = np.ascontiguousarray(labels, dtype=np.uint8)
+    _ck(lib().ref_write_field_snapshot(mesh.h, u.ctypes.data_as(C.POINTER(C.c_double)),
+                                       lab.ctypes.data_as(C.POINTER(C.c_uint8)), gamma, str(path).encode()))
+
+
+def write_census_csv(rows, n_cells, path):
+    arr = (A.CensusRow * max(1, len(rows)))()
+    for i, (step, t, dt, counts) in enumerate(rows):
+        arr[i].step, arr[i].t, arr[i].dt = step, t, dt
+        for k in range(4):
+            arr[i].counts[k] = int(counts[k])
+    _ck(lib().ref_write_census_csv(arr, len(rows), n_cells, str(path).encode()))
+
+
+def write_timing_csv(rows, path):
+    arr = (A.TimingRow * max(1, len(rows)))()
+    for i, r in enumerate(rows):
+        arr[i].step = r[0]
+        arr[i].wall, arr[i].reconstruct, arr[i].detect, arr[i].weights, arr[i].flux = r[1:6]
+    _ck(lib().ref_write_timing_csv(arr, len(rows), str(path).encode()))

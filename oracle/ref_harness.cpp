@@ -37,6 +37,7 @@
 #include "ucfv/cases.hpp"
 #include "ucfv/mesh.hpp"
 #include "ucfv/quadrature.hpp"
+#include "ucfv/run.hpp"
 #include "ucfv/stencil.hpp"
 
 #include "ucfvb.h"
@@ -551,6 +552,84 @@ int ref_run_steps(void* s, int n_steps, int rk, double t0, double t_end, double*
     if (wall_s)
       *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - w0).count();
     if (t_out) *t_out = t;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// run_steps with each step's dt (run.cpp:99-112)
+int ref_run_steps_log(void* s, int n_steps, int rk, double t0, double t_end, double* t_out, int64_t* census,
+                      double* dts) {
+  try {
+    auto* h = static_cast<SolverHolder*>(s);
+    double t = t0;
+    for (int k = 0; k < n_steps; ++k) {
+      const double dt = std::min(h->solver->max_stable_dt(), t_end - t);
+      if (rk == UCFVB_RK54)
+        h->solver->advance(dt, t);
+      else
+        rk3_step(*h, dt, t);
+      t += dt;
+      if (dts) dts[k] = dt;
+      if (census) {
+        int64_t* row = census + 4 * k;
+        row[0] = row[1] = row[2] = row[3] = 0;
+        for (Scheme sc : h->solver->step_labels()) ++row[static_cast<int>(sc)];
+      }
+    }
+    if (t_out) *t_out = t;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+// the reference's own output writers (run.cpp:160-213)
+int ref_write_field_snapshot(void* m, const double* state, const uint8_t* labels, double gamma, const char* path) {
+  try {
+    const Mesh& mesh = (*static_cast<std::shared_ptr<MeshHolder>*>(m))->mesh;
+    StateField u(mesh.n_cells());
+    std::vector<Scheme> lab(mesh.n_cells());
+    for (int c = 0; c < mesh.n_cells(); ++c) {
+      for (int v = 0; v < 4; ++v) u[c][v] = state[4 * c + v];
+      lab[c] = static_cast<Scheme>(labels[c]);
+    }
+    write_field_snapshot(mesh, u, lab, gamma, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_write_census_csv(const ucfvb_census_row* rows, int n_rows, int n_cells, const char* path) {
+  try {
+    std::vector<CensusRow> r(n_rows);
+    for (int i = 0; i < n_rows; ++i) {
+      r[i].step = rows[i].step;
+      r[i].t = rows[i].t;
+      r[i].dt = rows[i].dt;
+      for (int k = 0; k < 4; ++k) r[i].counts[k] = rows[i].counts[k];
+    }
+    write_census_csv(r, n_cells, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
+int ref_write_timing_csv(const ucfvb_timing_row* rows, int n_rows, const char* path) {
+  try {
+    std::vector<TimingRow> r(n_rows);
+    for (int i = 0; i < n_rows; ++i) {
+      r[i].step = rows[i].step;
+      r[i].wall = rows[i].wall;
+      r[i].phases.reconstruct = rows[i].reconstruct;
+      r[i].phases.detect = rows[i].detect;
+      r[i].phases.weights = rows[i].weights;
+      r[i].phases.flux = rows[i].flux;
+    }
+    write_timing_csv(r, path);
     return 0;
   } catch (const std::exception& e) {
     return fail(e);

@@ -100,6 +100,17 @@ class MeshView(C.Structure):
     ]
 
 
+class CensusRow(C.Structure):
+    """ucfvb_census_row = CensusRow (run.hpp:15-19)."""
+    _fields_ = [("step", C.c_int32), ("t", C.c_double), ("dt", C.c_double), ("counts", C.c_int64 * 4)]
+
+
+class TimingRow(C.Structure):
+    """ucfvb_timing_row = TimingRow (run.hpp:21-25), per-step phase deltas in seconds."""
+    _fields_ = [("step", C.c_int32), ("wall", C.c_double), ("reconstruct", C.c_double), ("detect", C.c_double),
+                ("weights", C.c_double), ("flux", C.c_double)]
+
+
 class StencilView(C.Structure):
     _fields_ = [
         ("order", C.c_int32), ("K", C.c_int32), ("n_qp", C.c_int32), ("si_exponent", C.c_int32),
@@ -303,6 +314,13 @@ def _declare(lib):
         "ucfvb_advance": (C.c_int32, [H, C.c_double, C.c_double, C.c_int32]),
         "ucfvb_compute_residual": (C.c_int32, [H, c_dp, C.c_double, c_dp]),
         "ucfvb_run_steps": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i64p]),
+        "ucfvb_run_steps_log": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i64p,
+                                            c_dp]),
+        "ucfvb_run_until": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i32p, c_i64p,
+                                        c_dp]),
+        "ucfvb_write_field_snapshot": (C.c_int32, [P(MeshView), c_dp, P(C.c_uint8), C.c_double, C.c_char_p]),
+        "ucfvb_write_census_csv": (C.c_int32, [P(CensusRow), C.c_int32, C.c_int64, C.c_char_p]),
+        "ucfvb_write_timing_csv": (C.c_int32, [P(TimingRow), C.c_int32, C.c_char_p]),
         "ucfvb_get_step_labels": (C.c_int32, [H, P(C.c_uint8)]),
         "ucfvb_get_labels": (C.c_int32, [H, P(C.c_uint8)]),
         "ucfvb_get_census": (C.c_int32, [H, c_i64p]),
@@ -342,7 +360,8 @@ ABI_SYMBOLS = [
     "ucfvb_mesh_free", "ucfvb_build_stencils", "ucfvb_stencils_get_view", "ucfvb_stencils_free",
     "ucfvb_project_initial", "ucfvb_create", "ucfvb_destroy", "ucfvb_set_state",
     "ucfvb_get_state", "ucfvb_max_stable_dt", "ucfvb_advance", "ucfvb_compute_residual",
-    "ucfvb_run_steps", "ucfvb_get_step_labels", "ucfvb_get_labels", "ucfvb_get_census",
+    "ucfvb_run_steps", "ucfvb_run_steps_log", "ucfvb_run_until", "ucfvb_write_field_snapshot", "ucfvb_write_census_csv",
+    "ucfvb_write_timing_csv", "ucfvb_get_step_labels", "ucfvb_get_labels", "ucfvb_get_census",
     "ucfvb_get_nad_ties", "ucfvb_get_face_values", "ucfvb_get_dofs", "ucfvb_set_phase_timing",
     "ucfvb_get_phase_times", "ucfvb_n_cells", "ucfvb_n_faces", "ucfvb_n_qp",
     "ucfvb_state_device_ptr", "ucfvb_stream", "ucfvb_launch_count",

@@ -21,6 +21,10 @@ struct ucfvb_solver {
 
 namespace ucfvb {
 void nccl_unique_id(uint8_t id[128]);
+void write_field_snapshot(const ucfvb_mesh_view& m, const double* state, const uint8_t* labels, double gamma,
+                          const char* path);
+void write_census_csv(const ucfvb_census_row* rows, int n_rows, int64_t n_cells, const char* path);
+void write_timing_csv(const ucfvb_timing_row* rows, int n_rows, const char* path);
 }
 
 namespace {
@@ -156,6 +160,35 @@ int32_t ucfvb_run_steps(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0,
     const double t = h->s->run_steps(n_steps, rk, t0, t_end, census_out);
     if (t_out) *t_out = t;
   });
+}
+int32_t ucfvb_run_steps_log(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end, double* t_out,
+                            int64_t* census_out, double* dt_out) {
+  return guard(h, [&] {
+    const double t = h->s->run_steps(n_steps, rk, t0, t_end, census_out, dt_out);
+    if (t_out) *t_out = t;
+  });
+}
+int32_t ucfvb_run_until(ucfvb_solver* h, int32_t max_steps, int32_t rk, double t0, double t_end, double* t_out,
+                        int32_t* n_steps_out, int64_t* census_out, double* dt_out) {
+  return guard(h, [&] {
+    int n = 0;
+    const double t = h->s->run_until(max_steps, rk, t0, t_end, census_out, dt_out, &n);
+    if (t_out) *t_out = t;
+    if (n_steps_out) *n_steps_out = n;
+  });
+}
+int32_t ucfvb_write_field_snapshot(const ucfvb_mesh_view* mesh, const double* state, const uint8_t* labels,
+                                   double gamma, const char* path) {
+  return guard(nullptr, [&] {
+    if (!mesh) throw ucfvb::ApiError(UCFVB_INVALID, "write_field_snapshot: null mesh");
+    ucfvb::write_field_snapshot(*mesh, state, labels, gamma, path);
+  });
+}
+int32_t ucfvb_write_census_csv(const ucfvb_census_row* rows, int32_t n_rows, int64_t n_cells, const char* path) {
+  return guard(nullptr, [&] { ucfvb::write_census_csv(rows, n_rows, n_cells, path); });
+}
+int32_t ucfvb_write_timing_csv(const ucfvb_timing_row* rows, int32_t n_rows, const char* path) {
+  return guard(nullptr, [&] { ucfvb::write_timing_csv(rows, n_rows, path); });
 }
 int32_t ucfvb_get_step_labels(ucfvb_solver* h, uint8_t* labels) {
   return guard(h, [&] { h->s->get_labels(labels, true); });

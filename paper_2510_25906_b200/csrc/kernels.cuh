@@ -640,7 +640,13 @@ struct DtState {
   double t_end;
   double cfl;
   double dmin;  // collected min(h/speed) (all-reduced across ranks before k_dt_finalize)
+  double* dt_log;  // nullable [steps]: each step's dt (run.cpp:111 CensusRow::dt)
+  int until;       // 1: stop at run_simulation's loop condition t < t_end - 1e-14 t_end (run.cpp:96)
 };
+
+// err[0] bit set when an `until` run reached t_end: every later kernel of the
+// batch exits early (like after an error); the host does not report it
+constexpr int kErrDone = 8;
 
 // max_stable_dt's per-cell term (solver.cpp:103-111): h_c / (|u| + |v| + a)
 __device__ __forceinline__ bool dt_term(const double* s, double gamma, double h, double& x) {
@@ -694,6 +700,15 @@ __device__ __forceinline__ void dt_collect(DtState* ds) {
 // step touches the state) or advance t by the previous dt and set this step's
 // dt = min(cfl * dmin, t_end - t) (run.cpp:97-132, solver.cpp:110)
 __device__ __forceinline__ void dt_finalize(DtState* ds, int* err) {
+  if (ds->until) {
+    const double t = ds->t + ds->dt;
+    if (!(t < ds->t_end - 1e-14 * ds->t_end)) {  // the loop ends before max_stable_dt is taken
+      ds->t = t;
+      ds->dt = 0.0;
+      atomicOr(&err[0], kErrDone);
+      return;
+    }
+  }
   if (ds->dt_bad) {
     atomicOr(&err[0], 2);
     atomicMin(&err[3], ds->step + 1);
@@ -703,6 +718,7 @@ __device__ __forceinline__ void dt_finalize(DtState* ds, int* err) {
   ds->step += 1;
   const double dt = ds->cfl * ds->dmin;
   ds->dt = smin(dt, ds->t_end - ds->t);
+  if (ds->dt_log) ds->dt_log[ds->step] = ds->dt;
 }
 
 __global__ void k_dt_collect(DtState* ds) {

@@ -238,6 +238,15 @@ struct TroubledStage {
   static constexpr uint32_t M_NBR = round16(NF * 32 * 4);
   static constexpr uint32_t M_BYTES = M_IDX + M_PLIN + M_PHI + M_NBR;
   static constexpr uint32_t BYTES = C_BYTES > M_BYTES ? C_BYTES : M_BYTES;
+  // split-phase groups (k_troubled_split): A = what the directional / linear
+  // solves read, B = what the blend, evaluation and fallback read
+  static constexpr uint32_t CA = C_DIDX + C_PDIR + C_DOFS;
+  static constexpr uint32_t CB = C_OI + C_PHI + C_NBR;
+  static constexpr uint32_t MA = M_IDX + M_PLIN;
+  static constexpr uint32_t MB = M_PHI + M_NBR;
+  static constexpr uint32_t A_BYTES = CA > MA ? CA : MA;
+  static constexpr uint32_t B_BYTES = CB > MB ? CB : MB;
+  static constexpr uint32_t SPLIT_BYTES = A_BYTES + B_BYTES;
 };
 
 // k_troubled_tma: the CWENOZ and MUSCL reconstructions of one stage in one
@@ -478,6 +487,266 @@ __global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, S
       }
     }
     __syncthreads();  // stage `st` fully consumed before it is refilled
+  }
+}
+
+// k_troubled_split: k_troubled_tma with split-phase refill (one stage, two
+// mbarriers). Group A of the next work item is requested as soon as the
+// directional (CWENOZ) or linear (MUSCL) solves of the current item have read
+// it, so its copy overlaps the blend / limiter / evaluation / fallback; group
+// B is requested once the evaluation and the fallback bounds are done.
+// Arithmetic is identical to k_troubled_tma.
+template <int K, int NQ, int NF, int MM, int MD>
+__global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph, Scratch S,
+                                                           const double4* __restrict__ U, int flags) {
+  using St = TroubledStage<K, NQ, NF, MM, MD>;
+  constexpr int Q = St::Q;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + St::SPLIT_BYTES);  // [0] group A, [1] group B
+  unsigned char* const ga = smem;
+  unsigned char* const gb = smem + St::A_BYTES;
+  const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
+  const int tid = threadIdx.x;
+  const int slot = tid >> 2;
+  const int v = tid & 3;
+  __shared__ int s_err, s_nc, s_nm;
+  pdl_wait();
+  if (tid == 0) {
+    s_err = *(volatile int*)S.err;
+    s_nc = S.counts[2];
+    s_nm = S.counts[3];
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (s_err) return;
+  const int nc = s_nc, nitems = s_nc + s_nm;
+  if (nc > 0 && !(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
+    if (blockIdx.x == 0 && tid == 0) atomicOr(&S.err[0], 4);
+    return;
+  }
+  auto item_chunk = [&](int i) { return i < nc ? S.chunks_c[i] : S.chunks_m[i - nc]; };
+  auto issue_a = [&](int i) {
+    const size_t ch = static_cast<size_t>(item_chunk(i).x);
+    unsigned char* p = ga;
+    if (i < nc) {
+      mbar_arrive_expect_tx(&bar[0], St::CA);
+      bulk_g2s(p, L.dir_idx + ch * NF * MD * 32, St::C_DIDX, &bar[0]);
+      p += St::C_DIDX;
+      bulk_g2s(p, L.pinv_dir + ch * NF * MD * 2 * 32, St::C_PDIR, &bar[0]);
+      p += St::C_PDIR;
+      bulk_g2s(p, S.dofs + ch * K * 32, St::C_DOFS, &bar[0]);
+    } else {
+      mbar_arrive_expect_tx(&bar[0], St::MA);
+      bulk_g2s(p, L.st_idx + ch * MM * 32, St::M_IDX, &bar[0]);
+      p += St::M_IDX;
+      bulk_g2s(p, L.pinv_lin + ch * MM * 2 * 32, St::M_PLIN, &bar[0]);
+    }
+  };
+  auto issue_b = [&](int i) {
+    const size_t ch = static_cast<size_t>(item_chunk(i).x);
+    unsigned char* p = gb;
+    if (i < nc) {
+      mbar_arrive_expect_tx(&bar[1], St::CB);
+      bulk_g2s(p, L.oi + ch * K * K * 32, St::C_OI, &bar[1]);
+      p += St::C_OI;
+      bulk_g2s(p, L.phi + ch * Q * K * 32, St::C_PHI, &bar[1]);
+      p += St::C_PHI;
+      bulk_g2s(p, L.nbr + ch * NF * 32, St::C_NBR, &bar[1]);
+    } else {
+      mbar_arrive_expect_tx(&bar[1], St::MB);
+      bulk_g2s(p, L.phi01 + ch * Q * 2 * 32, St::M_PHI, &bar[1]);
+      p += St::M_PHI;
+      bulk_g2s(p, L.nbr + ch * NF * 32, St::M_NBR, &bar[1]);
+    }
+  };
+  if (tid == 0 && static_cast<int>(blockIdx.x) < nitems) {
+    issue_a(blockIdx.x);
+    issue_b(blockIdx.x);
+  }
+  double* dofs = reinterpret_cast<double*>(S.dofs);
+  double* fv = reinterpret_cast<double*>(S.fp);
+  const bool venkat = ph.limiter == 1;
+  int it = 0;
+  for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
+    const uint32_t par = it & 1;
+    const int next = i + gridDim.x;
+    const int2 e = item_chunk(i);
+    const bool mine = (static_cast<unsigned>(e.y) >> slot) & 1u;
+    const int c = e.x * 32 + slot;  // chunks are full-size in the padded layout; cells past n are never in a mask
+    const int cc = c < L.n ? c : L.n - 1;
+    const double u0 = __ldg(Ud + 4 * static_cast<size_t>(cc) + v);
+    double vals[Q];
+    double lo = u0, hi = u0;
+    double kd[K];  // dofs to keep for the tap
+    mbar_wait(&bar[0], par);
+    if (i < nc) {
+      // ---- CWENOZ (solver.cpp:167-188, reconstruct.cpp:43-150)
+      const int* sdi = reinterpret_cast<const int*>(ga);
+      const double* spd = reinterpret_cast<const double*>(ga + St::C_DIDX);
+      const double* sdo = reinterpret_cast<const double*>(ga + St::C_DIDX + St::C_PDIR);
+      double um[NF][MD];
+#pragma unroll
+      for (int s = 0; s < NF; ++s)
+#pragma unroll
+        for (int m = 0; m < MD; ++m) um[s][m] = __ldg(Ud + 4 * static_cast<size_t>(sdi[(s * MD + m) * 32 + slot]) + v);
+      double dir[NF][2];
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        dir[s][0] = 0.0;
+        dir[s][1] = 0.0;
+#pragma unroll
+        for (int m = 0; m < MD; ++m) {
+          const double d = um[s][m] - u0;
+          dir[s][0] += spd[((s * MD + m) * 2 + 0) * 32 + slot] * d;
+          dir[s][1] += spd[((s * MD + m) * 2 + 1) * 32 + slot] * d;
+        }
+      }
+      double p1[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) p1[k] = sdo[(k * 32 + slot) * 4 + v];
+      __syncthreads();  // group A consumed: request the next item's
+      if (tid == 0 && next < nitems) {
+        fence_proxy_async_smem();
+        issue_a(next);
+      }
+      constexpr int st1 = NF + 1;
+      const double lam0 = 1.0 - 1.0 / ph.lambda1p;
+      const double lams = (1.0 - lam0) / (st1 - 1);
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        p1[0] -= lams * dir[s][0];
+        p1[1] -= lams * dir[s][1];
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) p1[k] /= lam0;
+      mbar_wait(&bar[1], par);
+      const double* soi = reinterpret_cast<const double*>(gb);
+      const double* sph = reinterpret_cast<const double*>(gb + St::C_OI);
+      const int* snb = reinterpret_cast<const int*>(gb + St::C_OI + St::C_PHI);
+      double si0 = 0.0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < K; ++q) t += soi[(k * K + q) * 32 + slot] * p1[q];
+        si0 += p1[k] * t;
+      }
+      const double o00 = soi[slot], o01 = soi[32 + slot], o10 = soi[K * 32 + slot], o11 = soi[(K + 1) * 32 + slot];
+      double sis[NF];
+      double tau = 0.0;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        const double a0 = dir[s][0], a1 = dir[s][1];
+        sis[s] = o00 * a0 * a0 + (o01 + o10) * a0 * a1 + o11 * a1 * a1;
+        tau += fabs(sis[s] - si0);
+      }
+      tau /= (st1 - 1);
+      tau = tau_pow(tau, ph.weno_b);
+      double om0 = lam0 * (1.0 + tau / (ph.weno_eps + si0));
+      double oms[NF];
+      double wsum = om0;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        oms[s] = lams * (1.0 + tau / (ph.weno_eps + sis[s]));
+        wsum += oms[s];
+      }
+      om0 /= wsum;
+#pragma unroll
+      for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
+#pragma unroll
+      for (int s = 0; s < NF; ++s) {
+        const double w = oms[s] / wsum;
+        p1[0] += w * dir[s][0];
+        p1[1] += w * dir[s][1];
+      }
+#pragma unroll
+      for (int lq = 0; lq < Q; ++lq) {
+        vals[lq] = u0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) vals[lq] += p1[k] * sph[(lq * K + k) * 32 + slot];
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) kd[k] = p1[k];
+      if (flags & FL_FALLBACK) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const int nb = snb[j * 32 + slot];
+          if (nb >= 0) {
+            const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
+            lo = smin(lo, x);
+            hi = smax(hi, x);
+          }
+        }
+      }
+    } else {
+      // ---- MUSCL (solver.cpp:189-221, reconstruct.cpp:30-86)
+      const int* sid = reinterpret_cast<const int*>(ga);
+      const double* spl = reinterpret_cast<const double*>(ga + St::M_IDX);
+      double um[MM];
+#pragma unroll
+      for (int m = 0; m < MM; ++m) um[m] = __ldg(Ud + 4 * static_cast<size_t>(sid[m * 32 + slot]) + v);
+      double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+      for (int m = 0; m < MM; ++m) {
+        const double d = um[m] - u0;
+        l0 += spl[(m * 2 + 0) * 32 + slot] * d;
+        l1 += spl[(m * 2 + 1) * 32 + slot] * d;
+      }
+      __syncthreads();  // group A consumed: request the next item's
+      if (tid == 0 && next < nitems) {
+        fence_proxy_async_smem();
+        issue_a(next);
+      }
+      mbar_wait(&bar[1], par);
+      const double* sp01 = reinterpret_cast<const double*>(gb);
+      const int* snb = reinterpret_cast<const int*>(gb + St::M_PHI);
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const int nb = snb[j * 32 + slot];
+        if (nb >= 0) {
+          const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
+          lo = smin(lo, x);
+          hi = smax(hi, x);
+        }
+      }
+      double theta = 1.0;
+      const double eps2 = venkat ? L.eps2[cc] : 0.0;
+#pragma unroll
+      for (int lq = 0; lq < Q; ++lq) {
+        const double p0 = sp01[(lq * 2 + 0) * 32 + slot], pq1 = sp01[(lq * 2 + 1) * 32 + slot];
+        const double qv = u0 + l0 * p0 + l1 * pq1;
+        theta = venkat ? venkat_update(theta, u0, lo, hi, qv, eps2) : bj_update(theta, u0, lo, hi, qv);
+      }
+      if (!venkat) theta = smax(theta, 0.0);
+      const double d0 = theta * l0, d1 = theta * l1;
+#pragma unroll
+      for (int lq = 0; lq < Q; ++lq) {
+        double o = u0;
+        o += d0 * sp01[(lq * 2 + 0) * 32 + slot];
+        o += d1 * sp01[(lq * 2 + 1) * 32 + slot];
+        vals[lq] = o;  // dofs k >= 2 are zero: adding 0*phi leaves o unchanged
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) kd[k] = k == 0 ? d0 : (k == 1 ? d1 : 0.0);
+    }
+    __syncthreads();  // group B consumed: request the next item's
+    if (tid == 0 && next < nitems) {
+      fence_proxy_async_smem();
+      issue_b(next);
+    }
+    bool demote = false;
+    if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);
+    if (mine) {
+#pragma unroll
+      for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
+      if (demote && v == 0) S.labels[c] = 3;
+      if (flags & FL_TAPS) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = demote ? 0.0 : kd[k];
+      }
+    }
   }
 }
 

@@ -153,6 +153,13 @@ void troubled_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physi
            L, p, S, U, f);
 }
 
+template <int K, int NQ, int NF, int MM, int MD>
+void troubled_split_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
+                             const double4* U, int f) {
+  launch_k(k_troubled_split<K, NQ, NF, MM, MD>, g, dim3(kBlock),
+           TroubledStage<K, NQ, NF, MM, MD>::SPLIT_BYTES + 16, st, L, p, S, U, f);
+}
+
 // pick the stage count (1..3), raise the dynamic smem limit, size the persistent grid
 template <typename St, typename Kfn>
 void tma_setup(int n_sm, int stages, int* grid, StageLaunch* launch, StageLaunch l1, StageLaunch l2, StageLaunch l3,
@@ -201,6 +208,16 @@ KernelSet make_set() {
     s.troubled_setup = [](int n_sm, int stages, int* grid, void (**launch)(dim3, cudaStream_t, const Layout&,
                                                                            const Physics&, const Scratch&,
                                                                            const double4*, int)) {
+      if (stages == 0) {  // split-phase single stage
+        using St = TroubledStage<K, NQ, NF, MMT, MDT>;
+        auto k = k_troubled_split<K, NQ, NF, MMT, MDT>;
+        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, St::SPLIT_BYTES + 16));
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, St::SPLIT_BYTES + 16));
+        *grid = std::max(1, per_sm) * n_sm;
+        *launch = troubled_split_launcher<K, NQ, NF, MMT, MDT>;
+        return;
+      }
       tma_setup<TroubledStage<K, NQ, NF, MMT, MDT>>(
           n_sm, stages, grid, launch, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 1>,
           troubled_tma_launcher<K, NQ, NF, MMT, MDT, 2>, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 3>,
@@ -275,6 +292,8 @@ struct GpuSolver::Impl {
   DtState* ds = nullptr;
   unsigned long long* census_dev = nullptr;
   size_t census_cap = 0;
+  double* dtlog_dev = nullptr;
+  size_t dtlog_cap = 0;
   int* step_zero = nullptr;  // device int 0 (census row for advance())
   bool stage_is_first = true;
   bool timing = false;
@@ -625,7 +644,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
     const char* e1 = std::getenv("UCFVB_TMA_STAGES_CENTRAL");
     const char* e2 = std::getenv("UCFVB_TMA_STAGES_TROUBLED");
     I.ks.central_tma_setup(I.n_sm, e1 ? std::atoi(e1) : 1, &I.ks.central_tma_grid, &I.ks.central);
-    I.ks.troubled_setup(I.n_sm, e2 ? std::atoi(e2) : 1, &I.ks.troubled_grid, &I.ks.troubled);
+    I.ks.troubled_setup(I.n_sm, e2 ? std::atoi(e2) : 0, &I.ks.troubled_grid, &I.ks.troubled);
   }
   auto& own = I.owned;
   Layout& L = I.L;
@@ -756,6 +775,7 @@ GpuSolver::~GpuSolver() {
   if (I.comm) nccl().CommDestroy(I.comm);
   for (void* p : I.owned) cudaFree(p);
   if (I.census_dev) cudaFree(I.census_dev);
+  if (I.dtlog_dev) cudaFree(I.dtlog_dev);
   for (auto& e : I.ev)
     if (e) cudaEventDestroy(e);
   if (I.stream) cudaStreamDestroy(I.stream);
@@ -842,9 +862,24 @@ void GpuSolver::compute_residual(const double* u, double t, double* out) {
   CK(cudaStreamSynchronize(I.stream));
 }
 
-double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census_out) {
+double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census_out, double* dt_out) {
+  int done = 0;
+  return run_impl(n_steps, rk, t0, t_end, false, census_out, dt_out, &done);
+}
+
+double GpuSolver::run_until(int max_steps, int rk, double t0, double t_end, int64_t* census_out, double* dt_out,
+                            int* n_done) {
+  return run_impl(max_steps, rk, t0, t_end, true, census_out, dt_out, n_done);
+}
+
+// run_simulation's stepping loop (run.cpp:96-132) on the device. Fixed count:
+// n_steps steps. `until`: steps while t < t_end - 1e-14 t_end, at most
+// n_steps; launched in batches, the device raises kErrDone at the loop end.
+double GpuSolver::run_impl(int n_steps, int rk, double t0, double t_end, bool until, int64_t* census_out,
+                           double* dt_out, int* n_done) {
   Impl& I = *p_;
   if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "run_steps: unknown integrator");
+  *n_done = 0;
   if (n_steps <= 0) return t0;
   const bool census = census_out != nullptr;
   if (census && I.census_cap < static_cast<size_t>(n_steps)) {
@@ -853,6 +888,11 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
     I.census_cap = n_steps;
   }
   if (census) CK(cudaMemsetAsync(I.census_dev, 0, sizeof(unsigned long long) * 4 * n_steps, I.stream));
+  if (dt_out && I.dtlog_cap < static_cast<size_t>(n_steps)) {
+    if (I.dtlog_dev) CK(cudaFree(I.dtlog_dev));
+    CK(cudaMalloc(&I.dtlog_dev, sizeof(double) * n_steps));
+    I.dtlog_cap = n_steps;
+  }
   DtState h{};
   h.dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);
   h.t = t0;
@@ -860,6 +900,8 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
   h.step = -1;
   h.t_end = t_end;
   h.cfl = I.opt.cfl;
+  h.dt_log = dt_out ? I.dtlog_dev : nullptr;
+  h.until = until ? 1 : 0;
   CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
   // census rows are indexed by the device step counter
   I.S.census = census ? I.census_dev : nullptr;
@@ -868,20 +910,30 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
   const int cur0 = I.cur;
   // the first step's max_stable_dt term; each step's final gather reduces the next one
   int64_t nl = I.launch_dt_reduce(I.ubuf[I.cur]);
-  for (int s = 0; s < n_steps; ++s) {
-    if (graphs) {
-      // graphs capture the census flag; keep separate graphs only for census runs
-      if (census) {
-        nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], true);
+  const int batch = until ? 32 : n_steps;
+  int launched = 0;
+  int k = 0, f = 0, c = 0;
+  while (launched < n_steps) {
+    const int nb = std::min(batch, n_steps - launched);
+    for (int s = 0; s < nb; ++s) {
+      if (graphs) {
+        // graphs capture the census flag; keep separate graphs only for census runs
+        if (census) {
+          nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], true);
+        } else {
+          cudaGraphExec_t g = I.get_graph(rk, true, I.cur);
+          CK(cudaGraphLaunch(g, I.stream));
+          nl += I.graph_launches[rk][1][I.cur];
+        }
       } else {
-        cudaGraphExec_t g = I.get_graph(rk, true, I.cur);
-        CK(cudaGraphLaunch(g, I.stream));
-        nl += I.graph_launches[rk][1][I.cur];
+        nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], census);
       }
-    } else {
-      nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], census);
+      I.cur ^= 1;
     }
-    I.cur ^= 1;
+    launched += nb;
+    if (!until) break;
+    I.allreduce_error();
+    if (I.read_error(&k, &f, &c)) break;  // t_end reached (kErrDone) or a failure
   }
   I.launches = nl;
   I.S.step = I.step_zero;
@@ -889,27 +941,38 @@ double GpuSolver::run_steps(int n_steps, int rk, double t0, double t_end, int64_
   if (census && I.comm)
     NK(nccl().AllReduce(I.census_dev, I.census_dev, 4 * static_cast<size_t>(n_steps), ncclUint64, ncclSum, I.comm,
                         I.stream));
-  I.allreduce_error();
+  if (!until) I.allreduce_error();
   CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
-  int k, f, c;
-  if (I.read_error(&k, &f, &c)) {
+  I.read_error(&k, &f, &c);
+  // steps that ran to completion: the device counter holds the last started step
+  int ran = launched;
+  if (until && (k & kErrDone)) ran = h.step + 1;
+  if (k & ~kErrDone) {
     // step s reads ubuf[(cur0 + s) & 1] and never overwrites it: the failing
     // step's input is the last good state (the reference throws out of
     // advance()/max_stable_dt() before touching state_)
     const int failed = std::min(std::max(0, I.err_step), n_steps - 1);
     I.cur = (cur0 + failed) & 1;
+    *n_done = failed;
     try {
-      I.raise_device_error(k, f, c);
+      I.raise_device_error(k & ~kErrDone, f, c);
     } catch (ApiError& e) {
       throw ApiError(e.code, "run failed at step " + std::to_string(failed) + ": " + e.what());
     }
   }
-  if (census) {
-    std::vector<unsigned long long> tmp(4 * static_cast<size_t>(n_steps));
+  if (k & kErrDone) {
+    I.reset_error();
+    I.cur = (cur0 + ran) & 1;
+  }
+  *n_done = ran;
+  if (census && ran > 0) {
+    std::vector<unsigned long long> tmp(4 * static_cast<size_t>(ran));
     CK(cudaMemcpy(tmp.data(), I.census_dev, tmp.size() * sizeof(tmp[0]), cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < tmp.size(); ++i) census_out[i] = static_cast<int64_t>(tmp[i]);
   }
+  if (dt_out && ran > 0) CK(cudaMemcpy(dt_out, I.dtlog_dev, sizeof(double) * ran, cudaMemcpyDeviceToHost));
   I.stage_is_first = false;
+  CK(cudaStreamSynchronize(I.stream));
   return h.t + h.dt;
 }
 

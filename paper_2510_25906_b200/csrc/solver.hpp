@@ -25,7 +25,9 @@ class GpuSolver {
   double max_stable_dt();                                            // solver.cpp:103-111
   void advance(double dt, double t, int rk);                         // solver.cpp:381-387
   void compute_residual(const double* u, double t, double* out);     // solver.cpp:316-379
-  double run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census);  // run.cpp:97-132
+  double run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census, double* dt_out = nullptr);
+  // run_simulation's loop condition (run.cpp:96): steps while t < t_end - 1e-14 t_end, at most max_steps
+  double run_until(int max_steps, int rk, double t0, double t_end, int64_t* census, double* dt_out, int* n_done);  // run.cpp:97-132
 
   void get_labels(uint8_t* out, bool step);
   void get_census(int64_t counts[4]);
@@ -46,6 +48,8 @@ class GpuSolver {
   void attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub);
 
  private:
+  double run_impl(int n_steps, int rk, double t0, double t_end, bool until, int64_t* census, double* dt_out,
+                  int* n_done);
   struct Impl;
   std::unique_ptr<Impl> p_;
 };

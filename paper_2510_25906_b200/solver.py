@@ -139,6 +139,28 @@ class Solver:
                                            cen.ctypes.data_as(A.c_i64p) if census else None))
         return t.value, cen
 
+    def run_log(self, n_steps: int, rk: int = A.RK3, t0: float = 0.0, t_end: float = float("inf")):
+        """run_steps that also returns each step's dt: (t, census[n,4], dt[n])."""
+        t = C.c_double()
+        cen = np.zeros((n_steps, 4), dtype=np.int64)
+        dts = np.zeros(n_steps)
+        self._ck(self._lib.ucfvb_run_steps_log(self._h, int(n_steps), int(rk), float(t0), float(t_end), C.byref(t),
+                                               cen.ctypes.data_as(A.c_i64p), _dp(dts)))
+        return t.value, cen, dts
+
+    def run_until(self, t_end: float, rk: int = A.RK3, t0: float = 0.0, max_steps: int = 1 << 20,
+                  census: bool = True):
+        """run_simulation's loop (run.cpp:96-132): step while t < t_end - 1e-14 t_end (at most
+        max_steps). Returns (t, n_steps, census[n,4] or None, dt[n])."""
+        t = C.c_double()
+        n = C.c_int32()
+        cen = np.zeros((max_steps, 4), dtype=np.int64) if census else None
+        dts = np.zeros(max_steps)
+        self._ck(self._lib.ucfvb_run_until(self._h, int(max_steps), int(rk), float(t0), float(t_end), C.byref(t),
+                                           C.byref(n), cen.ctypes.data_as(A.c_i64p) if census else None, _dp(dts)))
+        k = n.value
+        return t.value, k, (cen[:k] if census else None), dts[:k]
+
     def step_labels(self) -> np.ndarray:
         out = np.zeros(self.n_cells, dtype=np.uint8)
         self._ck(self._lib.ucfvb_get_step_labels(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8))))

@@ -7,6 +7,8 @@
 
 #include <cstdint>
 
+#include "exact_math.h"
+
 namespace ucfvb {
 
 constexpr int NV = 4;
@@ -30,13 +32,7 @@ __device__ __forceinline__ void st4(double4* p, const double* a) {
   *p = make_double4(a[0], a[1], a[2], a[3]);
 }
 
-// pressure / is_physical (euler.hpp:30-36)
-__device__ __forceinline__ double pressure(const double* s, double g) {
-  return (g - 1.0) * (s[3] - 0.5 * (s[1] * s[1] + s[2] * s[2]) / s[0]);
-}
-__device__ __forceinline__ bool is_physical(const double* s, double g) {
-  return s[0] > 0.0 && pressure(s, g) > 0.0;
-}
+
 
 // cons_to_prim (euler.hpp:38-45): returns false where the reference throws
 __device__ __forceinline__ bool cons_to_prim(const double* s, double g, double& rho, double& u, double& v,

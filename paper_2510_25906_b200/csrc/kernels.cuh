@@ -84,6 +84,11 @@ struct Layout {
 struct Physics {
   MarginParams mp;
   double gamma, lambda1p, weno_eps, weno_b;
+  // CWENOZ linear weights (reconstruct.cpp:104-106), host-computed with the
+  // same IEEE operations: lam0 = 1 - 1/lambda1', lams[nd] = (1 - lam0)/nd, and
+  // the correctly rounded reciprocals div_rn needs (nd = directional stencils)
+  double lam0, inv_lam0;
+  double lams[5], nd_d[5], inv_nd[5];
   int limiter;  // 0 BJ, 1 Venkat
   int hll;      // 0 HLLC, 1 HLL
   double qw[4];  // face quadrature weights (identical on every face)
@@ -226,6 +231,20 @@ __device__ __forceinline__ bool group_demote(const Physics& ph, int v, double lo
       bad |= !is_physical(s, ph.gamma);
       if (v == 0 || v == 3) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
     }
+  }
+  return grp_any(bad);
+}
+
+// group_demote with the positivity check spread over the group (each lane
+// tests Q/4 face points after a register transpose, group_nonphysical)
+template <int Q>
+__device__ __forceinline__ bool group_demote_t(const Physics& ph, int v, double lo, double hi, const double* vals) {
+  double dm, dw;
+  compute_margins(ph.mp, hi - lo, dm, dw);
+  bool bad = group_nonphysical<Q>(vals, Q, ph.gamma);
+  if (v == 0 || v == 3) {
+#pragma unroll
+    for (int lq = 0; lq < Q; ++lq) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
   }
   return grp_any(bad);
 }

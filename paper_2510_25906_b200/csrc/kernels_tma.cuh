@@ -611,16 +611,18 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
         fence_proxy_async_smem();
         issue_a(next);
       }
-      constexpr int st1 = NF + 1;
-      const double lam0 = 1.0 - 1.0 / ph.lambda1p;
-      const double lams = (1.0 - lam0) / (st1 - 1);
+      // lam0 = 1 - 1/lambda1', lams = (1 - lam0)/(st - 1) (reconstruct.cpp:104-106), host-computed;
+      // the divisions by lam0, st - 1 and wsum are div_rn (correctly rounded, as x / d)
+      const double lam0 = ph.lam0;
+      const double lams = ph.lams[NF];
+      const bool rl = lam0 >= 0x1p-60;
 #pragma unroll
       for (int s = 0; s < NF; ++s) {
         p1[0] -= lams * dir[s][0];
         p1[1] -= lams * dir[s][1];
       }
 #pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] /= lam0;
+      for (int k = 0; k < K; ++k) p1[k] = rl ? div_rn(p1[k], lam0, ph.inv_lam0) : p1[k] / lam0;
       mbar_wait(&bar[1], par);
       const double* soi = reinterpret_cast<const double*>(gb);
       const double* sph = reinterpret_cast<const double*>(gb + St::C_OI);
@@ -642,7 +644,7 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
         sis[s] = o00 * a0 * a0 + (o01 + o10) * a0 * a1 + o11 * a1 * a1;
         tau += fabs(sis[s] - si0);
       }
-      tau /= (st1 - 1);
+      tau = div_rn(tau, ph.nd_d[NF], ph.inv_nd[NF]);
       tau = tau_pow(tau, ph.weno_b);
       double om0 = lam0 * (1.0 + tau / (ph.weno_eps + si0));
       double oms[NF];
@@ -652,12 +654,16 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
         oms[s] = lams * (1.0 + tau / (ph.weno_eps + sis[s]));
         wsum += oms[s];
       }
-      om0 /= wsum;
+      const double rw = 1.0 / wsum;  // wsum >= lam0 > 0
+      const bool rwok = rl && wsum <= 0x1p60;
+      om0 = rwok ? div_rn(om0, wsum, rw) : om0 / wsum;
+#pragma unroll
+      for (int s = 0; s < NF; ++s) oms[s] = rwok ? div_rn(oms[s], wsum, rw) : oms[s] / wsum;
 #pragma unroll
       for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
 #pragma unroll
       for (int s = 0; s < NF; ++s) {
-        const double w = oms[s] / wsum;
+        const double w = oms[s];  // oms[s] / wsum
         p1[0] += w * dir[s][0];
         p1[1] += w * dir[s][1];
       }

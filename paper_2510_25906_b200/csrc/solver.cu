@@ -687,6 +687,13 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   ph.mp = MarginParams{mg.alpha_m, mg.beta_m, mg.alpha_w, mg.beta_w, mg.kappa, mg.deact_n};
   ph.gamma = o.gamma;
   ph.lambda1p = o.lambda1p;
+  ph.lam0 = 1.0 - 1.0 / o.lambda1p;
+  ph.inv_lam0 = 1.0 / ph.lam0;
+  for (int nd = 1; nd <= 4; ++nd) {
+    ph.nd_d[nd] = static_cast<double>(nd);
+    ph.lams[nd] = (1.0 - ph.lam0) / nd;
+    ph.inv_nd[nd] = 1.0 / nd;
+  }
   ph.weno_eps = o.weno_eps;
   ph.weno_b = o.weno_b;
   ph.limiter = o.limiter;

@@ -160,36 +160,32 @@ __device__ __forceinline__ int grp_max(int s) {
   return s;
 }
 
-__device__ __forceinline__ double pick4(double a, double b, double c, double d, int i) {
-  return i == 0 ? a : (i == 1 ? b : (i == 2 ? c : d));
-}
-
 // is_physical (euler.hpp:34-36) of the cell's Q face points without the 4x
-// redundancy: lane v holds variable v of every point; a 4x4 transpose through
-// rotated shuffles hands lane v all four variables of points v, v+4, ... and
-// each lane checks only those. Returns this lane's verdict (OR over the group
-// with grp_any).
+// redundancy: lane v holds variable v of every point; a 4x4 butterfly
+// transpose (shfl_xor 2, then shfl_xor 1, with selects on the lane's two
+// index bits) hands lane v all four variables of points v, v+4, ... and each
+// lane checks only those. Returns this lane's verdict (OR over the group with
+// grp_any).
 template <int Q>
 __device__ __forceinline__ bool group_nonphysical(const double* vals, int nq_cell, double gamma) {
   const int v = threadIdx.x & 3;
-  const int base = (threadIdx.x & 31) & ~3;
+  const bool b0 = v & 1, b1 = v & 2;
   bool bad = false;
 #pragma unroll
   for (int r = 0; r < (Q + 3) / 4; ++r) {
-    double t[4];
+    double row[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      // step k: send point 4r + ((v - k) & 3), receive variable (v + k) & 3 of point 4r + v
-      const int si = (v - k) & 3;
-      double send = 1.0;
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (i == si && 4 * r + i < Q) send = vals[4 * r + i];
-      t[k] = __shfl_sync(kFull, send, base | ((v + k) & 3));
-    }
-    double st[NV];
-#pragma unroll
-    for (int j = 0; j < NV; ++j) st[j] = pick4(t[0], t[1], t[2], t[3], (j - v) & 3);
+    for (int j = 0; j < 4; ++j) row[j] = 4 * r + j < Q ? vals[4 * r + j] : 1.0;
+    // step 1 (lane v^2): keep the two points whose bit 1 equals ours, trade the other two
+    const double k0 = b1 ? row[2] : row[0], k1 = b1 ? row[3] : row[1];
+    const double c0 = __shfl_xor_sync(kFull, b1 ? row[0] : row[2], 2);
+    const double c1 = __shfl_xor_sync(kFull, b1 ? row[1] : row[3], 2);
+    // step 2 (lane v^1): keep point v, trade point v^1 (own and the v^2 row's values)
+    const double A = b0 ? k1 : k0, C = b0 ? c1 : c0;  // variables v, v^2 of point v
+    const double B = __shfl_xor_sync(kFull, b0 ? k0 : k1, 1);  // variable v^1
+    const double D = __shfl_xor_sync(kFull, b0 ? c0 : c1, 1);  // variable v^3
+    const double P0 = b0 ? B : A, Q0 = b0 ? D : C, P1 = b0 ? A : B, Q1 = b0 ? C : D;
+    const double st[NV] = {b1 ? Q0 : P0, b1 ? Q1 : P1, b1 ? P0 : Q0, b1 ? P1 : Q1};
     if (4 * r + v < nq_cell) bad |= !is_physical(st, gamma);
   }
   return bad;

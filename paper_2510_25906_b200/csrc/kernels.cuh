@@ -209,38 +209,19 @@ __device__ __forceinline__ void var_bounds(const Layout& L, const double* __rest
   }
 }
 
-// fallback_check (solver.cpp:229-264) of a reconstructed cell, group-wide:
-// positivity of every face point (needs all four variables: shuffles) and the
-// relaxed DMP of rho (lane 0) and E (lane 3) against delta_m.
+// fallback_check's verdict for one cell (solver.cpp:229-264): positivity of
+// the first nq_cell face points spread over the group (group_nonphysical) and
+// the relaxed DMP of rho (lane 0) and E (lane 3) against delta_m.
 template <int Q>
 __device__ __forceinline__ bool group_demote(const Physics& ph, int v, double lo, double hi, const double* vals,
                                              int nq_cell) {
   double dm, dw;
   compute_margins(ph.mp, hi - lo, dm, dw);
-  bool bad = false;
-#pragma unroll
-  for (int lq = 0; lq < Q; ++lq) {
-    if (lq < nq_cell) {
-      double s[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) s[j] = grp_get(vals[lq], j);
-      bad |= !is_physical(s, ph.gamma);
-      if (v == 0 || v == 3) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
-    }
-  }
-  return grp_any(bad);
-}
-
-// group_demote with the positivity check spread over the group (each lane
-// tests Q/4 face points after a register transpose, group_nonphysical)
-template <int Q>
-__device__ __forceinline__ bool group_demote_t(const Physics& ph, int v, double lo, double hi, const double* vals) {
-  double dm, dw;
-  compute_margins(ph.mp, hi - lo, dm, dw);
-  bool bad = group_nonphysical<Q>(vals, Q, ph.gamma);
+  bool bad = group_nonphysical<Q>(vals, nq_cell, ph.gamma);
   if (v == 0 || v == 3) {
 #pragma unroll
-    for (int lq = 0; lq < Q; ++lq) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
+    for (int lq = 0; lq < Q; ++lq)
+      if (lq < nq_cell) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
   }
   return grp_any(bad);
 }

@@ -246,10 +246,7 @@ struct TroubledStage {
   static constexpr uint32_t MB = M_PHI + M_NBR;
   static constexpr uint32_t A_BYTES = CA > MA ? CA : MA;
   static constexpr uint32_t B_BYTES = CB > MB ? CB : MB;
-  // the group-B buffer doubles as k_troubled_split's fallback scratch (32 cells x (4Q+2) doubles)
-  static constexpr uint32_t FB_BYTES = 32 * (4 * Q + 2) * 8;
-  static constexpr uint32_t B_REGION = B_BYTES > FB_BYTES ? B_BYTES : FB_BYTES;
-  static constexpr uint32_t SPLIT_BYTES = A_BYTES + B_REGION;
+  static constexpr uint32_t SPLIT_BYTES = A_BYTES + B_BYTES;
 };
 
 // k_troubled_tma: the CWENOZ and MUSCL reconstructions of one stage in one
@@ -740,37 +737,13 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
 #pragma unroll
       for (int k = 0; k < K; ++k) kd[k] = k == 0 ? d0 : (k == 1 ? d1 : 0.0);
     }
-    __syncthreads();  // group B consumed: its buffer is the fallback scratch below
-    bool demote = false;
-    if (flags & FL_FALLBACK) {
-      // fallback_check (solver.cpp:229-264). Positivity of the cell's Q face points is
-      // spread over its four lanes through shared memory (lane v tests points v, v+4):
-      // a quarter of the is_physical work of every lane testing every point.
-      constexpr int SV = 4 * Q + 2;  // per-cell stride in doubles (16 B aligned, bank spread)
-      static_assert(32 * SV * 8 <= St::B_REGION, "fallback scratch exceeds the group-B buffer");
-      double* sv = reinterpret_cast<double*>(gb) + slot * SV;
-#pragma unroll
-      for (int lq = 0; lq < Q; ++lq) sv[lq * 4 + v] = vals[lq];
-      __syncwarp();
-      bool bad = false;
-#pragma unroll
-      for (int r = 0; r < (Q + 3) / 4; ++r) {
-        const int lq = 4 * r + v;
-        if (lq < Q) {
-          const double2 a = *reinterpret_cast<const double2*>(sv + lq * 4);
-          const double2 b = *reinterpret_cast<const double2*>(sv + lq * 4 + 2);
-          const double s4[NV] = {a.x, a.y, b.x, b.y};
-          bad |= !is_physical(s4, ph.gamma);
-        }
-      }
-      if (v == 0 || v == 3) {  // relaxed DMP of rho and E against delta_m
-        double dm, dw;
-        compute_margins(ph.mp, hi - lo, dm, dw);
-#pragma unroll
-        for (int lq = 0; lq < Q; ++lq) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
-      }
-      demote = grp_any(bad);
+    __syncthreads();  // group B consumed: request the next item's
+    if (tid == 0 && next < nitems) {
+      fence_proxy_async_smem();
+      issue_b(next);
     }
+    bool demote = false;
+    if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);
     if (mine) {
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
@@ -779,11 +752,6 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
 #pragma unroll
         for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = demote ? 0.0 : kd[k];
       }
-    }
-    if (flags & FL_FALLBACK) __syncthreads();  // scratch consumed
-    if (tid == 0 && next < nitems) {  // request the next item's group B
-      fence_proxy_async_smem();
-      issue_b(next);
     }
   }
 }

@@ -795,41 +795,45 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
 
 // ---------------------------------------------------------------------------
 // k_gather_rk: assemble_fluxes pass 2 (solver.cpp:294-311) fused with the RK
-// stage combination. Four lanes per cell (lane v = variable v): acc = sum over
-// the cell's faces, in the cell's face order, of +-face_flux; residual =
-// -acc * (1/area); out = sum_i coef_i * term_i left to right (combine2,
-// time_integrator.cpp:31-38; final SSPRK(5,4) line :70-73). Owner-ordered:
-// no atomics.
+// stage combination, one thread per cell (all four variables, 32 B loads and
+// stores: the pass is latency-bound and this keeps 3 + nterms independent
+// loads in flight per thread). acc = sum over the cell's faces, in the cell's
+// face order, of +-face_flux (scattered into the cell's slots by k_face_flux);
+// residual = -acc * (1/area); out = sum_i coef_i * term_i left to right
+// (combine2, time_integrator.cpp:31-38; final SSPRK(5,4) line :70-73).
+// Owner-ordered: no atomics.
 template <int NF, bool UNI>
 __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags, DtState* ds,
-                                                      double gamma) {
-  const int g = blockIdx.x * kBlock + threadIdx.x;
-  const int v = g & 3;
-  const int c0 = g >> 2;
+                                                       double gamma) {
+  const int c0 = blockIdx.x * kBlock + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool live = c0 < L.n_owned;
   const int c = live ? c0 : L.n_owned - 1;
-  const double* rsd = reinterpret_cast<const double*>(S.rs);
-  // RK terms were written by earlier stages (complete before our predecessor
-  // started) and 1/area is static: both are fetched while the face kernel drains
-  double term[5];
+  // RK terms were written by earlier stages and 1/area is static: fetched while the face kernel drains
+  d4 term[5];
 #pragma unroll
-  for (int i = 0; i < 5; ++i)
-    term[i] = (i < rk.nterms && rk.term[i]) ? __ldg(reinterpret_cast<const double*>(rk.term[i] + c) + v) : 0.0;
+  for (int i = 0; i < 5; ++i) {
+    if (i < rk.nterms && rk.term[i]) {
+      term[i] = ld4(rk.term[i] + c);
+    } else {
+      term[i] = d4{{0.0, 0.0, 0.0, 0.0}};
+    }
+  }
   const double inv_vol = L.inv_vol[c];
   pdl_wait();
   const int err0 = *(volatile int*)S.err;
   const int nf = UNI ? NF : L.nfc[c];
-  // acc += sgn * face_flux_ in the cell's face order; the signed terms were
-  // scattered into this cell's slots by k_face_flux (coalesced reads here)
-  double acc = 0.0;
+  double acc[NV] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int j = 0; j < NF; ++j)
-    if (j < nf) acc += rsd[4 * aos(c, j, NF) + v];
+    if (j < nf) {
+      const d4 r = ld4(&S.rs[aos(c, j, NF)]);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] += r.v[v];
+    }
   if (flags & (FL_CENSUS | FL_STEP_LABELS)) {
-    const bool leader = live && v == 0;
-    const int lab = leader ? S.labels[c] : -1;
-    if ((flags & FL_STEP_LABELS) && leader && !err0) S.step_labels[c] = static_cast<uint8_t>(lab);
+    const int lab = live ? S.labels[c] : -1;
+    if ((flags & FL_STEP_LABELS) && live && !err0) S.step_labels[c] = static_cast<uint8_t>(lab);
     if ((flags & FL_CENSUS) && !err0) {
       unsigned long long* row = S.census + 4 * static_cast<size_t>(*S.step);
 #pragma unroll
@@ -839,29 +843,33 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
       }
     }
   }
-  const double r = -acc * inv_vol;
-  double o = 0.0;
+  double r[NV], o[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    r[v] = -acc[v] * inv_vol;
+    o[v] = 0.0;
+  }
   if (rk.out) {
     const double dt = rk.nterms ? *rk.dt : 0.0;
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
       if (i < rk.nterms) {
         const double w = rk.dt_scaled[i] ? rk.coef[i] * dt : rk.coef[i];
-        const double x = rk.term[i] ? term[i] : r;
-        o = (i == 0) ? w * x : o + w * x;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const double x = rk.term[i] ? term[i].v[v] : r[v];
+          o[v] = (i == 0) ? w * x : o[v] + w * x;
+        }
       }
     }
   }
   if (live && !err0) {
-    if (rk.rhs_out) reinterpret_cast<double*>(rk.rhs_out + c)[v] = r;
-    if (rk.out) reinterpret_cast<double*>(rk.out + c)[v] = o;
+    if (rk.rhs_out) st4(rk.rhs_out + c, r);
+    if (rk.out) st4(rk.out + c, o);
   }
   if (flags & FL_DT) {  // max_stable_dt of the new state, for the next step (block-uniform branch)
-    double s4[NV];
-#pragma unroll
-    for (int jv = 0; jv < NV; ++jv) s4[jv] = grp_get(o, jv);
     double x = 1e300;
-    if (v == 0 && live && !err0 && !dt_term(s4, gamma, L.h[c], x)) {
+    if (live && !err0 && !dt_term(o, gamma, L.h[c], x)) {
       x = 1e300;
       ds->dt_bad = 1;
       atomicMin(&S.err[2], c);

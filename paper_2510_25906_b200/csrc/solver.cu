@@ -317,7 +317,7 @@ struct GpuSolver::Impl {
 
   size_t l2_window_bytes = 0, l2_persist_bytes = 0;
   bool per_cell_lists = false;  // UCFVB_TROUBLED=lists: dense per-cell class lists instead of chunk lists
-  dim3 grid_owned4() const { return dim3((4 * L.n_owned + kBlock - 1) / kBlock); }
+  dim3 grid_owned() const { return dim3((L.n_owned + kBlock - 1) / kBlock); }
 
   // halo exchange of a stage state: pack per peer, then one grouped send/recv
   int64_t exchange(double4* buf) {
@@ -422,7 +422,7 @@ struct GpuSolver::Impl {
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
     ks.face_flux(dim3((L.n_faces + ks.faces_per_flux_block - 1) / ks.faces_per_flux_block), stream, L, ph, S);
-    ks.gather(grid_owned4(), stream, L, S, rk, ff | (dt_next ? FL_DT : 0), ds, opt.gamma);
+    ks.gather(grid_owned(), stream, L, S, rk, ff | (dt_next ? FL_DT : 0), ds, opt.gamma);
     ++nl;
     record(4);
     CK(cudaGetLastError());

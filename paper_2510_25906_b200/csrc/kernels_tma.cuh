@@ -240,10 +240,11 @@ struct TroubledStage {
   static constexpr uint32_t BYTES = C_BYTES > M_BYTES ? C_BYTES : M_BYTES;
   // split-phase groups (k_troubled_split): A = what the directional / linear
   // solves read, B = what the blend, evaluation and fallback read
+  static constexpr uint32_t DEST = round16(Q * 32 * 4);  // face-point destinations (the stores' addresses)
   static constexpr uint32_t CA = C_DIDX + C_PDIR + C_DOFS;
-  static constexpr uint32_t CB = C_OI + C_PHI + C_NBR;
+  static constexpr uint32_t CB = C_OI + C_PHI + C_NBR + DEST;
   static constexpr uint32_t MA = M_IDX + M_PLIN;
-  static constexpr uint32_t MB = M_PHI + M_NBR;
+  static constexpr uint32_t MB = M_PHI + M_NBR + DEST;
   static constexpr uint32_t A_BYTES = CA > MA ? CA : MA;
   static constexpr uint32_t B_BYTES = CB > MB ? CB : MB;
   static constexpr uint32_t SPLIT_BYTES = A_BYTES + B_BYTES;
@@ -554,12 +555,15 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
       bulk_g2s(p, L.phi + ch * Q * K * 32, St::C_PHI, &bar[1]);
       p += St::C_PHI;
       bulk_g2s(p, L.nbr + ch * NF * 32, St::C_NBR, &bar[1]);
+      p += St::C_NBR;
     } else {
       mbar_arrive_expect_tx(&bar[1], St::MB);
       bulk_g2s(p, L.phi01 + ch * Q * 2 * 32, St::M_PHI, &bar[1]);
       p += St::M_PHI;
       bulk_g2s(p, L.nbr + ch * NF * 32, St::M_NBR, &bar[1]);
+      p += St::M_NBR;
     }
+    bulk_g2s(p, L.dest + ch * Q * 32, St::DEST, &bar[1]);
   };
   if (tid == 0 && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);
@@ -737,6 +741,13 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
 #pragma unroll
       for (int k = 0; k < K; ++k) kd[k] = k == 0 ? d0 : (k == 1 ? d1 : 0.0);
     }
+    int dst[Q];  // face-point destinations, staged with group B
+    {
+      const int* sdst = reinterpret_cast<const int*>(gb + (i < nc ? St::C_OI + St::C_PHI + St::C_NBR
+                                                                  : St::M_PHI + St::M_NBR));
+#pragma unroll
+      for (int lq = 0; lq < Q; ++lq) dst[lq] = sdst[lq * 32 + slot];
+    }
     __syncthreads();  // group B consumed: request the next item's
     if (tid == 0 && next < nitems) {
       fence_proxy_async_smem();
@@ -746,7 +757,7 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
     if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);
     if (mine) {
 #pragma unroll
-      for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
+      for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(dst[lq]) + v] = demote ? u0 : vals[lq];
       if (demote && v == 0) S.labels[c] = 3;
       if (flags & FL_TAPS) {
 #pragma unroll

@@ -191,6 +191,18 @@ __device__ __forceinline__ bool group_nonphysical(const double* vals, int nq_cel
   return bad;
 }
 
+// NAD detector value (solver.cpp:136-141): v = max over the cell's face points
+// q of max(lo - u_q, u_q - hi), starting from v0 = -1e300, from the running
+// min / max of u_q. Exact: RN(lo - u) is non-increasing and RN(u - hi)
+// non-decreasing in u, so the per-point maxima are attained at min_q u_q and
+// max_q u_q; std::max ignores NaN points in both forms (a NaN point leaves
+// the running value unchanged), and the sign of a zero v is never observed
+// (v only enters comparisons and |v - delta|). The fallback pre-check's
+// "some q with max(lo - u_q, u_q - hi) > delta_m" is then v > delta_m.
+__device__ __forceinline__ double nad_violation(double v0, double lo, double hi, double qmin, double qmax) {
+  return smax(v0, smax(lo - qmin, qmax - hi));
+}
+
 // neighbourhood bounds of this lane's variable over {c} U face neighbours
 // (solver.cpp:120-129, 207-211)
 template <int NF>
@@ -274,7 +286,7 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
   const double du = hi - lo;
   double dm, dw;
   compute_margins(ph.mp, du, dm, dw);
-  double vmax = -1e300;
+  double vmax = -1e300, qmin = INFINITY, qmax = -INFINITY;
   bool bad = false;
   const double* fp = L.phi + aos(c, 0, Q * K);
   double* fv = reinterpret_cast<double*>(S.fp);
@@ -288,13 +300,16 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
       for (int k = 0; k < K; ++k) val += acc[k] * __ldg(fp + (lq * K + k) * 32);
       vals[lq] = val;
       if (detect) {
-        const double x = smax(lo - val, val - hi);
-        vmax = smax(vmax, x);
-        if (v == 0 || v == 3) bad |= x > dm;
+        qmin = smin(qmin, val);
+        qmax = smax(qmax, val);
       }
     }
   }
-  if (detect) bad |= group_nonphysical<Q>(vals, nf * NQ, ph.gamma);
+  if (detect) {
+    vmax = nad_violation(vmax, lo, hi, qmin, qmax);
+    if (v == 0 || v == 3) bad |= vmax > dm;
+    bad |= group_nonphysical<Q>(vals, nf * NQ, ph.gamma);
+  }
   int sev = 0;
   bool tie = false;
   if (detect && (flags & FL_NAD) && (v == 0 || v == 3)) {

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
       const double du = hi - lo;
       double dm, dw;
       compute_margins(ph.mp, du, dm, dw);
-      double vmax = -1e300;
+      double vmax = -1e300, qmin = INFINITY, qmax = -INFINITY;
       bool bad = false;
       bool store = true;
       double vals[Q];
@@ -177,12 +177,13 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
         for (int k = 0; k < K; ++k) val += acc[k] * sf[(lq * K + k) * 32 + slot];
         vals[lq] = val;
         if (detect) {
-          const double x = smax(lo - val, val - hi);
-          vmax = smax(vmax, x);
-          if (v == 0 || v == 3) bad |= x > dm;
+          qmin = smin(qmin, val);
+          qmax = smax(qmax, val);
         }
       }
       if (detect) {
+        vmax = nad_violation(vmax, lo, hi, qmin, qmax);
+        if (v == 0 || v == 3) bad |= vmax > dm;
         bad |= group_nonphysical<Q>(vals, Q, ph.gamma);
         int sev = 0;
         bool tie = false;

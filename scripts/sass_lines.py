@@ -44,6 +44,10 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kregex}",
                           "--print-source", "sass"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
+    # one section per captured launch of the kernel: keep the first
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+    if len(starts) > 1:
+        rows = rows[: starts[1]]
     h = next(i for i, r in enumerate(rows) if "Address" in r)
     hdr = rows[h]
     ia, ie, iw, isrc = (hdr.index("Address"), hdr.index("Instructions Executed"),

@@ -38,7 +38,13 @@ struct CentralStage {
   static constexpr uint32_t NBR = round16(NF * 32 * 4);
   static constexpr uint32_t DEST = round16(Q * 32 * 4);
   static constexpr uint32_t B_BYTES = PHI + THR + NBR + DEST;
-  static constexpr uint32_t BYTES = A_BYTES + B_BYTES;  // one stage
+  // the U values of the chunk's central-stencil members, gathered with cp.async
+  // (8 B per lane and member) one chunk ahead. Only for the larger stencils
+  // (p = 3: 18 members), where hiding the gather latency beats the occupancy
+  // the extra 18 KB and registers cost (p = 3: central -8 %; p = 2: +3 %).
+  static constexpr bool PREFETCH = MM >= 16;
+  static constexpr uint32_t UG = PREFETCH ? MM * 128 * 8 : 0;
+  static constexpr uint32_t BYTES = A_BYTES + B_BYTES + UG;  // one stage
 };
 
 // k_central on the fast path: same arithmetic as k_central (kernels.cuh).
@@ -106,6 +112,22 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
       }
     return;
   }
+  // cp.async of this lane's stencil-member values of `chunk` (stage st, group A landed)
+  auto gather_ahead = [&](int chunk, int st) {
+    const unsigned char* b = smem + st * St::BYTES;
+    const int* si = reinterpret_cast<const int*>(b + St::PINV);
+    double* ug = reinterpret_cast<double*>(smem + st * St::BYTES + St::A_BYTES + St::B_BYTES);
+#pragma unroll
+    for (int m = 0; m < MM; ++m)
+      cp_async8(ug + m * 128 + tid, Ud + 4 * static_cast<size_t>(si[m * 32 + slot]) + v);
+    cp_async_commit();
+  };
+  if constexpr (St::PREFETCH) {
+    if (static_cast<int>(blockIdx.x) < nchunks) {
+      mbar_wait(&bar[0], 0);
+      gather_ahead(blockIdx.x, 0);
+    }
+  }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool detect = (flags & (FL_NAD | FL_PRECHECK)) != 0;
@@ -132,8 +154,15 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
 #pragma unroll
     for (int k = 0; k < K; ++k) acc[k] = 0.0;
     double um[MM];
+    if constexpr (St::PREFETCH) {
+      cp_async_wait_all();  // this lane's own prefetched member values
+      const double* ug = reinterpret_cast<const double*>(b + St::A_BYTES + St::B_BYTES);
 #pragma unroll
-    for (int m = 0; m < MM; ++m) um[m] = __ldg(Ud + 4 * static_cast<size_t>(si[m * 32 + slot]) + v);
+      for (int m = 0; m < MM; ++m) um[m] = ug[m * 128 + tid];
+    } else {
+#pragma unroll
+      for (int m = 0; m < MM; ++m) um[m] = __ldg(Ud + 4 * static_cast<size_t>(si[m * 32 + slot]) + v);
+    }
 #pragma unroll
     for (int m = 0; m < MM; ++m) {
       const double d = um[m] - u0;
@@ -217,6 +246,14 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
     if (tid == 0 && refill < nchunks) {
       fence_proxy_async_smem();
       issue_b(refill, st);
+    }
+    if constexpr (St::PREFETCH) {  // gather the next chunk's member values while the other warps finish this one
+      const int nxt = chunk + static_cast<int>(gridDim.x);
+      if (nxt < nchunks) {
+        const int st2 = (it + 1) % NS;
+        mbar_wait(&bar[2 * st2], ((it + 1) / NS) & 1);
+        gather_ahead(nxt, st2);
+      }
     }
   }
 }

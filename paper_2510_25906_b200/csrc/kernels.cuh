@@ -817,17 +817,17 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
 // residual = -acc * (1/area); out = sum_i coef_i * term_i left to right
 // (combine2, time_integrator.cpp:31-38; final SSPRK(5,4) line :70-73).
 // Owner-ordered: no atomics.
-template <int NF, bool UNI>
+template <int NF, bool UNI, int NT>  // NT >= rk.nterms: registers for the prefetched RK terms
 __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags, DtState* ds,
-                                                       double gamma) {
+                                                      double gamma) {
   const int c0 = blockIdx.x * kBlock + threadIdx.x;
   const int lane = threadIdx.x & 31;
   const bool live = c0 < L.n_owned;
   const int c = live ? c0 : L.n_owned - 1;
   // RK terms were written by earlier stages and 1/area is static: fetched while the face kernel drains
-  d4 term[5];
+  d4 term[NT];
 #pragma unroll
-  for (int i = 0; i < 5; ++i) {
+  for (int i = 0; i < NT; ++i) {
     if (i < rk.nterms && rk.term[i]) {
       term[i] = ld4(rk.term[i] + c);
     } else {
@@ -867,7 +867,7 @@ __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpi
   if (rk.out) {
     const double dt = rk.nterms ? *rk.dt : 0.0;
 #pragma unroll
-    for (int i = 0; i < 5; ++i) {
+    for (int i = 0; i < NT; ++i) {
       if (i < rk.nterms) {
         const double w = rk.dt_scaled[i] ? rk.coef[i] * dt : rk.coef[i];
 #pragma unroll

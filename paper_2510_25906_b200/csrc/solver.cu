@@ -193,7 +193,12 @@ KernelSet make_set() {
     launch_k(k_face_flux<NQ>, g, kBlock, 0, st, L, p, S);
   };
   s.gather = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const RkEpilogue& rk, int f, DtState* ds,
-                 double gamma) { launch_k(k_gather_rk<NF, UNI>, g, kBlock, 0, st, L, S, rk, f, ds, gamma); };
+                 double gamma) {
+    if (rk.nterms <= 3)
+      launch_k(k_gather_rk<NF, UNI, 3>, g, kBlock, 0, st, L, S, rk, f, ds, gamma);
+    else
+      launch_k(k_gather_rk<NF, UNI, 5>, g, kBlock, 0, st, L, S, rk, f, ds, gamma);
+  };
   s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
   if constexpr (MMT > 0 && UNI) {
     s.central_tma = true;

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <vector>
 
 #include "ucfvb.h"
 
@@ -18,6 +19,10 @@ void mesh_free(ucfvb_mesh* m);
 ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_exponent, int n_threads);
 ucfvb_stencil_view stencils_view(const ucfvb_stencils* s);
 void stencils_free(ucfvb_stencils* s);
+
+// column-pivoting Householder QR least-squares pseudo-inverse (the
+// ColPivHouseholderQR restatement in setup_stencil.cpp); false when rank < cols
+bool qr_pinv(const std::vector<double>& A, int rows, int cols, std::vector<double>& pinv);
 
 void project_initial(const ucfvb_mesh_view& m, int ic, const double* params, int n_params, uint64_t seed,
                      int degree, double gamma, int n_threads, double* u_out);

@@ -367,6 +367,10 @@ struct Builder {
 
 }  // namespace
 
+bool qr_pinv(const std::vector<double>& A, int rows, int cols, std::vector<double>& pinv) {
+  return lsq_pinv(A, rows, cols, pinv);
+}
+
 ucfvb_stencils* build_stencils(const ucfvb_mesh_view& m, int order, int si_exponent, int n_threads) {
   if (order < 1) throw ApiError(UCFVB_INVALID, "build_stencils: order must be >= 1");
   if (order > 8) throw ApiError(UCFVB_INVALID, "build_stencils: order must be <= 8");

@@ -1,0 +1,1034 @@
+// 3D stage pass on B200 (BASELINE configs 4-5).
+//
+// Five conserved variables per cell. Reconstruction kernels run one WARP PER
+// CONSERVED VARIABLE over a chunk of 32 cells (block = 5 warps = 160
+// threads): lane = cell, warp = variable, so every per-cell operator load is
+// a coalesced 256 B line (32-cell AoSoA chunks, as the 2D path), the five
+// warps of a block read the same operator lines (L1 hits after the first),
+// and each thread keeps only its variable's K accumulators. The cross-variable
+// steps (NAD severity over rho and E, positivity of the face values) meet in
+// shared memory. Op orders follow oracle/ucfv3_port.c (the 3D restatement of
+// the reference's 2D functions); kernels are compiled with --fmad=false.
+//
+//   k3_central   solve_dofs + evaluate_cell + NAD raw label + fallback pre-check  (solver.cpp:336-349, 113-149, 229-264)
+//   k3_spread    spread_flags (pull form) + class lists + Linear-cell demotion    (detector.cpp:37-53)
+//   k3_cwenoz    directional solves + CWENOZ blend + evaluate + fallback          (solver.cpp:167-188, reconstruct.cpp:43-150)
+//   k3_muscl     r=1 solve + BJ/Venkatakrishnan limiter + evaluate + fallback    (solver.cpp:189-221)
+//   k3_face_flux HLLC/HLL at every face Gauss point, summed in qp order          (solver.cpp:266-295)
+//   k3_gather_rk owner-ordered face->cell sum + SSP-RK combination               (solver.cpp:296-311, time_integrator.cpp:31-38)
+//   k3_dt        max_stable_dt                                                   (solver.cpp:103-111)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "device_math.cuh"
+#include "layout.hpp"
+#include "solver3d.hpp"
+
+namespace ucfvb {
+namespace {
+
+constexpr int V5 = 5;
+constexpr int MD3 = 6;
+constexpr int kCwList = 0, kMuList = 1, kBadFace = 2, kBadCell = 3;
+
+#define CK3(x)                                                                                      \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess) throw ApiError(UCFVB_CUDA, std::string("CUDA: ") + cudaGetErrorString(e_) + " at " #x); \
+  } while (0)
+
+__device__ __forceinline__ size_t ao(int c, int e, int E) {
+  return (static_cast<size_t>(c >> 5) * E + e) * 32 + (c & 31);
+}
+
+// pressure / is_physical / cons_to_prim with three momenta (euler.hpp:30-45)
+__device__ __forceinline__ double pressure3(const double* s, double g) {
+  return (g - 1.0) * (s[4] - 0.5 * (s[1] * s[1] + s[2] * s[2] + s[3] * s[3]) / s[0]);
+}
+__device__ __forceinline__ bool is_physical3(const double* s, double g) { return s[0] > 0.0 && pressure3(s, g) > 0.0; }
+
+struct P3 {
+  double rho, u, v, w, un, p, E, a;
+};
+__device__ __forceinline__ bool prep3(const double* s, const double* n, double g, P3& f) {
+  if (!(s[0] > 0.0)) return false;
+  const double u = s[1] / s[0], v = s[2] / s[0], w = s[3] / s[0];
+  const double p = (g - 1.0) * (s[4] - 0.5 * s[0] * (u * u + v * v + w * w));
+  if (!(p > 0.0)) return false;
+  f.rho = s[0], f.u = u, f.v = v, f.w = w, f.p = p;
+  f.un = u * n[0] + v * n[1] + w * n[2];
+  f.E = s[4];
+  f.a = sqrt(g * p / s[0]);
+  return true;
+}
+__device__ __forceinline__ void phys_flux3(const P3& f, const double* n, double* o) {
+  o[0] = f.rho * f.un;
+  o[1] = f.rho * f.u * f.un + f.p * n[0];
+  o[2] = f.rho * f.v * f.un + f.p * n[1];
+  o[3] = f.rho * f.w * f.un + f.p * n[2];
+  o[4] = (f.E + f.p) * f.un;
+}
+__device__ __forceinline__ void cons3(const P3& f, double* o) {
+  o[0] = f.rho, o[1] = f.rho * f.u, o[2] = f.rho * f.v, o[3] = f.rho * f.w, o[4] = f.E;
+}
+// hllc_flux / hll_flux (euler.cpp:40-89), Cartesian form of oracle/ucfv3_port.c
+__device__ __forceinline__ bool riemann3(bool hll, const double* UL, const double* UR, const double* n, double g,
+                                         double* out) {
+  P3 L, R;
+  if (!prep3(UL, n, g, L) || !prep3(UR, n, g, R)) return false;
+  const double SL = smin(L.un - L.a, R.un - R.a);
+  const double SR = smax(L.un + L.a, R.un + R.a);
+  if (SL >= 0.0) {
+    phys_flux3(L, n, out);
+  } else if (SR <= 0.0) {
+    phys_flux3(R, n, out);
+  } else if (!hll) {
+    const double dL = L.rho * (SL - L.un);
+    const double dR = R.rho * (SR - R.un);
+    const double Ss = (R.p - L.p + L.un * dL - R.un * dR) / (dL - dR);
+    const bool left = Ss >= 0.0;
+    const P3& K = left ? L : R;
+    const double SK = left ? SL : SR;
+    double WK[5], FK[5], Ws[5];
+    cons3(K, WK);
+    phys_flux3(K, n, FK);
+    const double coef = K.rho * (SK - K.un) / (SK - Ss);
+    Ws[0] = coef;
+    Ws[1] = coef * (Ss * n[0] + (K.u - K.un * n[0]));
+    Ws[2] = coef * (Ss * n[1] + (K.v - K.un * n[1]));
+    Ws[3] = coef * (Ss * n[2] + (K.w - K.un * n[2]));
+    Ws[4] = coef * (WK[4] / K.rho + (Ss - K.un) * (Ss + K.p / (K.rho * (SK - K.un))));
+#pragma unroll
+    for (int v = 0; v < V5; ++v) out[v] = FK[v] + SK * (Ws[v] - WK[v]);
+  } else {
+    double FL[5], FR[5], WL[5], WR[5];
+    phys_flux3(L, n, FL);
+    phys_flux3(R, n, FR);
+    cons3(L, WL);
+    cons3(R, WR);
+#pragma unroll
+    for (int v = 0; v < V5; ++v) out[v] = (SR * FL[v] - SL * FR[v] + SL * SR * (WR[v] - WL[v])) / (SR - SL);
+  }
+  return true;
+}
+
+struct Dev3 {
+  int n, nF, n_ops;
+  // per cell, 32-cell AoSoA
+  const int32_t* central;  // [M+1]
+  const int32_t* nbr;      // [NF]
+  const int32_t* slot;     // [Q]
+  const int32_t* cface;    // [NF] (face << 1) | side
+  const int32_t* opi;      // [n]
+  const double *thr, *eps2, *inv_vol, *h;
+  // per operator row, 32-row AoSoA
+  const double* pinv;      // [M][K]
+  const double* pinv_lin;  // [M][3]
+  const int32_t* dirm;     // [NF][MD]
+  const double* pinv_dir;  // [NF][3][MD]
+  const double* oi;        // [K][K]
+  const double* phi;       // [Q][K]
+  // faces
+  const double* fnrm;  // [nF][NQ][3]
+  const double* fwa;   // [nF][NQ]
+};
+
+struct Phys3 {
+  double gamma, cfl, lambda1p, weno_eps, weno_b, lam0, lams;
+  MarginParams mg;
+  int mode, limiter, hll, detect;
+};
+
+struct Work3 {
+  double* fp;        // [nF][NQ][2][5]
+  double* ff;        // [nF][5]
+  double* dofs;      // AoSoA [K*5]
+  double* bounds;    // AoSoA [4]
+  uint8_t* raw;      // raw label | prefail << 2
+  uint8_t* labels;
+  int32_t* lists;    // [2][n]
+  int32_t* counters; // cw, mu, bad face, bad cell
+  unsigned long long* dtmin;
+  double* dt;        // device dt of the current step
+  double* t;         // device time
+  unsigned long long* ties;
+};
+
+// ---- central: solve + evaluate + NAD + fallback pre-check -----------------------------
+template <int K, int M, int NF, int NQ>
+__global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
+                                                   int nad) {
+  constexpr int Q = NF * NQ;
+  __shared__ double sval[Q][V5][33];
+  __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
+  const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+  if (blockIdx.x == 0 && threadIdx.x < 2) W.counters[threadIdx.x] = 0;  // list counters of this stage
+  const int nch = (D.n + 31) >> 5;
+  for (int ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+    const int c = (ch << 5) + lane;
+    const bool act = c < D.n;
+    const int cc = act ? c : (D.n - 1);
+    const int op = D.opi[cc];
+    const double u0 = U[static_cast<size_t>(cc) * V5 + v];
+    double lo = u0, hi = u0;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      const double x = U[static_cast<size_t>(D.nbr[ao(cc, i, NF)]) * V5 + v];
+      lo = smin(lo, x);
+      hi = smax(hi, x);
+    }
+    double a[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a[k] = 0.0;
+#pragma unroll 2
+    for (int m = 0; m < M; ++m) {
+      const int id = D.central[ao(cc, m + 1, M + 1)];
+      const double d = U[static_cast<size_t>(id) * V5 + v] - u0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] += D.pinv[ao(op, m * K + k, M * K)] * d;
+    }
+    if (act) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) W.dofs[ao(c, k * V5 + v, K * V5)] = a[k];
+    }
+    const bool chk = (v == 0 || v == 4);
+    double viol = -1e300;
+    if (eval) {
+      for (int q = 0; q < Q; ++q) {
+        double val = u0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) val += a[k] * D.phi[ao(op, q * K + k, Q * K)];
+        if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = val;
+        sval[q][v][lane] = val;
+        if (chk) viol = smax(viol, smax(lo - val, val - hi));
+      }
+    }
+    // per checked variable: deactivation, severity vote and bounds failure
+    if (chk && eval) {
+      const int t = v == 0 ? 0 : 1;
+      const double du = hi - lo;
+      double dm, dw;
+      compute_margins(P.mg, du, dm, dw);
+      int sev = 0;
+      if (nad) {
+        const double thr = D.thr[cc];
+        const bool deact = P.mg.kappa > 0.0 && du < thr;
+        if (!deact) sev = violation_severity(viol, dm, dw);
+        const double sc = 1e-12 * smax(fabs(u0), smax(du, fabs(dm)));
+        const bool tie = (P.mg.kappa > 0.0 && fabs(du - thr) <= 1e-12 * thr) ||
+                         (!deact && (fabs(viol - dm) <= sc || fabs(viol - dw) <= 1e-12 * smax(fabs(u0), smax(du, fabs(dw)))));
+        if (tie && act) atomicAdd(W.ties, 1ull);
+        if (act) {
+          W.bounds[ao(c, 2 * t, 4)] = lo;
+          W.bounds[ao(c, 2 * t + 1, 4)] = hi;
+        }
+      }
+      s_sev[t][lane] = sev;
+      s_bf[t][lane] = viol > dm;
+    }
+    if (v == 0) s_pos[lane] = 0;
+    __syncthreads();
+    if (eval && nad) {
+      // positivity of every face value of the 32 cells, spread over the block
+      for (int p = threadIdx.x; p < Q * 32; p += 160) {
+        const int q = p >> 5, l = p & 31;
+        double s[5];
+#pragma unroll
+        for (int w = 0; w < V5; ++w) s[w] = sval[q][w][l];
+        if (!is_physical3(s, P.gamma)) s_pos[l] = 1;
+      }
+    }
+    __syncthreads();
+    if (v == 0 && act && nad) {
+      const int sev = max(s_sev[0][lane], s_sev[1][lane]);
+      const int fail = s_pos[lane] | s_bf[0][lane] | s_bf[1][lane];
+      W.raw[c] = static_cast<uint8_t>(sev | (fail << 2));
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int sev_of(int s) { return s == 0 ? 0 : (s == 1 ? 1 : 2); }
+
+// ---- spread + lists (hybrid detection stage) ------------------------------------------
+template <int NF, int NQ>
+__global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* __restrict__ U) {
+  constexpr int Q = NF * NQ;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int lab = 0;
+  bool ok = c < D.n;
+  if (ok) {
+    const int r = W.raw[c];
+    int sev = r & 3;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) sev = max(sev, static_cast<int>(W.raw[D.nbr[ao(c, i, NF)]] & 3));
+    lab = sev == 0 ? UCFVB_SCHEME_LINEAR : (sev == 1 ? UCFVB_SCHEME_CWENOZ : UCFVB_SCHEME_MUSCL);
+    if (lab == UCFVB_SCHEME_LINEAR && (r >> 2)) {
+      // fallback_check demotes the Linear candidate: first-order values (solver.cpp:256-262)
+      lab = UCFVB_SCHEME_FIRST;
+      for (int q = 0; q < Q; ++q) {
+        double* dst = &W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5];
+#pragma unroll
+        for (int v = 0; v < V5; ++v) dst[v] = U[static_cast<size_t>(c) * V5 + v];
+      }
+    }
+    W.labels[c] = static_cast<uint8_t>(lab);
+  }
+  // warp-aggregated appends to the CWENOZ / MUSCL lists
+  for (int L = 0; L < 2; ++L) {
+    const bool mine = ok && lab == (L == 0 ? UCFVB_SCHEME_CWENOZ : UCFVB_SCHEME_MUSCL);
+    const unsigned b = __ballot_sync(0xffffffffu, mine);
+    if (!b) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(&W.counters[L], __popc(b));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (mine) W.lists[static_cast<size_t>(L) * D.n + base + __popc(b & ((1u << lane) - 1u))] = c;
+  }
+}
+
+// forced modes: every cell in one list (SchemeMode::Cwenoz / Muscl, solver.cpp:322-328)
+__global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c == 0) W.counters[which] = n;
+  if (c < n) {
+    W.lists[static_cast<size_t>(which) * n + c] = c;
+    W.labels[c] = lab;
+  }
+}
+
+// evaluate the reconstruction of (cell, var) at its Q face points, stage the
+// values for the positivity check, and report the bounds failure (fallback_check)
+template <int K, int NQ, int NF>
+__device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
+                                           double u0, const double* a, double (*sval)[V5][33], bool chk,
+                                           double blo, double bhi, double& viol) {
+  constexpr int Q = NF * NQ;
+  for (int q = 0; q < Q; ++q) {
+    double val = u0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) val += a[k] * D.phi[ao(op, q * K + k, Q * K)];
+    if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = val;
+    sval[q][v][lane] = val;
+    if (chk) viol = smax(viol, smax(blo - val, val - bhi));
+  }
+}
+
+// fallback (solver.cpp:229-264) after a troubled reconstruction; demoted cells
+// get first-order values
+template <int NF, int NQ>
+__device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
+                                                  int lane, bool act, double u0, bool chk, double blo, double bhi,
+                                                  double viol, double (*sval)[V5][33], int* s_fail) {
+  constexpr int Q = NF * NQ;
+  if (v == 0) s_fail[lane] = 0;
+  __syncthreads();
+  if (P.mode == UCFVB_HYBRID) {
+    if (chk) {
+      double dm, dw;
+      compute_margins(P.mg, bhi - blo, dm, dw);
+      if (viol > dm) s_fail[lane] = 1;
+    }
+    for (int p = threadIdx.x; p < Q * 32; p += 160) {
+      const int q = p >> 5, l = p & 31;
+      double s[5];
+#pragma unroll
+      for (int w = 0; w < V5; ++w) s[w] = sval[q][w][l];
+      if (!is_physical3(s, P.gamma)) s_fail[l] = 1;
+    }
+  }
+  __syncthreads();
+  if (act && s_fail[lane]) {
+    if (v == 0) W.labels[c] = UCFVB_SCHEME_FIRST;
+    for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = u0;
+  }
+  __syncthreads();
+}
+
+// ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
+template <int K, int M, int NF, int NQ>
+__global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+  constexpr int Q = NF * NQ;
+  __shared__ double sval[Q][V5][33];
+  __shared__ int s_fail[32];
+  const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+  const int cnt = W.counters[kCwList];
+  const int32_t* list = W.lists;
+  for (int base = blockIdx.x * 32; base < cnt; base += gridDim.x * 32) {
+    const bool act = base + lane < cnt;
+    const int c = list[act ? base + lane : base];
+    const int op = D.opi[c];
+    const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    double dir[NF][3];
+#pragma unroll
+    for (int s = 0; s < NF; ++s) {
+      double x[MD3];
+#pragma unroll
+      for (int m = 0; m < MD3; ++m) {
+        const int j = D.dirm[ao(op, s * MD3 + m, NF * MD3)];
+        x[m] = U[static_cast<size_t>(D.central[ao(c, j, M + 1)]) * V5 + v] - u0;
+      }
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < MD3; ++m) acc += D.pinv_dir[ao(op, (s * 3 + k) * MD3 + m, NF * 3 * MD3)] * x[m];
+        dir[s][k] = acc;
+      }
+    }
+    double p1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p1[k] = W.dofs[ao(c, k * V5 + v, K * V5)];
+#pragma unroll
+    for (int s = 0; s < NF; ++s) {
+      p1[0] -= P.lams * dir[s][0];
+      p1[1] -= P.lams * dir[s][1];
+      p1[2] -= P.lams * dir[s][2];
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) p1[k] /= P.lam0;
+    // SI_0 = p1' OI p1 (row then dot) and the directional SI from the 3x3 block
+    double si0 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      double t = 0.0;
+#pragma unroll
+      for (int q = 0; q < K; ++q) t += D.oi[ao(op, k * K + q, K * K)] * p1[q];
+      si0 += p1[k] * t;
+    }
+    const double o00 = D.oi[ao(op, 0, K * K)], o01 = D.oi[ao(op, 1, K * K)], o02 = D.oi[ao(op, 2, K * K)];
+    const double o10 = D.oi[ao(op, K, K * K)], o11 = D.oi[ao(op, K + 1, K * K)], o12 = D.oi[ao(op, K + 2, K * K)];
+    const double o20 = D.oi[ao(op, 2 * K, K * K)], o21 = D.oi[ao(op, 2 * K + 1, K * K)],
+                 o22 = D.oi[ao(op, 2 * K + 2, K * K)];
+    double si[NF];
+    double tau = 0.0;
+#pragma unroll
+    for (int s = 0; s < NF; ++s) {
+      const double a0 = dir[s][0], a1 = dir[s][1], a2 = dir[s][2];
+      double t = o00 * a0 * a0;
+      t = t + (o01 + o10) * a0 * a1;
+      t = t + (o02 + o20) * a0 * a2;
+      t = t + o11 * a1 * a1;
+      t = t + (o12 + o21) * a1 * a2;
+      t = t + o22 * a2 * a2;
+      si[s] = t;
+      tau += fabs(t - si0);
+    }
+    tau /= NF;
+    tau = tau_pow(tau, P.weno_b);
+    double om0 = P.lam0 * (1.0 + tau / (P.weno_eps + si0));
+    double om[NF];
+    double wsum = om0;
+#pragma unroll
+    for (int s = 0; s < NF; ++s) {
+      om[s] = P.lams * (1.0 + tau / (P.weno_eps + si[s]));
+      wsum += om[s];
+    }
+    om0 /= wsum;
+#pragma unroll
+    for (int s = 0; s < NF; ++s) om[s] /= wsum;
+    double bl[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) bl[k] = om0 * p1[k];
+#pragma unroll
+    for (int s = 0; s < NF; ++s) {
+      bl[0] += om[s] * dir[s][0];
+      bl[1] += om[s] * dir[s][1];
+      bl[2] += om[s] * dir[s][2];
+    }
+    const bool chk = (v == 0 || v == 4);
+    double blo = 0.0, bhi = 0.0, viol = -1e300;
+    if (chk && P.mode == UCFVB_HYBRID) {
+      blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
+      bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
+    }
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol);
+    troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+  }
+}
+
+// ---- MUSCL (solver.cpp:189-221; reconstruct.cpp:30-86) ---------------------------------
+template <int K, int M, int NF, int NQ>
+__global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+  constexpr int Q = NF * NQ;
+  __shared__ double sval[Q][V5][33];
+  __shared__ int s_fail[32];
+  const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+  const int cnt = W.counters[kMuList];
+  const int32_t* list = W.lists + D.n;
+  for (int base = blockIdx.x * 32; base < cnt; base += gridDim.x * 32) {
+    const bool act = base + lane < cnt;
+    const int c = list[act ? base + lane : base];
+    const int op = D.opi[c];
+    const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+#pragma unroll 2
+    for (int m = 0; m < M; ++m) {
+      const double d = U[static_cast<size_t>(D.central[ao(c, m + 1, M + 1)]) * V5 + v] - u0;
+      l0 += D.pinv_lin[ao(op, 0 * M + m, 3 * M)] * d;
+      l1 += D.pinv_lin[ao(op, 1 * M + m, 3 * M)] * d;
+      l2 += D.pinv_lin[ao(op, 2 * M + m, 3 * M)] * d;
+    }
+    double lo = u0, hi = u0;
+#pragma unroll
+    for (int i = 0; i < NF; ++i) {
+      const double x = U[static_cast<size_t>(D.nbr[ao(c, i, NF)]) * V5 + v];
+      lo = smin(lo, x);
+      hi = smax(hi, x);
+    }
+    double th = 1.0;
+    const double e2 = D.eps2[c];
+    for (int q = 0; q < Q; ++q) {
+      const double uq = u0 + l0 * D.phi[ao(op, q * K + 0, Q * K)] + l1 * D.phi[ao(op, q * K + 1, Q * K)] +
+                        l2 * D.phi[ao(op, q * K + 2, Q * K)];
+      th = (P.limiter == UCFVB_BARTH_JESPERSEN) ? bj_update(th, u0, lo, hi, uq) : venkat_update(th, u0, lo, hi, uq, e2);
+    }
+    if (P.limiter == UCFVB_BARTH_JESPERSEN) th = smax(th, 0.0);
+    double a[K];
+    a[0] = th * l0;
+    a[1] = th * l1;
+    a[2] = th * l2;
+#pragma unroll
+    for (int k = 3; k < K; ++k) a[k] = 0.0;
+    const bool chk = (v == 0 || v == 4);
+    double blo = 0.0, bhi = 0.0, viol = -1e300;
+    if (chk && P.mode == UCFVB_HYBRID) {
+      blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
+      bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
+    }
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol);
+    troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+  }
+}
+
+// first-order everywhere (SchemeMode::First)
+template <int NF, int NQ>
+__global__ void k3_constant(Dev3 D, Work3 W, const double* __restrict__ U) {
+  constexpr int Q = NF * NQ;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D.n) return;
+  W.labels[c] = UCFVB_SCHEME_FIRST;
+  for (int q = 0; q < Q; ++q)
+#pragma unroll
+    for (int v = 0; v < V5; ++v) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = U[static_cast<size_t>(c) * V5 + v];
+}
+
+// ---- fluxes (solver.cpp:266-295) ----------------------------------------------------------
+template <int NQ>
+__global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= D.nF) return;
+  double tot[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  bool ok = true;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const double* UL = &W.fp[(static_cast<size_t>(f) * NQ + q) * 2 * V5];
+    double ul[5], ur[5], n[3], fl[5];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[V5 + v];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) n[d] = D.fnrm[(static_cast<size_t>(f) * NQ + q) * 3 + d];
+    ok = riemann3(P.hll, ul, ur, n, P.gamma, fl) && ok;
+    const double w = D.fwa[static_cast<size_t>(f) * NQ + q];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) tot[v] += w * fl[v];
+  }
+  if (!ok) atomicMin(&W.counters[kBadFace], f);
+#pragma unroll
+  for (int v = 0; v < V5; ++v) W.ff[static_cast<size_t>(f) * V5 + v] = tot[v];
+}
+
+// ---- gather + RK combination (solver.cpp:296-311, time_integrator.cpp:31-38) --------------
+// out = wa*ua + wb*ub + (wr*dt)*res, res = -acc*(1/vol); store_res keeps res (compute_residual tap / RK54)
+template <int NF>
+__global__ void __launch_bounds__(256) k3_gather_rk(Dev3 D, Work3 W, const double* __restrict__ ua,
+                                                    const double* __restrict__ ub, double* __restrict__ out,
+                                                    double* __restrict__ res_out, double wa, double wb, double wr,
+                                                    int combine) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= D.n) return;
+  double acc[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < NF; ++i) {
+    const int cf = D.cface[ao(c, i, NF)];
+    const double sgn = (cf & 1) ? -1.0 : 1.0;
+    const double* fl = &W.ff[static_cast<size_t>(cf >> 1) * V5];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) acc[v] += sgn * fl[v];
+  }
+  const double iv = D.inv_vol[c];
+  double r[V5];
+#pragma unroll
+  for (int v = 0; v < V5; ++v) r[v] = -acc[v] * iv;
+  if (res_out) {
+#pragma unroll
+    for (int v = 0; v < V5; ++v) res_out[static_cast<size_t>(c) * V5 + v] = r[v];
+  }
+  if (combine) {
+    const double wrdt = wr * W.dt[0];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) {
+      const size_t i = static_cast<size_t>(c) * V5 + v;
+      out[i] = wa * ua[i] + wb * ub[i] + wrdt * r[v];
+    }
+  }
+}
+
+// SSPRK(5,4) final combination (time_integrator.cpp:66-73)
+__global__ void k3_rk54_final(int64_t N, double* u, const double* ub, const double* uc, const double* rhs3,
+                              const double* ud, const double* rhs, const double* dtp) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= N) return;
+  const double dt = dtp[0];
+  const double c52 = 0.517231671970585, c53 = 0.096059710526147, a53 = 0.063692468666290;
+  const double c54 = 0.386708617503269, a54 = 0.226007483236906;
+  u[i] = c52 * ub[i] + c53 * uc[i] + a53 * dt * rhs3[i] + c54 * ud[i] + a54 * dt * rhs[i];
+}
+
+// ---- max_stable_dt (solver.cpp:103-111) ----------------------------------------------------
+__global__ void __launch_bounds__(256) k3_dt(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  double dt = 1e300;
+  if (c < D.n) {
+    const double* s = &U[static_cast<size_t>(c) * V5];
+    bool ok = s[0] > 0.0;
+    if (ok) {
+      const double u = s[1] / s[0], v = s[2] / s[0], w = s[3] / s[0];
+      const double p = (P.gamma - 1.0) * (s[4] - 0.5 * s[0] * (u * u + v * v + w * w));
+      ok = p > 0.0;
+      if (ok) {
+        const double speed = fabs(u) + fabs(v) + fabs(w) + sqrt(P.gamma * p / s[0]);
+        dt = D.h[c] / speed;
+      }
+    }
+    if (!ok) atomicMin(&W.counters[kBadCell], c);
+  }
+  for (int o = 16; o; o >>= 1) dt = smin(dt, __shfl_xor_sync(0xffffffffu, dt, o));
+  if ((threadIdx.x & 31) == 0) atomicMin(W.dtmin, static_cast<unsigned long long>(__double_as_longlong(dt)));
+}
+
+__global__ void k3_dt_init(Work3 W) { *W.dtmin = static_cast<unsigned long long>(__double_as_longlong(1e300)); }
+
+__global__ void k3_dt_finalize(Work3 W, double cfl, int advance_time) {
+  const double dt = cfl * __longlong_as_double(static_cast<long long>(*W.dtmin));
+  if (advance_time) *W.t += W.dt[0];  // previous step's dt
+  W.dt[0] = dt;
+}
+
+__global__ void k3_time_add(Work3 W) { *W.t += W.dt[0]; }
+
+// ---- dispatch ----------------------------------------------------------------------------------
+struct Kern3 {
+  void (*central)(Dev3, Phys3, Work3, const double*, int, int);
+  void (*spread)(Dev3, Work3, const double*);
+  void (*cwenoz)(Dev3, Phys3, Work3, const double*);
+  void (*muscl)(Dev3, Phys3, Work3, const double*);
+  void (*constant)(Dev3, Work3, const double*);
+  void (*flux)(Dev3, Phys3, Work3);
+  void (*gather)(Dev3, Work3, const double*, const double*, double*, double*, double, double, double, int);
+};
+
+template <int K, int M, int NF, int NQ>
+Kern3 kern3() {
+  return Kern3{k3_central<K, M, NF, NQ>, k3_spread<NF, NQ>, k3_cwenoz<K, M, NF, NQ>, k3_muscl<K, M, NF, NQ>,
+               k3_constant<NF, NQ>, k3_face_flux<NQ>, k3_gather_rk<NF>};
+}
+
+bool pick3(int K, int M, int NF, int NQ, Kern3& k) {
+#define PICK3(k_, m_, nf_, nq_) \
+  if (K == k_ && M == m_ && NF == nf_ && NQ == nq_) return k = kern3<k_, m_, nf_, nq_>(), true;
+  PICK3(3, 6, 6, 1)
+  PICK3(9, 18, 6, 4)
+  PICK3(19, 38, 6, 4)
+  PICK3(3, 6, 4, 3)
+  PICK3(9, 18, 4, 6)
+  PICK3(19, 38, 4, 6)
+#undef PICK3
+  return false;
+}
+
+template <typename T>
+T* dalloc(size_t count, std::vector<void*>& owned) {
+  void* p = nullptr;
+  CK3(cudaMalloc(&p, std::max<size_t>(1, count) * sizeof(T)));
+  owned.push_back(p);
+  return static_cast<T*>(p);
+}
+
+// 32-row AoSoA of a row-major [rows][E] host array
+template <typename T>
+std::vector<T> to_aosoa(const T* src, int64_t rows, int E, int n_threads) {
+  const int64_t nch = (rows + 31) / 32;
+  std::vector<T> out(static_cast<size_t>(nch) * 32 * E, T{});
+  parallel_for(rows, n_threads, [&](int64_t a0, int64_t a1) {
+    for (int64_t r = a0; r < a1; ++r)
+      for (int e = 0; e < E; ++e) out[((r >> 5) * E + e) * 32 + (r & 31)] = src[r * E + e];
+  });
+  return out;
+}
+
+}  // namespace
+
+struct GpuSolver3::Impl {
+  int device = 0, n = 0, nF = 0, K = 0, M = 0, NF = 0, NQ = 0, Q = 0;
+  ucfvb_options o{};
+  Kern3 kern{};
+  Dev3 D{};
+  Phys3 P{};
+  Work3 W{};
+  cudaStream_t st = nullptr;
+  std::vector<void*> owned;
+  double *U = nullptr, *ua = nullptr, *ub = nullptr, *uc = nullptr, *ud = nullptr, *rhs = nullptr, *rhs3 = nullptr;
+  uint8_t* step_labels = nullptr;
+  int32_t* h_counters = nullptr;
+  double* h_dt = nullptr;
+  int64_t launches = 0, graph_launches = 0;
+  int central_grid = 0;
+  cudaGraphExec_t step_graph = nullptr;
+  int graph_rk = -1;
+
+  void launch_stage(const double* Us, bool first, double* out, const double* wa_src, const double* wb_src,
+                    double wa, double wb, double wr, double* res, int combine) {
+    const int mode = o.mode;
+    const bool nad = mode == UCFVB_HYBRID;
+    const int nblk = (n + 255) / 256;
+    if (mode == UCFVB_LINEAR || mode == UCFVB_CWENOZ || mode == UCFVB_HYBRID) {
+      kern.central<<<central_grid, 160, 0, st>>>(D, P, W, Us, mode != UCFVB_CWENOZ ? 1 : 0, nad ? 1 : 0);
+      ++launches;
+    }
+    if (nad) {
+      kern.spread<<<nblk, 256, 0, st>>>(D, W, Us);
+      ++launches;
+    } else if (mode == UCFVB_CWENOZ || mode == UCFVB_MUSCL) {
+      k3_fill_list<<<nblk, 256, 0, st>>>(n, mode == UCFVB_CWENOZ ? kCwList : kMuList,
+                                         mode == UCFVB_CWENOZ ? UCFVB_SCHEME_CWENOZ : UCFVB_SCHEME_MUSCL, W);
+      ++launches;
+    } else if (mode == UCFVB_FIRST) {
+      kern.constant<<<nblk, 256, 0, st>>>(D, W, Us);
+      ++launches;
+    } else {
+      CK3(cudaMemsetAsync(W.labels, UCFVB_SCHEME_LINEAR, n, st));
+    }
+    if (mode == UCFVB_HYBRID || mode == UCFVB_CWENOZ) {
+      kern.cwenoz<<<central_grid, 160, 0, st>>>(D, P, W, Us);
+      ++launches;
+    }
+    if (mode == UCFVB_HYBRID || mode == UCFVB_MUSCL) {
+      kern.muscl<<<central_grid, 160, 0, st>>>(D, P, W, Us);
+      ++launches;
+    }
+    if (first) CK3(cudaMemcpyAsync(step_labels, W.labels, n, cudaMemcpyDeviceToDevice, st));
+    kern.flux<<<(nF + 127) / 128, 128, 0, st>>>(D, P, W);
+    kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine);
+    launches += 2;
+  }
+
+  // one RK step on the device state U with the device dt W.dt
+  void step(int rk) {
+    if (rk == UCFVB_RK3) {
+      launch_stage(U, true, ua, U, U, 1.0, 0.0, 1.0, nullptr, 1);
+      launch_stage(ua, false, ub, U, ua, 0.75, 0.25, 0.25, nullptr, 1);
+      launch_stage(ub, false, U, U, ub, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, nullptr, 1);
+      return;
+    }
+    const double a10 = 0.391752226571890;
+    const double b20 = 0.444370493651235, b21 = 0.555629506348765, a21 = 0.368410593050371;
+    const double b30 = 0.620101851488403, b32 = 0.379898148511597, a32 = 0.251891774271694;
+    const double b40 = 0.178079954393132, b43 = 0.821920045606868, a43 = 0.544974750228521;
+    launch_stage(U, true, ua, U, U, 1.0, 0.0, a10, nullptr, 1);
+    launch_stage(ua, false, ub, U, ua, b20, b21, a21, nullptr, 1);
+    launch_stage(ub, false, uc, U, ub, b30, b32, a32, nullptr, 1);
+    launch_stage(uc, false, ud, U, uc, b40, b43, a43, rhs3, 1);
+    launch_stage(ud, false, nullptr, nullptr, nullptr, 0, 0, 0, rhs, 0);
+    const int64_t N = static_cast<int64_t>(n) * V5;
+    k3_rk54_final<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(N, U, ub, uc, rhs3, ud, rhs, W.dt);
+    ++launches;
+  }
+
+  void dt_kernels(bool advance_time) {
+    k3_dt_init<<<1, 1, 0, st>>>(W);
+    k3_dt<<<(n + 255) / 256, 256, 0, st>>>(D, P, W, U);
+    k3_dt_finalize<<<1, 1, 0, st>>>(W, o.cfl, advance_time ? 1 : 0);
+    launches += 3;
+  }
+
+  void reset_errors() {
+    const int32_t init[2] = {0x7fffffff, 0x7fffffff};
+    CK3(cudaMemcpyAsync(W.counters + 2, init, sizeof init, cudaMemcpyHostToDevice, st));
+  }
+
+  void check_errors() {
+    CK3(cudaMemcpyAsync(h_counters, W.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CK3(cudaStreamSynchronize(st));
+    CK3(cudaGetLastError());
+    if (h_counters[kBadFace] != 0x7fffffff)
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state at face " + std::to_string(h_counters[kBadFace]));
+    if (h_counters[kBadCell] != 0x7fffffff)
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state in cell " + std::to_string(h_counters[kBadCell]));
+  }
+};
+
+GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device)
+    : p_(new Impl) {
+  Impl& I = *p_;
+  try {
+    if (m.n_cells != s.n_cells || m.nf != s.nf || m.nq != s.nq || s.MD != MD3)
+      throw ApiError(UCFVB_INVALID, "solver3d: stencils do not match the mesh");
+    if (o.mode < UCFVB_LINEAR || o.mode > UCFVB_FIRST) throw ApiError(UCFVB_INVALID, "solver3d: unknown mode");
+    if (!o.detect_every_stage && o.mode == UCFVB_HYBRID)
+      throw ApiError(UCFVB_UNSUPPORTED, "solver3d: frozen detection (detect_every_stage = 0) is 2D-only");
+    if (!(o.lambda1p > 1.0)) throw ApiError(UCFVB_INVALID, "cwenoz: central linear weight lambda1' must exceed 1");
+    if (o.margins.alpha_m < 0.0 || o.margins.beta_m < 0.0)
+      throw ApiError(UCFVB_INVALID, "NAD margins: alpha_m and beta_m must be non-negative");
+    if (o.margins.beta_w > 0.0 && (o.margins.beta_w > o.margins.beta_m || o.margins.alpha_w > o.margins.alpha_m))
+      throw ApiError(UCFVB_INVALID, "NAD margins: delta_w <= delta_m requires beta_w <= beta_m and alpha_w <= alpha_m");
+    if (o.margins.kappa < 0.0) throw ApiError(UCFVB_INVALID, "NAD margins: kappa must be >= 0");
+    I.o = o;
+    I.n = m.n_cells, I.nF = m.n_faces, I.K = s.K, I.M = s.M, I.NF = m.nf, I.NQ = m.nq, I.Q = s.Q;
+    if (!pick3(I.K, I.M, I.NF, I.NQ, I.kern))
+      throw ApiError(UCFVB_UNSUPPORTED, "solver3d: no kernel instance for K=" + std::to_string(I.K) +
+                                            " M=" + std::to_string(I.M) + " nf=" + std::to_string(I.NF) +
+                                            " nq=" + std::to_string(I.NQ));
+    I.device = device;
+    CK3(cudaSetDevice(device));
+    CK3(cudaStreamCreateWithFlags(&I.st, cudaStreamNonBlocking));
+    const int n = I.n, K = I.K, M = I.M, NF = I.NF, NQ = I.NQ, Q = I.Q, nops = s.n_ops;
+    const int nth = 0;
+    auto up = [&](auto* dst, const auto& host) {
+      CK3(cudaMemcpy(dst, host.data(), host.size() * sizeof(host[0]), cudaMemcpyHostToDevice));
+    };
+    auto upload_ao = [&](auto ptr, int64_t rows, int E) {
+      using T = std::remove_const_t<std::remove_pointer_t<decltype(ptr)>>;
+      auto h = to_aosoa<T>(ptr, rows, E, nth);
+      T* d = dalloc<T>(h.size(), I.owned);
+      up(d, h);
+      return static_cast<const T*>(d);
+    };
+    Dev3& D = I.D;
+    D.n = n, D.nF = I.nF, D.n_ops = nops;
+    D.central = upload_ao(s.central, n, M + 1);
+    D.nbr = upload_ao(m.cell_nbr, n, NF);
+    D.slot = upload_ao(s.qp_slot, n, Q);
+    {
+      std::vector<int32_t> cf(static_cast<size_t>(n) * NF);
+      for (size_t i = 0; i < cf.size(); ++i) cf[i] = (m.cell_faces[i] << 1) | (m.cell_side[i] ? 1 : 0);
+      D.cface = upload_ao(cf.data(), n, NF);
+    }
+    {
+      int32_t* d = dalloc<int32_t>(n, I.owned);
+      CK3(cudaMemcpy(d, s.op_index, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+      D.opi = d;
+    }
+    std::vector<double> thr(n), eps2(n), iv(n), hh(n);
+    for (int c = 0; c < n; ++c) {
+      thr[c] = std::pow(o.margins.kappa * m.cell_h[c], o.margins.deact_n);  // deactivate_smooth (detector.cpp:34)
+      eps2[c] = std::pow(o.venkat_kappa * m.cell_h[c], 3);                   // solver.cpp:203
+      iv[c] = 1.0 / m.cell_volume[c];
+      hh[c] = m.cell_h[c];
+    }
+    auto upd = [&](const std::vector<double>& h) {
+      double* d = dalloc<double>(h.size(), I.owned);
+      up(d, h);
+      return static_cast<const double*>(d);
+    };
+    D.thr = upd(thr), D.eps2 = upd(eps2), D.inv_vol = upd(iv), D.h = upd(hh);
+    {
+      // pinv [K][M] -> [M][K] (m-major), then AoSoA
+      std::vector<double> t(static_cast<size_t>(nops) * K * M);
+      for (int64_t r = 0; r < nops; ++r)
+        for (int k = 0; k < K; ++k)
+          for (int mm = 0; mm < M; ++mm) t[(r * M + mm) * K + k] = s.pinv[(r * K + k) * M + mm];
+      D.pinv = upload_ao(t.data(), nops, M * K);
+    }
+    D.pinv_lin = upload_ao(s.pinv_lin, nops, 3 * M);
+    D.dirm = upload_ao(s.dir_members, nops, NF * MD3);
+    D.pinv_dir = upload_ao(s.pinv_dir, nops, NF * 3 * MD3);
+    D.oi = upload_ao(s.oi, nops, K * K);
+    D.phi = upload_ao(s.phi, nops, Q * K);
+    {
+      double* fn = dalloc<double>(static_cast<size_t>(I.nF) * NQ * 3, I.owned);
+      double* fw = dalloc<double>(static_cast<size_t>(I.nF) * NQ, I.owned);
+      CK3(cudaMemcpy(fn, m.face_normal, sizeof(double) * I.nF * NQ * 3, cudaMemcpyHostToDevice));
+      CK3(cudaMemcpy(fw, m.face_wa, sizeof(double) * I.nF * NQ, cudaMemcpyHostToDevice));
+      D.fnrm = fn, D.fwa = fw;
+    }
+    Phys3& P = I.P;
+    P.gamma = o.gamma, P.cfl = o.cfl, P.lambda1p = o.lambda1p, P.weno_eps = o.weno_eps, P.weno_b = o.weno_b;
+    P.lam0 = 1.0 - 1.0 / o.lambda1p;            // reconstruct.cpp:113
+    P.lams = (1.0 - P.lam0) / (I.NF + 1 - 1);   // reconstruct.cpp:114
+    P.mg = MarginParams{o.margins.alpha_m, o.margins.beta_m, o.margins.alpha_w, o.margins.beta_w, o.margins.kappa,
+                        o.margins.deact_n};
+    P.mode = o.mode, P.limiter = o.limiter, P.hll = o.riemann == UCFVB_HLL ? 1 : 0, P.detect = 1;
+    Work3& W = I.W;
+    const int64_t nch = (n + 31) / 32;
+    W.fp = dalloc<double>(static_cast<size_t>(I.nF) * NQ * 2 * V5, I.owned);
+    W.ff = dalloc<double>(static_cast<size_t>(I.nF) * V5, I.owned);
+    W.dofs = dalloc<double>(static_cast<size_t>(nch) * 32 * K * V5, I.owned);
+    W.bounds = dalloc<double>(static_cast<size_t>(nch) * 32 * 4, I.owned);
+    W.raw = dalloc<uint8_t>(n, I.owned);
+    W.labels = dalloc<uint8_t>(n, I.owned);
+    W.lists = dalloc<int32_t>(static_cast<size_t>(2) * n, I.owned);
+    W.counters = dalloc<int32_t>(4, I.owned);
+    W.dtmin = dalloc<unsigned long long>(1, I.owned);
+    W.dt = dalloc<double>(1, I.owned);
+    W.t = dalloc<double>(1, I.owned);
+    W.ties = dalloc<unsigned long long>(1, I.owned);
+    CK3(cudaMemset(W.fp, 0, sizeof(double) * static_cast<size_t>(I.nF) * NQ * 2 * V5));
+    CK3(cudaMemset(W.labels, 0, n));
+    CK3(cudaMemset(W.counters, 0, 4 * sizeof(int32_t)));
+    CK3(cudaMemset(W.ties, 0, sizeof(unsigned long long)));
+    I.step_labels = dalloc<uint8_t>(n, I.owned);
+    CK3(cudaMemset(I.step_labels, 0, n));
+    const size_t sz = static_cast<size_t>(n) * V5;
+    I.U = dalloc<double>(sz, I.owned);
+    I.ua = dalloc<double>(sz, I.owned);
+    I.ub = dalloc<double>(sz, I.owned);
+    I.uc = dalloc<double>(sz, I.owned);
+    I.ud = dalloc<double>(sz, I.owned);
+    I.rhs = dalloc<double>(sz, I.owned);
+    I.rhs3 = dalloc<double>(sz, I.owned);
+    CK3(cudaMemset(I.U, 0, sz * sizeof(double)));
+    CK3(cudaMallocHost(&I.h_counters, 4 * sizeof(int32_t)));
+    CK3(cudaMallocHost(&I.h_dt, 2 * sizeof(double)));
+    int sms = 148, per = 1;
+    CK3(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    CK3(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, I.kern.central, 160, 0));
+    I.central_grid = static_cast<int>(std::min<int64_t>(nch, static_cast<int64_t>(sms) * std::max(1, per)));
+    I.central_grid = std::max(1, I.central_grid);
+    I.reset_errors();
+    CK3(cudaStreamSynchronize(I.st));
+  } catch (...) {
+    for (void* q : I.owned) cudaFree(q);
+    if (I.h_counters) cudaFreeHost(I.h_counters);
+    if (I.h_dt) cudaFreeHost(I.h_dt);
+    if (I.st) cudaStreamDestroy(I.st);
+    delete p_;
+    throw;
+  }
+}
+
+GpuSolver3::~GpuSolver3() {
+  Impl& I = *p_;
+  cudaSetDevice(I.device);
+  if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
+  if (I.st) cudaStreamSynchronize(I.st);
+  for (void* q : I.owned) cudaFree(q);
+  if (I.h_counters) cudaFreeHost(I.h_counters);
+  if (I.h_dt) cudaFreeHost(I.h_dt);
+  if (I.st) cudaStreamDestroy(I.st);
+  delete p_;
+}
+
+void GpuSolver3::set_state(const double* u) {
+  CK3(cudaSetDevice(p_->device));
+  CK3(cudaMemcpyAsync(p_->U, u, sizeof(double) * p_->n * V5, cudaMemcpyHostToDevice, p_->st));
+  CK3(cudaStreamSynchronize(p_->st));
+}
+void GpuSolver3::get_state(double* u) {
+  CK3(cudaSetDevice(p_->device));
+  CK3(cudaMemcpyAsync(u, p_->U, sizeof(double) * p_->n * V5, cudaMemcpyDeviceToHost, p_->st));
+  CK3(cudaStreamSynchronize(p_->st));
+}
+
+double GpuSolver3::max_stable_dt() {
+  Impl& I = *p_;
+  CK3(cudaSetDevice(I.device));
+  I.reset_errors();
+  I.dt_kernels(false);
+  CK3(cudaMemcpyAsync(I.h_dt, I.W.dt, sizeof(double), cudaMemcpyDeviceToHost, I.st));
+  I.check_errors();
+  return I.h_dt[0];
+}
+
+void GpuSolver3::advance(double dt, double t, int rk) {
+  Impl& I = *p_;
+  (void)t;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance: unknown integrator");
+  CK3(cudaSetDevice(I.device));
+  I.reset_errors();
+  I.h_dt[1] = dt;
+  CK3(cudaMemcpyAsync(I.W.dt, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
+  I.step(rk);
+  I.check_errors();
+}
+
+double GpuSolver3::run_steps(int n_steps, double t0, int rk) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "run_steps: unknown integrator");
+  CK3(cudaSetDevice(I.device));
+  I.reset_errors();
+  I.h_dt[1] = t0;
+  CK3(cudaMemcpyAsync(I.W.t, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
+  if (!I.step_graph || I.graph_rk != rk) {
+    if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
+    I.step_graph = nullptr;
+    cudaGraph_t g = nullptr;
+    const int64_t before = I.launches;
+    CK3(cudaStreamBeginCapture(I.st, cudaStreamCaptureModeThreadLocal));
+    I.dt_kernels(false);
+    I.step(rk);
+    k3_time_add<<<1, 1, 0, I.st>>>(I.W);
+    ++I.launches;
+    CK3(cudaStreamEndCapture(I.st, &g));
+    CK3(cudaGraphInstantiate(&I.step_graph, g, 0));
+    CK3(cudaGraphDestroy(g));
+    I.graph_launches = I.launches - before;
+    I.launches = before;
+    I.graph_rk = rk;
+  }
+  for (int i = 0; i < n_steps; ++i) {
+    CK3(cudaGraphLaunch(I.step_graph, I.st));
+    I.launches += I.graph_launches;
+  }
+  CK3(cudaMemcpyAsync(I.h_dt, I.W.t, sizeof(double), cudaMemcpyDeviceToHost, I.st));
+  I.check_errors();
+  return I.h_dt[0];
+}
+
+void GpuSolver3::compute_residual(const double* u, double t, double* out) {
+  Impl& I = *p_;
+  (void)t;
+  CK3(cudaSetDevice(I.device));
+  I.reset_errors();
+  CK3(cudaMemcpyAsync(I.ua, u, sizeof(double) * I.n * V5, cudaMemcpyHostToDevice, I.st));
+  I.launch_stage(I.ua, true, nullptr, nullptr, nullptr, 0, 0, 0, I.rhs, 0);
+  CK3(cudaMemcpyAsync(out, I.rhs, sizeof(double) * I.n * V5, cudaMemcpyDeviceToHost, I.st));
+  I.check_errors();
+}
+
+void GpuSolver3::get_labels(int which, uint8_t* out) {
+  CK3(cudaSetDevice(p_->device));
+  CK3(cudaMemcpyAsync(out, which ? p_->step_labels : p_->W.labels, p_->n, cudaMemcpyDeviceToHost, p_->st));
+  CK3(cudaStreamSynchronize(p_->st));
+}
+
+void GpuSolver3::get_face_values(double* out) {
+  CK3(cudaSetDevice(p_->device));
+  CK3(cudaMemcpyAsync(out, p_->W.fp, sizeof(double) * static_cast<size_t>(p_->nF) * p_->NQ * 2 * V5,
+                      cudaMemcpyDeviceToHost, p_->st));
+  CK3(cudaStreamSynchronize(p_->st));
+}
+
+void GpuSolver3::census(int64_t out[4]) {
+  std::vector<uint8_t> l(p_->n);
+  get_labels(1, l.data());
+  for (int i = 0; i < 4; ++i) out[i] = 0;
+  for (uint8_t x : l) ++out[x & 3];
+}
+
+int64_t GpuSolver3::nad_ties() {
+  unsigned long long t = 0;
+  CK3(cudaSetDevice(p_->device));
+  CK3(cudaMemcpyAsync(&t, p_->W.ties, sizeof t, cudaMemcpyDeviceToHost, p_->st));
+  CK3(cudaStreamSynchronize(p_->st));
+  return static_cast<int64_t>(t);
+}
+
+int64_t GpuSolver3::launches() const { return p_->launches; }
+void* GpuSolver3::stream() const { return p_->st; }
+
+}  // namespace ucfvb

@@ -1,0 +1,38 @@
+// 3D device solver (BASELINE configs 4-5): the stage pass of solver.cu for
+// five conserved variables on periodic hexahedral / tetrahedral meshes.
+#pragma once
+
+#include <cstdint>
+
+#include "ucfvb.h"
+#include "ucfvb3.h"
+
+namespace ucfvb {
+
+class GpuSolver3 {
+ public:
+  GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device);
+  ~GpuSolver3();
+  GpuSolver3(const GpuSolver3&) = delete;
+  GpuSolver3& operator=(const GpuSolver3&) = delete;
+
+  void set_state(const double* u);
+  void get_state(double* u);
+  double max_stable_dt();
+  void advance(double dt, double t, int rk);
+  double run_steps(int n_steps, double t0, int rk);
+  void compute_residual(const double* u, double t, double* out);
+  void get_labels(int which, uint8_t* out);
+  void get_face_values(double* out);
+  void census(int64_t out[4]);
+  int64_t nad_ties();
+  int64_t launches() const;
+  void* stream() const;
+
+  struct Impl;
+
+ private:
+  Impl* p_;
+};
+
+}  // namespace ucfvb

@@ -50,6 +50,19 @@ CONFIGS = {
 }
 SEED = 1
 
+# 3D configurations (the reference is 2D only)
+CONFIGS3 = {
+    "4": dict(n=128, kind=0, jitter=0.05, order=2, ic=0, params=[0.1], mode="hybrid", classes=False,
+              desc="BASELINE config 4: periodic [0,2pi]^3, 128^3 hexahedra (+-5% jitter), p=2, Taylor-Green M=0.1, "
+                   "hybrid"),
+    "4c": dict(n=128, kind=0, jitter=0.05, order=2, ic=0, params=[0.1], mode="cwenoz", classes=False,
+               desc="BASELINE config 4, forced all-CWENOZ: periodic [0,2pi]^3, 128^3 hexahedra (+-5% jitter), p=2, "
+                    "Taylor-Green M=0.1"),
+    "5": dict(n=128, kind=1, jitter=0.0, order=3, ic=1, params=[0.6, 4.0, 8], mode="hybrid", classes=True,
+              desc="BASELINE config 5: periodic [0,2pi]^3, 128^3 cubes x 6 tetrahedra, p=3, random-phase solenoidal "
+                   "field E(k)~k^4 exp(-2(k/4)^2) (|k|<=8), rms Mach 0.6, hybrid"),
+}
+
 
 def env_rank():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
@@ -140,6 +153,26 @@ def kernel_bytes(K, NQ, NF, MM, MD):
     spread = 1 + 4 * NF + 1 + 1
     return dict(central=int(central), spread=spread, cwenoz=int(cwenoz), muscl=int(muscl),
                 flux=int(flux + gather))
+
+
+def kernel_bytes3(K, M, NF, NQ, MD, per_cell_ops):
+    """Algorithmic HBM bytes per cell of each 3D kernel: own
+    U (40 B), index arrays, operator rows (per-cell rows only; lattice-class
+    rows are a few KB in total and live in L1/L2), face values (40 B per
+    point) and residual terms; stencil gathers of U counted as L2 hits."""
+    Q = NF * NQ
+    ops = 1 if per_cell_ops else 0
+    central = (40 + 4 + 8 + 4 * NF + 4 * (M + 1) + ops * 8 * M * K + ops * 8 * Q * K + 4 * Q
+               + 40 * Q + 40 * K + 32 + 1)
+    spread = 1 + 4 * NF + 1 + 4
+    cwenoz = (4 + 40 + 4 + 4 * (M + 1) + ops * (4 * NF * MD + 24 * NF * MD + 8 * K * K + 8 * Q * K)
+              + 40 * K + 4 * Q + 32 + 40 * Q + 1)
+    muscl = 4 + 40 + 4 + 4 * (M + 1) + ops * (24 * M + 24 * Q) + 4 * NF + 8 + 4 * Q + 32 + 40 * Q + 1
+    faces = NF / 2.0
+    flux = faces * (2 * NQ * 40 + NQ * 32 + 40)
+    gather = 4 * NF + 40 * NF + 8 + 3 * 40
+    return dict(central=int(central), spread=spread, cwenoz=int(cwenoz), muscl=int(muscl), flux=int(flux),
+                gather=int(gather))
 
 
 def measured_peak_hbm():
@@ -429,18 +462,174 @@ def run_b200_arm(args):
         dist.destroy_process_group()
 
 
+def build_case3(cfg, n_threads=0, n=None):
+    from paper_2510_25906_b200.solver3d import Mesh3, Stencils3
+    c = CONFIGS3[cfg]
+    t0 = time.perf_counter()
+    mesh = Mesh3(n or c["n"], kind=c["kind"], jitter=c["jitter"], seed=SEED, order=c["order"], n_threads=n_threads)
+    st = Stencils3(mesh, c["order"], lattice_classes=c["classes"], n_threads=n_threads)
+    deg = 1 if c["ic"] == 1 else max(2 * c["order"], 2)
+    u0 = mesh.project_initial(c["ic"], c["params"], seed=SEED, degree=deg, n_threads=n_threads)
+    return mesh, st, u0, time.perf_counter() - t0
+
+
+def port3_rate(cfg, budget_s):
+    """The 3D oracle restatement (oracle/ucfv3_port.c, 1 thread) on a bounded
+    sample: the same config on a 12^3-cube mesh, RK3 steps until `budget_s`."""
+    from oracle.port3 import Port3Solver
+    from paper_2510_25906_b200 import _abi as A
+    c = CONFIGS3[cfg]
+    mesh, st, u0, _ = build_case3(cfg, n=12)
+    P = Port3Solver(mesh, st, A.options_from_dict(order=c["order"], mode=c["mode"], cfl=0.5))
+    P.state = u0.copy()
+    done, t0 = 0, time.perf_counter()
+    while done < 2 or (time.perf_counter() - t0 < budget_s and done < 200):
+        P.advance(P.max_stable_dt(), rk=A.RK3)
+        done += 1
+    dt = time.perf_counter() - t0
+    return mesh.n_cells * 3 * done / dt, done, mesh.n_cells
+
+
+def run_arm_3d(args):
+    """3D configurations 4 / 4c / 5 on one GPU (the 3D path has no domain
+    decomposition yet)."""
+    import ctypes as C
+
+    import torch
+    rank, world, local = env_rank()
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"impl": args.impl, "unavailable": "3D configs run on one GPU (no 3D decomposition)"}))
+        return
+    cfg = args.config
+    c = CONFIGS3[cfg]
+    from paper_2510_25906_b200 import _abi as A
+    if args.impl == "reference":
+        rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "20")))
+        sample = (f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle restatement "
+                  f"oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has {os.cpu_count()} cores")
+        print(json.dumps({"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 1, "steps": done, "warmup": 0,
+                          "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "dtype": "f64", "data": "synthetic", "impl": "reference",
+                          "config": {"workload": c["desc"]},
+                          "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+                          "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+    from paper_2510_25906_b200 import solver3d as S3
+    torch.cuda.set_device(local)
+    threads = os.cpu_count() or 1
+    mesh, st, u0, setup_s = build_case3(cfg, n_threads=threads)
+    opts = A.options_from_dict(order=c["order"], mode=c["mode"], cfl=0.5)
+    solver = S3.Solver3(mesh, opts, st, device=local)
+    n = mesh.n_cells
+    stream = torch.cuda.ExternalStream(solver.stream(), device=local)
+    solver.state = u0
+    solver.run_steps(args.warmup)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        solver.run_steps(args.steps)
+        ev1.record(stream)
+        ev1.synchronize()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    launches = solver.launch_count()
+    value = n * 3 * args.steps / (ms * 1e-3)
+    census = np.array(solver.census(), dtype=float)
+    mix = census / census.sum()
+    ties = solver.nad_ties()
+    # per-kernel-group durations (events between groups, un-graphed stages)
+    solver.set_phase_timing(True)
+    p0 = solver.phase_times().copy()
+    nps = 3
+    solver.run_steps(nps)
+    phases = (solver.phase_times() - p0) / (3 * nps)
+    solver.set_phase_timing(False)
+    # e2e: pinned host state, H2D + step + D2H every step
+    host = [torch.from_numpy(np.ascontiguousarray(u0)).pin_memory(),
+            torch.empty((n, 5), dtype=torch.float64).pin_memory()]
+    L = S3.lib()
+    hp = [C.cast(h.data_ptr(), C.POINTER(C.c_double)) for h in host]
+    tt = C.c_double()
+
+    def e2e_step(i):
+        rc = L.ucfvb3_set_state(solver._h, hp[i & 1])
+        rc |= L.ucfvb3_run_steps(solver._h, 1, 0.0, A.RK3, C.byref(tt))
+        rc |= L.ucfvb3_get_state(solver._h, hp[(i + 1) & 1])
+        if rc:
+            raise RuntimeError(L.ucfvb3_last_error(solver._h).decode())
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    host[0].copy_(torch.from_numpy(np.ascontiguousarray(u0)))
+    e2e_steps = max(3, args.steps // 4)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(stream)
+    for i in range(e2e_steps):
+        e2e_step(i)
+    e1.record(stream)
+    e1.synchronize()
+    e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - w0))
+    e2e_value = n * 3 * e2e_steps / (e2e_ms * 1e-3)
+    kb = kernel_bytes3(st.K, st.M, mesh.nf, mesh.nq, st.MD, not c["classes"])
+    names = ["central (reconstruct)", "spread+compaction (detect)", "cwenoz+muscl (weights)", "flux", "gather+RK"]
+    if c["mode"] == "cwenoz":
+        wbytes = kb["cwenoz"]
+    else:
+        wbytes = kb["cwenoz"] * mix[1] + kb["muscl"] * mix[2]
+    phase_bytes = [kb["central"] * n, kb["spread"] * n, wbytes * n, kb["flux"] * n, kb["gather"] * n]
+    dom = int(np.argmax(phases))
+    peak, peak_kind = measured_peak_hbm()
+    achieved = phase_bytes[dom] / phases[dom] / 1e9
+    stage_achieved = sum(phase_bytes) / phases.sum() / 1e9
+    cpu_baseline = None
+    if not args.no_cpu_baseline:
+        rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "12")))
+        cpu_baseline = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
+                        "sample": f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle "
+                                  f"restatement oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has "
+                                  f"{os.cpu_count()} cores"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": c["desc"], "cells": n, "order": c["order"], "K": st.K, "M": st.M, "nf": mesh.nf,
+                   "nq": mesh.nq, "integrator": "SSP-RK3 (3 stages/step)", "mode": c["mode"],
+                   "operator_rows": "lattice classes (6 shared rows)" if c["classes"] else "per cell",
+                   "parallelism": "single",
+                   "l2": "inputs larger than L2 (face values alone %.0f MB)" % (mesh.n_faces * mesh.nq * 80 / 1e6),
+                   "class_mix_last_step": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
+                                           "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
+                   "nad_ties": int(ties), "setup_s": round(setup_s, 2)},
+        "clocks": clk.summary(),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 40)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": names[dom], "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                     "bytes_per_cell": {k: int(v) for k, v in kb.items()},
+                     "stage_achieved": stage_achieved, "stage_frac": stage_achieved / peak,
+                     "phase_us": [round(1e6 * p, 2) for p in phases]},
+        "cpu_baseline": cpu_baseline,
+    }
+    print(json.dumps(line))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="2", choices=sorted(CONFIGS) + sorted(CONFIGS3))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.config in CONFIGS3:
+        run_arm_3d(args)
+    elif args.impl == "reference":
         run_reference_arm(args)
     else:
         run_b200_arm(args)

@@ -152,6 +152,11 @@ int32_t ucfvb3_get_face_values(ucfvb3_solver* h, double* out);
 int32_t ucfvb3_get_census(ucfvb3_solver* h, int64_t out[4]);
 /* NAD threshold near-ties of the last detection stage */
 int32_t ucfvb3_get_nad_ties(ucfvb3_solver* h, int64_t* out);
+/* PhaseTimes (solver.hpp:45-50) of the device pass: events between kernel
+ * groups of un-graphed stages while enabled; seconds accumulated per group
+ * {reconstruct (central), detect (spread), weights (CWENOZ+MUSCL), flux, gather+RK} */
+int32_t ucfvb3_set_phase_timing(ucfvb3_solver* h, int32_t on);
+int32_t ucfvb3_get_phase_times(ucfvb3_solver* h, double out[5]);
 int64_t ucfvb3_launch_count(const ucfvb3_solver* h);
 /* stream the solver launches on (cudaStream_t as void*) */
 void* ucfvb3_stream(const ucfvb3_solver* h);

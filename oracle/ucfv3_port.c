@@ -24,6 +24,16 @@
  *   SSP-RK3 / SSPRK(5,4) time_integrator.cpp:31-74
  * The 2D restatement of the same functions (oracle/ucfv_port.c) is pinned
  * bit-exactly to the compiled reference.
+ *
+ * Arithmetic: the 2D path keeps the reference's unfused x86-64 arithmetic
+ * (no FMA) for bit parity. The 3D discretisation has no reference
+ * arithmetic to match, so its least-squares solves and polynomial
+ * evaluations (the K x M and Q x K contractions) accumulate with fused
+ * multiply-adds, acc = fma(a, b, acc) in the same term order -- one rounding
+ * per term and half the fp64 instructions on the device; every other
+ * operation is unfused as in 2D. C's fma() and CUDA's __fma_rn are both the
+ * correctly rounded fused operation, so the device matches this restatement
+ * bit for bit.
  */
 #include <math.h>
 #include <stdint.h>
@@ -162,7 +172,7 @@ static void solve_dofs(const port3* P, int c, const double* u, double* dofs) {
     for (int m = 0; m < M; ++m) {
       const double* um = &u[(int64_t)st[m + 1] * NV];
       const double w = row[m];
-      for (int v = 0; v < NV; ++v) s[v] += w * (um[v] - u0[v]);
+      for (int v = 0; v < NV; ++v) s[v] = fma(w, um[v] - u0[v], s[v]);
     }
     for (int v = 0; v < NV; ++v) dofs[k * NV + v] = s[v];
   }
@@ -179,7 +189,7 @@ static void evaluate_cell(port3* P, const double* u, int c, const double* dofs) 
     for (int v = 0; v < NV; ++v) out[v] = u0[v];
     for (int k = 0; k < K; ++k) {
       const double p = phi[q * K + k];
-      for (int v = 0; v < NV; ++v) out[v] += dofs[k * NV + v] * p;
+      for (int v = 0; v < NV; ++v) out[v] = fma(dofs[k * NV + v], p, out[v]);
     }
     memcpy(slot_ptr(P, slots[q]), out, sizeof out);
   }
@@ -345,7 +355,7 @@ static int apply_troubled(port3* P, const double* u) {
         for (int k = 0; k < 3; ++k)
           for (int v = 0; v < NV; ++v) {
             double acc = 0.0;
-            for (int m = 0; m < MD; ++m) acc += pd[k * MD + m] * (u[(int64_t)st[mem[m]] * NV + v] - u0[v]);
+            for (int m = 0; m < MD; ++m) acc = fma(pd[k * MD + m], u[(int64_t)st[mem[m]] * NV + v] - u0[v], acc);
             dir[s][v][k] = acc;
           }
       }
@@ -365,13 +375,13 @@ static int apply_troubled(port3* P, const double* u) {
       for (int k = 0; k < 3; ++k) /* solve_dofs_linear (reconstruct.cpp:30-41) */
         for (int v = 0; v < NV; ++v) {
           double s = 0.0;
-          for (int m = 0; m < M; ++m) s += pl[k * M + m] * (u[(int64_t)st[m + 1] * NV + v] - u0[v]);
+          for (int m = 0; m < M; ++m) s = fma(pl[k * M + m], u[(int64_t)st[m + 1] * NV + v] - u0[v], s);
           lin[k][v] = s;
         }
       const double* phi = &P->s.phi[(int64_t)op * Q * K];
       for (int q = 0; q < Q; ++q) {
         const double p0 = phi[q * K], p1 = phi[q * K + 1], p2 = phi[q * K + 2];
-        for (int v = 0; v < NV; ++v) qv[q * NV + v] = u0[v] + lin[0][v] * p0 + lin[1][v] * p1 + lin[2][v] * p2;
+        for (int v = 0; v < NV; ++v) qv[q * NV + v] = fma(lin[2][v], p2, fma(lin[1][v], p1, fma(lin[0][v], p0, u0[v])));
       }
       for (int v = 0; v < NV; ++v) {
         double lo = u0[v], hi = u0[v];

@@ -150,6 +150,14 @@ int32_t ucfvb3_get_nad_ties(ucfvb3_solver* h, int64_t* out) {
   NEED(h);
   return guard3(h, [&] { *out = h->s->nad_ties(); });
 }
+int32_t ucfvb3_set_phase_timing(ucfvb3_solver* h, int32_t on) {
+  NEED(h);
+  return guard3(h, [&] { h->s->set_phase_timing(on != 0); });
+}
+int32_t ucfvb3_get_phase_times(ucfvb3_solver* h, double out[5]) {
+  NEED(h);
+  return guard3(h, [&] { h->s->phase_times(out); });
+}
 int64_t ucfvb3_launch_count(const ucfvb3_solver* h) { return (h && h->s) ? h->s->launches() : 0; }
 void* ucfvb3_stream(const ucfvb3_solver* h) { return (h && h->s) ? h->s->stream() : nullptr; }
 

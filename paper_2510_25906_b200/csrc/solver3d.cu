@@ -8,7 +8,9 @@
 // and each thread keeps only its variable's K accumulators. The cross-variable
 // steps (NAD severity over rho and E, positivity of the face values) meet in
 // shared memory. Op orders follow oracle/ucfv3_port.c (the 3D restatement of
-// the reference's 2D functions); kernels are compiled with --fmad=false.
+// the reference's 2D functions); kernels are compiled with --fmad=false and
+// the K x M / Q x K contractions use explicit __fma_rn, as the restatement
+// does with fma() (no reference arithmetic exists in 3D; see its header).
 //
 //   k3_central   solve_dofs + evaluate_cell + NAD raw label + fallback pre-check  (solver.cpp:336-349, 113-149, 229-264)
 //   k3_spread    spread_flags (pull form) + class lists + Linear-cell demotion    (detector.cpp:37-53)
@@ -28,6 +30,7 @@
 #include "device_math.cuh"
 #include "layout.hpp"
 #include "solver3d.hpp"
+#include "tma.cuh"
 
 namespace ucfvb {
 namespace {
@@ -159,12 +162,77 @@ struct Work3 {
   unsigned long long* ties;
 };
 
+// dynamic shared memory of the reconstruction kernels: the cp.async stencil
+// gather [G][160] and, after the solve, the face values [Q][5][33] (union)
+constexpr size_t smem3_bytes(int G, int Q) {
+  return 8 * static_cast<size_t>((G * 160 > Q * V5 * 33) ? G * 160 : Q * V5 * 33);
+}
+
+// evaluate the reconstruction of (cell, var) at its Q face points, stage the
+// values for the positivity check, and report the bounds failure (fallback_check)
+template <int K, int NQ, int NF>
+__device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
+                                           double u0, const double* a, double (*sval)[V5][33], bool chk,
+                                           double blo, double bhi, double& viol) {
+  constexpr int Q = NF * NQ;
+  constexpr int QG = (Q % 4 == 0) ? 4 : ((Q % 3 == 0) ? 3 : 1);  // independent fma chains in flight
+  for (int q0 = 0; q0 < Q; q0 += QG) {
+    double val[QG];
+#pragma unroll
+    for (int j = 0; j < QG; ++j) val[j] = u0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], D.phi[ao(op, (q0 + j) * K + k, Q * K)], val[j]);
+#pragma unroll
+    for (int j = 0; j < QG; ++j) {
+      if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q0 + j, Q)]) * V5 + v] = val[j];
+      sval[q0 + j][v][lane] = val[j];
+      if (chk) viol = smax(viol, smax(blo - val[j], val[j] - bhi));
+    }
+  }
+}
+
+// fallback (solver.cpp:229-264) after a troubled reconstruction; demoted cells
+// get first-order values
+template <int NF, int NQ>
+__device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
+                                                  int lane, bool act, double u0, bool chk, double blo, double bhi,
+                                                  double viol, double (*sval)[V5][33], int* s_fail) {
+  constexpr int Q = NF * NQ;
+  if (v == 0) s_fail[lane] = 0;
+  __syncthreads();
+  if (P.mode == UCFVB_HYBRID) {
+    if (chk) {
+      double dm, dw;
+      compute_margins(P.mg, bhi - blo, dm, dw);
+      if (viol > dm) s_fail[lane] = 1;
+    }
+    for (int p = threadIdx.x; p < Q * 32; p += 160) {
+      const int q = p >> 5, l = p & 31;
+      double s[5];
+#pragma unroll
+      for (int w = 0; w < V5; ++w) s[w] = sval[q][w][l];
+      if (!is_physical3(s, P.gamma)) s_fail[l] = 1;
+    }
+  }
+  __syncthreads();
+  if (act && s_fail[lane]) {
+    if (v == 0) W.labels[c] = UCFVB_SCHEME_FIRST;
+    for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = u0;
+  }
+  __syncthreads();
+}
+
 // ---- central: solve + evaluate + NAD + fallback pre-check -----------------------------
 template <int K, int M, int NF, int NQ>
 __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
-  __shared__ double sval[Q][V5][33];
+  constexpr int G = M + NF;  // stencil members + face neighbours
+  extern __shared__ __align__(16) double smem3[];
+  double* xs = smem3;
+  auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2) W.counters[threadIdx.x] = 0;  // list counters of this stage
@@ -174,40 +242,51 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
     const bool act = c < D.n;
     const int cc = act ? c : (D.n - 1);
     const int op = D.opi[cc];
+    if (D.n_ops == D.n && threadIdx.x == 0 && ch + static_cast<int>(gridDim.x) < nch) {
+      // per-cell operator rows of this block's next chunk -> L2 (TMA prefetch)
+      const int nx = ch + gridDim.x;
+      bulk_prefetch_l2(D.pinv + static_cast<size_t>(nx) * M * K * 32, M * K * 32 * 8);
+      bulk_prefetch_l2(D.phi + static_cast<size_t>(nx) * Q * K * 32, Q * K * 32 * 8);
+      bulk_prefetch_l2(D.central + static_cast<size_t>(nx) * (M + 1) * 32, (M + 1) * 32 * 4);
+    }
+    // every stencil and neighbour value of this (cell, variable) in flight at
+    // once: G fire-and-forget 8-byte cp.async copies into shared memory
+    {
+      int id[G];
+#pragma unroll
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(cc, m + 1, M + 1)];
+#pragma unroll
+      for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(cc, i, NF)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      cp_async_commit();
+    }
     const double u0 = U[static_cast<size_t>(cc) * V5 + v];
+    cp_async_wait_all();  // this thread's own copies
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
-      const double x = U[static_cast<size_t>(D.nbr[ao(cc, i, NF)]) * V5 + v];
+      const double x = xs[(M + i) * 160 + threadIdx.x];
       lo = smin(lo, x);
       hi = smax(hi, x);
     }
     double a[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) a[k] = 0.0;
-#pragma unroll 2
-    for (int m = 0; m < M; ++m) {
-      const int id = D.central[ao(cc, m + 1, M + 1)];
-      const double d = U[static_cast<size_t>(id) * V5 + v] - u0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) a[k] += D.pinv[ao(op, m * K + k, M * K)] * d;
+    for (int m = 0; m < M; ++m) {
+      const double x = xs[m * 160 + threadIdx.x] - u0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
     }
+    __syncthreads();  // the gather buffer becomes the face-value buffer
     if (act) {
 #pragma unroll
       for (int k = 0; k < K; ++k) W.dofs[ao(c, k * V5 + v, K * V5)] = a[k];
     }
     const bool chk = (v == 0 || v == 4);
     double viol = -1e300;
-    if (eval) {
-      for (int q = 0; q < Q; ++q) {
-        double val = u0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) val += a[k] * D.phi[ao(op, q * K + k, Q * K)];
-        if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = val;
-        sval[q][v][lane] = val;
-        if (chk) viol = smax(viol, smax(lo - val, val - hi));
-      }
-    }
+    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol);
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
       const int t = v == 0 ? 0 : 1;
@@ -302,59 +381,14 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
   }
 }
 
-// evaluate the reconstruction of (cell, var) at its Q face points, stage the
-// values for the positivity check, and report the bounds failure (fallback_check)
-template <int K, int NQ, int NF>
-__device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
-                                           double u0, const double* a, double (*sval)[V5][33], bool chk,
-                                           double blo, double bhi, double& viol) {
-  constexpr int Q = NF * NQ;
-  for (int q = 0; q < Q; ++q) {
-    double val = u0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) val += a[k] * D.phi[ao(op, q * K + k, Q * K)];
-    if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = val;
-    sval[q][v][lane] = val;
-    if (chk) viol = smax(viol, smax(blo - val, val - bhi));
-  }
-}
-
-// fallback (solver.cpp:229-264) after a troubled reconstruction; demoted cells
-// get first-order values
-template <int NF, int NQ>
-__device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
-                                                  int lane, bool act, double u0, bool chk, double blo, double bhi,
-                                                  double viol, double (*sval)[V5][33], int* s_fail) {
-  constexpr int Q = NF * NQ;
-  if (v == 0) s_fail[lane] = 0;
-  __syncthreads();
-  if (P.mode == UCFVB_HYBRID) {
-    if (chk) {
-      double dm, dw;
-      compute_margins(P.mg, bhi - blo, dm, dw);
-      if (viol > dm) s_fail[lane] = 1;
-    }
-    for (int p = threadIdx.x; p < Q * 32; p += 160) {
-      const int q = p >> 5, l = p & 31;
-      double s[5];
-#pragma unroll
-      for (int w = 0; w < V5; ++w) s[w] = sval[q][w][l];
-      if (!is_physical3(s, P.gamma)) s_fail[l] = 1;
-    }
-  }
-  __syncthreads();
-  if (act && s_fail[lane]) {
-    if (v == 0) W.labels[c] = UCFVB_SCHEME_FIRST;
-    for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = u0;
-  }
-  __syncthreads();
-}
-
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
 template <int K, int M, int NF, int NQ>
 __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
-  __shared__ double sval[Q][V5][33];
+  constexpr int G = NF * MD3;
+  extern __shared__ __align__(16) double smem3[];
+  double* xs = smem3;
+  auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int cnt = W.counters[kCwList];
@@ -364,20 +398,30 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    // the NF x MD directional gathers in flight at once (cp.async)
+    {
+      int j[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) j[g] = D.dirm[ao(op, g, G)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) j[g] = D.central[ao(c, j[g], M + 1)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(j[g]) * V5 + v]);
+      cp_async_commit();
+    }
+    cp_async_wait_all();
     double dir[NF][3];
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
       double x[MD3];
 #pragma unroll
-      for (int m = 0; m < MD3; ++m) {
-        const int j = D.dirm[ao(op, s * MD3 + m, NF * MD3)];
-        x[m] = U[static_cast<size_t>(D.central[ao(c, j, M + 1)]) * V5 + v] - u0;
-      }
+      for (int m = 0; m < MD3; ++m) x[m] = xs[(s * MD3 + m) * 160 + threadIdx.x] - u0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double acc = 0.0;
 #pragma unroll
-        for (int m = 0; m < MD3; ++m) acc += D.pinv_dir[ao(op, (s * 3 + k) * MD3 + m, NF * 3 * MD3)] * x[m];
+        for (int m = 0; m < MD3; ++m)
+          acc = __fma_rn(D.pinv_dir[ao(op, (s * 3 + k) * MD3 + m, NF * 3 * MD3)], x[m], acc);
         dir[s][k] = acc;
       }
     }
@@ -446,6 +490,7 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
+    __syncthreads();  // the gather buffer becomes the face-value buffer
     eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
@@ -455,7 +500,10 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
 template <int K, int M, int NF, int NQ>
 __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
-  __shared__ double sval[Q][V5][33];
+  constexpr int G = M + NF;
+  extern __shared__ __align__(16) double smem3[];
+  double* xs = smem3;
+  auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int cnt = W.counters[kMuList];
@@ -465,26 +513,39 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    {
+      int id[G];
+#pragma unroll
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
+#pragma unroll
+      for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(c, i, NF)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      cp_async_commit();
+    }
+    cp_async_wait_all();
     double l0 = 0.0, l1 = 0.0, l2 = 0.0;
-#pragma unroll 2
+#pragma unroll
     for (int m = 0; m < M; ++m) {
-      const double d = U[static_cast<size_t>(D.central[ao(c, m + 1, M + 1)]) * V5 + v] - u0;
-      l0 += D.pinv_lin[ao(op, 0 * M + m, 3 * M)] * d;
-      l1 += D.pinv_lin[ao(op, 1 * M + m, 3 * M)] * d;
-      l2 += D.pinv_lin[ao(op, 2 * M + m, 3 * M)] * d;
+      const double x = xs[m * 160 + threadIdx.x] - u0;
+      l0 = __fma_rn(D.pinv_lin[ao(op, 0 * M + m, 3 * M)], x, l0);
+      l1 = __fma_rn(D.pinv_lin[ao(op, 1 * M + m, 3 * M)], x, l1);
+      l2 = __fma_rn(D.pinv_lin[ao(op, 2 * M + m, 3 * M)], x, l2);
     }
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
-      const double x = U[static_cast<size_t>(D.nbr[ao(c, i, NF)]) * V5 + v];
+      const double x = xs[(M + i) * 160 + threadIdx.x];
       lo = smin(lo, x);
       hi = smax(hi, x);
     }
+    __syncthreads();  // the gather buffer becomes the face-value buffer
     double th = 1.0;
     const double e2 = D.eps2[c];
     for (int q = 0; q < Q; ++q) {
-      const double uq = u0 + l0 * D.phi[ao(op, q * K + 0, Q * K)] + l1 * D.phi[ao(op, q * K + 1, Q * K)] +
-                        l2 * D.phi[ao(op, q * K + 2, Q * K)];
+      const double uq = __fma_rn(l2, D.phi[ao(op, q * K + 2, Q * K)],
+                                 __fma_rn(l1, D.phi[ao(op, q * K + 1, Q * K)],
+                                          __fma_rn(l0, D.phi[ao(op, q * K + 0, Q * K)], u0)));
       th = (P.limiter == UCFVB_BARTH_JESPERSEN) ? bj_update(th, u0, lo, hi, uq) : venkat_update(th, u0, lo, hi, uq, e2);
     }
     if (P.limiter == UCFVB_BARTH_JESPERSEN) th = smax(th, 0.0);
@@ -623,6 +684,7 @@ __global__ void k3_time_add(Work3 W) { *W.t += W.dt[0]; }
 
 // ---- dispatch ----------------------------------------------------------------------------------
 struct Kern3 {
+  size_t smem_central, smem_cwenoz, smem_muscl;
   void (*central)(Dev3, Phys3, Work3, const double*, int, int);
   void (*spread)(Dev3, Work3, const double*);
   void (*cwenoz)(Dev3, Phys3, Work3, const double*);
@@ -634,7 +696,8 @@ struct Kern3 {
 
 template <int K, int M, int NF, int NQ>
 Kern3 kern3() {
-  return Kern3{k3_central<K, M, NF, NQ>, k3_spread<NF, NQ>, k3_cwenoz<K, M, NF, NQ>, k3_muscl<K, M, NF, NQ>,
+  return Kern3{smem3_bytes(M + NF, NF * NQ), smem3_bytes(NF * MD3, NF * NQ), smem3_bytes(M + NF, NF * NQ),
+               k3_central<K, M, NF, NQ>, k3_spread<NF, NQ>, k3_cwenoz<K, M, NF, NQ>, k3_muscl<K, M, NF, NQ>,
                k3_constant<NF, NQ>, k3_face_flux<NQ>, k3_gather_rk<NF>};
 }
 
@@ -687,19 +750,38 @@ struct GpuSolver3::Impl {
   int32_t* h_counters = nullptr;
   double* h_dt = nullptr;
   int64_t launches = 0, graph_launches = 0;
-  int central_grid = 0;
+  int central_grid = 0, cw_grid = 0, mu_grid = 0;
   cudaGraphExec_t step_graph = nullptr;
   int graph_rk = -1;
+  // per-kernel-group timing (central, detect, weights, flux, gather+RK) with
+  // events between the groups of un-graphed stages
+  bool timing = false;
+  cudaEvent_t ev[6] = {};
+  double phase_s[5] = {0, 0, 0, 0, 0};
+  void mark(int i) {
+    if (timing) CK3(cudaEventRecord(ev[i], st));
+  }
+  void collect() {
+    if (!timing) return;
+    CK3(cudaEventSynchronize(ev[5]));
+    for (int i = 0; i < 5; ++i) {
+      float ms = 0.f;
+      CK3(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      phase_s[i] += 1e-3 * ms;
+    }
+  }
 
   void launch_stage(const double* Us, bool first, double* out, const double* wa_src, const double* wb_src,
                     double wa, double wb, double wr, double* res, int combine) {
     const int mode = o.mode;
     const bool nad = mode == UCFVB_HYBRID;
     const int nblk = (n + 255) / 256;
+    mark(0);
     if (mode == UCFVB_LINEAR || mode == UCFVB_CWENOZ || mode == UCFVB_HYBRID) {
-      kern.central<<<central_grid, 160, 0, st>>>(D, P, W, Us, mode != UCFVB_CWENOZ ? 1 : 0, nad ? 1 : 0);
+      kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, mode != UCFVB_CWENOZ ? 1 : 0, nad ? 1 : 0);
       ++launches;
     }
+    mark(1);
     if (nad) {
       kern.spread<<<nblk, 256, 0, st>>>(D, W, Us);
       ++launches;
@@ -713,18 +795,23 @@ struct GpuSolver3::Impl {
     } else {
       CK3(cudaMemsetAsync(W.labels, UCFVB_SCHEME_LINEAR, n, st));
     }
+    mark(2);
     if (mode == UCFVB_HYBRID || mode == UCFVB_CWENOZ) {
-      kern.cwenoz<<<central_grid, 160, 0, st>>>(D, P, W, Us);
+      kern.cwenoz<<<cw_grid, 160, kern.smem_cwenoz, st>>>(D, P, W, Us);
       ++launches;
     }
     if (mode == UCFVB_HYBRID || mode == UCFVB_MUSCL) {
-      kern.muscl<<<central_grid, 160, 0, st>>>(D, P, W, Us);
+      kern.muscl<<<mu_grid, 160, kern.smem_muscl, st>>>(D, P, W, Us);
       ++launches;
     }
+    mark(3);
     if (first) CK3(cudaMemcpyAsync(step_labels, W.labels, n, cudaMemcpyDeviceToDevice, st));
     kern.flux<<<(nF + 127) / 128, 128, 0, st>>>(D, P, W);
+    mark(4);
     kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine);
+    mark(5);
     launches += 2;
+    collect();
   }
 
   // one RK step on the device state U with the device dt W.dt
@@ -894,11 +981,17 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     CK3(cudaMemset(I.U, 0, sz * sizeof(double)));
     CK3(cudaMallocHost(&I.h_counters, 4 * sizeof(int32_t)));
     CK3(cudaMallocHost(&I.h_dt, 2 * sizeof(double)));
-    int sms = 148, per = 1;
+    int sms = 148;
     CK3(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-    CK3(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, I.kern.central, 160, 0));
-    I.central_grid = static_cast<int>(std::min<int64_t>(nch, static_cast<int64_t>(sms) * std::max(1, per)));
-    I.central_grid = std::max(1, I.central_grid);
+    auto grid_for = [&](auto fn, size_t smem) {
+      CK3(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      int per = 1;
+      CK3(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 160, smem));
+      return std::max(1, static_cast<int>(std::min<int64_t>(nch, static_cast<int64_t>(sms) * std::max(1, per))));
+    };
+    I.central_grid = grid_for(I.kern.central, I.kern.smem_central);
+    I.cw_grid = grid_for(I.kern.cwenoz, I.kern.smem_cwenoz);
+    I.mu_grid = grid_for(I.kern.muscl, I.kern.smem_muscl);
     I.reset_errors();
     CK3(cudaStreamSynchronize(I.st));
   } catch (...) {
@@ -916,6 +1009,8 @@ GpuSolver3::~GpuSolver3() {
   cudaSetDevice(I.device);
   if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
   if (I.st) cudaStreamSynchronize(I.st);
+  for (auto& e : I.ev)
+    if (e) cudaEventDestroy(e);
   for (void* q : I.owned) cudaFree(q);
   if (I.h_counters) cudaFreeHost(I.h_counters);
   if (I.h_dt) cudaFreeHost(I.h_dt);
@@ -963,6 +1058,17 @@ double GpuSolver3::run_steps(int n_steps, double t0, int rk) {
   I.reset_errors();
   I.h_dt[1] = t0;
   CK3(cudaMemcpyAsync(I.W.t, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
+  if (I.timing) {
+    for (int i = 0; i < n_steps; ++i) {
+      I.dt_kernels(false);
+      I.step(rk);
+      k3_time_add<<<1, 1, 0, I.st>>>(I.W);
+      ++I.launches;
+    }
+    CK3(cudaMemcpyAsync(I.h_dt, I.W.t, sizeof(double), cudaMemcpyDeviceToHost, I.st));
+    I.check_errors();
+    return I.h_dt[0];
+  }
   if (!I.step_graph || I.graph_rk != rk) {
     if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
     I.step_graph = nullptr;
@@ -998,6 +1104,22 @@ void GpuSolver3::compute_residual(const double* u, double t, double* out) {
   I.launch_stage(I.ua, true, nullptr, nullptr, nullptr, 0, 0, 0, I.rhs, 0);
   CK3(cudaMemcpyAsync(out, I.rhs, sizeof(double) * I.n * V5, cudaMemcpyDeviceToHost, I.st));
   I.check_errors();
+}
+
+void GpuSolver3::set_phase_timing(bool on) {
+  Impl& I = *p_;
+  CK3(cudaSetDevice(I.device));
+  if (on && !I.ev[0])
+    for (auto& e : I.ev) CK3(cudaEventCreate(&e));
+  if (on && I.step_graph) {  // graphs bypass the per-group events
+    cudaGraphExecDestroy(I.step_graph);
+    I.step_graph = nullptr;
+  }
+  I.timing = on;
+}
+
+void GpuSolver3::phase_times(double out[5]) {
+  for (int i = 0; i < 5; ++i) out[i] = p_->phase_s[i];
 }
 
 void GpuSolver3::get_labels(int which, uint8_t* out) {

@@ -26,6 +26,8 @@ class GpuSolver3 {
   void get_face_values(double* out);
   void census(int64_t out[4]);
   int64_t nad_ties();
+  void set_phase_timing(bool on);
+  void phase_times(double out[5]);
   int64_t launches() const;
   void* stream() const;
 

@@ -74,6 +74,8 @@ def lib():
             "ucfvb3_get_census": (C.c_int32, [H, P(C.c_int64)]),
             "ucfvb3_get_nad_ties": (C.c_int32, [H, P(C.c_int64)]),
             "ucfvb3_launch_count": (C.c_int64, [H]),
+            "ucfvb3_set_phase_timing": (C.c_int32, [H, C.c_int32]),
+            "ucfvb3_get_phase_times": (C.c_int32, [H, _dp]),
             "ucfvb3_stream": (C.c_void_p, [H]),
         }
         for n, (r, a) in sig.items():
@@ -231,6 +233,14 @@ class Solver3:
         t = C.c_int64()
         _ck(lib().ucfvb3_get_nad_ties(self._h, C.byref(t)), self._h)
         return t.value
+
+    def set_phase_timing(self, on):
+        _ck(lib().ucfvb3_set_phase_timing(self._h, int(on)), self._h)
+
+    def phase_times(self):
+        out = np.zeros(5)
+        _ck(lib().ucfvb3_get_phase_times(self._h, out.ctypes.data_as(_dp)), self._h)
+        return out
 
     def launch_count(self):
         return lib().ucfvb3_launch_count(self._h)

@@ -44,3 +44,17 @@ def test_struct_sizes_match_c_layout():
     # the header's structs are plain C; sizes checked against the ctypes mirror
     assert C.sizeof(A.Options) == 4 * 4 + 6 * 8 + 5 * 8 + 4 + 4 + 8 + 4 + 4
     assert C.sizeof(A.Margins) == 48
+
+
+HEADER3 = Path(__file__).resolve().parents[1] / "include" / "ucfvb3.h"
+
+
+def test_3d_library_exports_every_declared_symbol():
+    text = re.sub(r"/\*.*?\*/", "", HEADER3.read_text(), flags=re.S)
+    syms = sorted(set(re.findall(r"\b(ucfvb3_[a-z0-9_]+)\s*\(", text)))
+    assert len(syms) >= 20
+    lib = C.CDLL(str(A.LIB_PATH))
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    from paper_2510_25906_b200 import solver3d as S3
+    S3.lib()  # every declared 3D symbol has a Python signature

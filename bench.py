@@ -163,10 +163,11 @@ def kernel_bytes3(K, M, NF, NQ, MD, per_cell_ops):
     Q = NF * NQ
     ops = 1 if per_cell_ops else 0
     central = (40 + 4 + 8 + 4 * NF + 4 * (M + 1) + ops * 8 * M * K + ops * 8 * Q * K + 4 * Q
-               + 40 * Q + 40 * K + 32 + 1)
+               + 40 * Q + 32 + 1)
     spread = 1 + 4 * NF + 1 + 4
-    cwenoz = (4 + 40 + 4 + 4 * (M + 1) + ops * (4 * NF * MD + 24 * NF * MD + 8 * K * K + 8 * Q * K)
-              + 40 * K + 4 * Q + 32 + 40 * Q + 1)
+    # CWENOZ recomputes the central solve (pinv re-read) instead of reading stored dofs
+    cwenoz = (4 + 40 + 4 + 4 * (M + 1) + ops * (8 * M * K + 4 * NF * MD + 24 * NF * MD + 8 * K * K + 8 * Q * K)
+              + 4 * Q + 32 + 40 * Q + 1)
     muscl = 4 + 40 + 4 + 4 * (M + 1) + ops * (24 * M + 24 * Q) + 4 * NF + 8 + 4 * Q + 32 + 40 * Q + 1
     faces = NF / 2.0
     flux = faces * (2 * NQ * 40 + NQ * 32 + 40)

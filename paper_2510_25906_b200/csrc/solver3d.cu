@@ -150,7 +150,6 @@ struct Phys3 {
 struct Work3 {
   double* fp;        // [nF][NQ][2][5]
   double* ff;        // [nF][5]
-  double* dofs;      // AoSoA [K*5]
   double* bounds;    // AoSoA [4]
   uint8_t* raw;      // raw label | prefail << 2
   uint8_t* labels;
@@ -173,10 +172,13 @@ constexpr size_t smem3_bytes(int G, int Q) {
 template <int K, int NQ, int NF>
 __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
                                            double u0, const double* a, double (*sval)[V5][33], bool chk,
-                                           double blo, double bhi, double& viol) {
+                                           double blo, double bhi, double& viol, const int* sl) {
   constexpr int Q = NF * NQ;
   constexpr int QG = (Q % 4 == 0) ? 4 : ((Q % 3 == 0) ? 3 : 1);  // independent fma chains in flight
   for (int q0 = 0; q0 < Q; q0 += QG) {
+    int gs[QG];  // this group's slots (issued before the fma chains)
+#pragma unroll
+    for (int j = 0; j < QG; ++j) gs[j] = sl ? sl[q0 + j] : D.slot[ao(c, q0 + j, Q)];
     double val[QG];
 #pragma unroll
     for (int j = 0; j < QG; ++j) val[j] = u0;
@@ -186,7 +188,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
       for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], D.phi[ao(op, (q0 + j) * K + k, Q * K)], val[j]);
 #pragma unroll
     for (int j = 0; j < QG; ++j) {
-      if (act) W.fp[static_cast<size_t>(D.slot[ao(c, q0 + j, Q)]) * V5 + v] = val[j];
+      if (act) W.fp[static_cast<size_t>(gs[j]) * V5 + v] = val[j];
       sval[q0 + j][v][lane] = val[j];
       if (chk) viol = smax(viol, smax(blo - val[j], val[j] - bhi));
     }
@@ -261,6 +263,15 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
       for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
       cp_async_commit();
     }
+    // face-point slots: loaded up front while the gather is in flight for small
+    // stencils, per face-point group for p = 3 (register pressure; measured)
+    constexpr bool kHoist = K * M <= 200;
+    int slh[kHoist ? NF * NQ : 1];
+    if (kHoist) {
+#pragma unroll
+      for (int q = 0; q < (kHoist ? NF * NQ : 0); ++q) slh[q] = D.slot[ao(c, q, NF * NQ)];
+    }
+    const int* sl = kHoist ? slh : nullptr;
     const double u0 = U[static_cast<size_t>(cc) * V5 + v];
     cp_async_wait_all();  // this thread's own copies
     double lo = u0, hi = u0;
@@ -280,13 +291,9 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
       for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
-    if (act) {
-#pragma unroll
-      for (int k = 0; k < K; ++k) W.dofs[ao(c, k * V5 + v, K * V5)] = a[k];
-    }
     const bool chk = (v == 0 || v == 4);
     double viol = -1e300;
-    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol);
+    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl);
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
       const int t = v == 0 ? 0 : 1;
@@ -385,7 +392,7 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
 template <int K, int M, int NF, int NQ>
 __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
-  constexpr int G = NF * MD3;
+  constexpr int G = M;  // the central stencil (the directional members are a subset of it)
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
@@ -398,24 +405,36 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
-    // the NF x MD directional gathers in flight at once (cp.async)
+    // the M central-stencil values in flight at once (cp.async); the central
+    // solve is recomputed here (bit-identical to k3_central's) instead of
+    // storing K x 5 dofs for every cell
     {
-      int j[G];
+      int id[M];
 #pragma unroll
-      for (int g = 0; g < G; ++g) j[g] = D.dirm[ao(op, g, G)];
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
 #pragma unroll
-      for (int g = 0; g < G; ++g) j[g] = D.central[ao(c, j[g], M + 1)];
-#pragma unroll
-      for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(j[g]) * V5 + v]);
+      for (int m = 0; m < M; ++m) cp_async8(&xs[m * 160 + threadIdx.x], &U[static_cast<size_t>(id[m]) * V5 + v]);
       cp_async_commit();
     }
+    int sl[NF * NQ];  // face-point slots, loaded while the gather is in flight
+#pragma unroll
+    for (int q = 0; q < NF * NQ; ++q) sl[q] = D.slot[ao(c, q, NF * NQ)];
     cp_async_wait_all();
+    double p1[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) p1[k] = 0.0;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double x = xs[m * 160 + threadIdx.x] - u0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) p1[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
+    }
     double dir[NF][3];
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
       double x[MD3];
 #pragma unroll
-      for (int m = 0; m < MD3; ++m) x[m] = xs[(s * MD3 + m) * 160 + threadIdx.x] - u0;
+      for (int m = 0; m < MD3; ++m) x[m] = xs[(D.dirm[ao(op, s * MD3 + m, NF * MD3)] - 1) * 160 + threadIdx.x] - u0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double acc = 0.0;
@@ -425,9 +444,6 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
         dir[s][k] = acc;
       }
     }
-    double p1[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) p1[k] = W.dofs[ao(c, k * V5 + v, K * V5)];
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
       p1[0] -= P.lams * dir[s][0];
@@ -491,7 +507,7 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol);
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
@@ -523,6 +539,9 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
       cp_async_commit();
     }
+    int sl[NF * NQ];  // face-point slots, loaded while the gather is in flight
+#pragma unroll
+    for (int q = 0; q < NF * NQ; ++q) sl[q] = D.slot[ao(c, q, NF * NQ)];
     cp_async_wait_all();
     double l0 = 0.0, l1 = 0.0, l2 = 0.0;
 #pragma unroll
@@ -561,7 +580,7 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol);
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
@@ -696,7 +715,7 @@ struct Kern3 {
 
 template <int K, int M, int NF, int NQ>
 Kern3 kern3() {
-  return Kern3{smem3_bytes(M + NF, NF * NQ), smem3_bytes(NF * MD3, NF * NQ), smem3_bytes(M + NF, NF * NQ),
+  return Kern3{smem3_bytes(M + NF, NF * NQ), smem3_bytes(M, NF * NQ), smem3_bytes(M + NF, NF * NQ),
                k3_central<K, M, NF, NQ>, k3_spread<NF, NQ>, k3_cwenoz<K, M, NF, NQ>, k3_muscl<K, M, NF, NQ>,
                k3_constant<NF, NQ>, k3_face_flux<NQ>, k3_gather_rk<NF>};
 }
@@ -777,8 +796,8 @@ struct GpuSolver3::Impl {
     const bool nad = mode == UCFVB_HYBRID;
     const int nblk = (n + 255) / 256;
     mark(0);
-    if (mode == UCFVB_LINEAR || mode == UCFVB_CWENOZ || mode == UCFVB_HYBRID) {
-      kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, mode != UCFVB_CWENOZ ? 1 : 0, nad ? 1 : 0);
+    if (mode == UCFVB_LINEAR || mode == UCFVB_HYBRID) {  // forced CWENOZ solves inside k3_cwenoz
+      kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
       ++launches;
     }
     mark(1);
@@ -954,7 +973,6 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     const int64_t nch = (n + 31) / 32;
     W.fp = dalloc<double>(static_cast<size_t>(I.nF) * NQ * 2 * V5, I.owned);
     W.ff = dalloc<double>(static_cast<size_t>(I.nF) * V5, I.owned);
-    W.dofs = dalloc<double>(static_cast<size_t>(nch) * 32 * K * V5, I.owned);
     W.bounds = dalloc<double>(static_cast<size_t>(nch) * 32 * 4, I.owned);
     W.raw = dalloc<uint8_t>(n, I.owned);
     W.labels = dalloc<uint8_t>(n, I.owned);

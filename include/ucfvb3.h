@@ -52,14 +52,18 @@ typedef struct ucfvb3_stencils ucfvb3_stencils;
 typedef struct ucfvb3_solver ucfvb3_solver;
 
 /*
- * Flattened periodic 3D mesh. Cell c lies in lattice cube c / n_types
- * ((k*ny + j)*nx + i) and has type c % n_types (hex: 1 type; tet: the 6
- * Freudenthal tetrahedra of the cube). Faces per cell nf (hex 6, tet 4),
+ * Flattened periodic 3D mesh. Each lattice cube ((k*ny + j)*nx + i) holds
+ * n_types cells (hex: 1; tet: the 6 Freudenthal tetrahedra), numbered as
+ * cell_order says. Faces per cell nf (hex 6, tet 4),
  * quadrature points per face nq.
  */
 typedef struct ucfvb3_mesh_view {
   int32_t kind, nx, ny, nz, n_types;
   int32_t n_cells, n_faces, nf, nq, nvc;
+  /* 0: cell = cube * n_types + type; 1 (tetrahedra, nx*ny*nz % 32 == 0): cubes in
+   * blocks of 32, type-major inside a block: cell = ((cube/32)*6 + type)*32 + cube%32,
+   * so every 32-cell chunk holds a single type */
+  int32_t cell_order;
   double period[3];
   const double* cell_vtx;       /* [n_cells][nvc][3] vertex coordinates, unwrapped around the cell */
   const double* cell_centroid;  /* [n_cells][3] */

@@ -26,7 +26,7 @@
 #include "ucfvb3.h"
 
 struct ucfvb3_mesh {
-  int kind = 0, nx = 0, ny = 0, nz = 0, nt = 1, n = 0, nF = 0, nf = 0, nq = 0, nvc = 0;
+  int kind = 0, nx = 0, ny = 0, nz = 0, nt = 1, n = 0, nF = 0, nf = 0, nq = 0, nvc = 0, blocked = 0;
   double L[3] = {0, 0, 0};
   std::vector<double> cell_vtx, centroid, volume, h;
   std::vector<int32_t> cell_faces, cell_nbr, cell_nbr_shift;
@@ -350,6 +350,10 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
   if (nF64 * M->nq * 2 >= (int64_t(1) << 31)) throw ApiError(UCFVB_INVALID, "mesh3d: too many faces for int32 slots");
   const int n = static_cast<int>(n64), nF = static_cast<int>(nF64);
   M->n = n, M->nF = nF;
+  // tetrahedra of 32 consecutive cubes are numbered type-major, so every
+  // 32-cell chunk holds one type (one shared operator row under lattice classes)
+  M->blocked = (T.nt == 6 && ncube % 32 == 0) ? 1 : 0;
+  const CellOrder ord{T.nt, M->blocked};
   const double hh[3] = {lx / nx, ly / ny, lz / nz};
   // wrapped vertex positions
   std::vector<double> vpos(static_cast<size_t>(ncube) * 3);
@@ -377,7 +381,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
   M->face_vtx.assign(static_cast<size_t>(nF) * 12, 0.0);
   const int N3[3] = {nx, ny, nz};
   auto cube_of = [&](int64_t c, int* ijk) {
-    const int64_t q = c / T.nt;
+    const int64_t q = ord.cube(c);
     ijk[0] = static_cast<int>(q % nx);
     ijk[1] = static_cast<int>((q / nx) % ny);
     ijk[2] = static_cast<int>(q / (static_cast<int64_t>(nx) * ny));
@@ -388,7 +392,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
     for (int64_t c = a0; c < a1; ++c) {
       int ijk[3];
       cube_of(c, ijk);
-      const int t = static_cast<int>(c % T.nt);
+      const int t = ord.type(c);
       double* cv = &M->cell_vtx[static_cast<size_t>(c) * nvc * 3];
       for (int v = 0; v < nvc; ++v) {
         int64_t w[3];
@@ -411,7 +415,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
       M->volume[c] = vol;
       M->h[c] = std::cbrt(vol);
       for (int d = 0; d < 3; ++d) M->centroid[3 * c + d] = xc[d] / vol;
-      const int64_t cube = c / T.nt;
+      const int64_t cube = ord.cube(c);
       for (int lf = 0; lf < nf; ++lf) {
         const auto& F = T.face[t][lf];
         int nb[3];
@@ -422,7 +426,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
           sh[d] = (g < 0) ? -1 : (g >= N3[d] ? 1 : 0);
         }
         M->cell_nbr[static_cast<size_t>(c) * nf + lf] =
-            static_cast<int32_t>(((static_cast<int64_t>(nb[2]) * ny + nb[1]) * nx + nb[0]) * T.nt + F.nt);
+            static_cast<int32_t>(ord.cell((static_cast<int64_t>(nb[2]) * ny + nb[1]) * nx + nb[0], F.nt));
         M->cell_side[static_cast<size_t>(c) * nf + lf] = F.left ? 0 : 1;
         if (F.left)
           M->cell_faces[static_cast<size_t>(c) * nf + lf] =
@@ -433,7 +437,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
   // pass 2: right-face ids and face geometry (computed by the left cell)
   parallel_for(n, n_threads, [&](int64_t a0, int64_t a1) {
     for (int64_t c = a0; c < a1; ++c) {
-      const int t = static_cast<int>(c % T.nt);
+      const int t = ord.type(c);
       for (int lf = 0; lf < nf; ++lf) {
         const auto& F = T.face[t][lf];
         const size_t i = static_cast<size_t>(c) * nf + lf;
@@ -476,6 +480,7 @@ ucfvb3_mesh* mesh3_periodic_box(int nx, int ny, int nz, double lx, double ly, do
 ucfvb3_mesh_view mesh3_view(const ucfvb3_mesh* M) {
   ucfvb3_mesh_view v{};
   v.kind = M->kind, v.nx = M->nx, v.ny = M->ny, v.nz = M->nz, v.n_types = M->nt;
+  v.cell_order = M->blocked;
   v.n_cells = M->n, v.n_faces = M->nF, v.nf = M->nf, v.nq = M->nq, v.nvc = M->nvc;
   for (int d = 0; d < 3; ++d) v.period[d] = M->L[d];
   v.cell_vtx = M->cell_vtx.data();
@@ -772,17 +777,18 @@ ucfvb3_stencils* build_stencils3(const ucfvb3_mesh_view& m, int order, int si, i
   const int nt = m.n_types, nx = m.nx, ny = m.ny, nz = m.nz;
   const int ci[3] = {nx / 2, ny / 2, nz / 2};
   const double hx[3] = {m.period[0] / nx, m.period[1] / ny, m.period[2] / nz};
+  const CellOrder ord{nt, m.cell_order};
   auto cell_id = [&](int64_t i, int64_t j, int64_t k, int t) {
-    return static_cast<int32_t>(((k * ny + j) * nx + i) * nt + t);
+    return static_cast<int32_t>(ord.cell((k * ny + j) * nx + i, t));
   };
   {
     // translation check on the corner coordinates (unjittered lattice only)
     std::vector<int> bad(1, 0);
     parallel_for(n, n_threads, [&](int64_t a0, int64_t a1) {
       for (int64_t c = a0; c < a1; ++c) {
-        const int64_t q = c / nt;
+        const int64_t q = ord.cube(c);
         const int64_t ijk[3] = {q % nx, (q / nx) % ny, q / (static_cast<int64_t>(nx) * ny)};
-        const int64_t c0 = cell_id(0, 0, 0, static_cast<int>(c % nt));
+        const int64_t c0 = cell_id(0, 0, 0, ord.type(c));
         for (int v = 0; v < m.nvc; ++v)
           for (int d = 0; d < 3; ++d) {
             const double a = m.cell_vtx[(static_cast<size_t>(c) * m.nvc + v) * 3 + d] - ijk[d] * hx[d];
@@ -801,19 +807,19 @@ ucfvb3_stencils* build_stencils3(const ucfvb3_mesh_view& m, int order, int si, i
     B.build(c0, o);
     store_ops(t, o);
     for (const E3& e : o.central) {
-      const int64_t q = e.cell / nt;
+      const int64_t q = ord.cube(e.cell);
       const int64_t ijk[3] = {q % nx, (q / nx) % ny, q / (static_cast<int64_t>(nx) * ny)};
       std::array<int, 4> d{};
       const int N3[3] = {nx, ny, nz};
       for (int a = 0; a < 3; ++a) d[a] = static_cast<int>(ijk[a] + static_cast<int64_t>(e.s[a]) * N3[a] - ci[a]);
-      d[3] = e.cell % nt;
+      d[3] = ord.type(e.cell);
       offs[t].push_back(d);
     }
   }
   parallel_for(n, n_threads, [&](int64_t a0, int64_t a1) {
     for (int64_t c = a0; c < a1; ++c) {
-      const int t = static_cast<int>(c % nt);
-      const int64_t q = c / nt;
+      const int t = ord.type(c);
+      const int64_t q = ord.cube(c);
       const int64_t ijk[3] = {q % nx, (q / nx) % ny, q / (static_cast<int64_t>(nx) * ny)};
       S->op_index[c] = t;
       for (int j = 0; j <= M; ++j) {

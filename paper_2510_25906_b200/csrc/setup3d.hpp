@@ -9,6 +9,18 @@
 
 namespace ucfvb {
 
+// cell numbering of the lattice meshes: cube-major (c = cube * nt + type), or
+// for tetrahedra on n^3 % 32 == 0 lattices type-major within blocks of 32
+// cubes (c = ((cube / 32) * 6 + type) * 32 + cube % 32)
+struct CellOrder {
+  int nt, blocked;
+  int64_t cell(int64_t cube, int t) const {
+    return blocked ? (((cube >> 5) * nt + t) << 5) + (cube & 31) : cube * nt + t;
+  }
+  int64_t cube(int64_t c) const { return blocked ? (((c >> 5) / nt) << 5) + (c & 31) : c / nt; }
+  int type(int64_t c) const { return static_cast<int>(blocked ? (c >> 5) % nt : c % nt); }
+};
+
 // Legendre-product basis P_i(x) P_j(y) P_k(z), 1 <= i+j+k <= r, ordered by
 // total degree then descending i, j (basis.cpp:34-68 with a third factor)
 struct Family3 {

@@ -37,7 +37,7 @@ namespace {
 
 constexpr int V5 = 5;
 constexpr int MD3 = 6;
-constexpr int kCwList = 0, kMuList = 1, kBadFace = 2, kBadCell = 3;
+constexpr int kCwList = 0, kMuList = 1, kBadFace = 2, kBadCell = 3, kCnt0 = 4;
 
 #define CK3(x)                                                                                      \
   do {                                                                                              \
@@ -153,17 +153,23 @@ struct Work3 {
   double* bounds;    // AoSoA [4]
   uint8_t* raw;      // raw label | prefail << 2
   uint8_t* labels;
-  int32_t* lists;    // [2][n]
-  int32_t* counters; // cw, mu, bad face, bad cell
+  int32_t* lists;    // [2][ntl][cap] class lists (ntl = 1, or one per lattice type when staged)
+  int32_t* counters; // [0..1] unused, bad face, bad cell, then [4 + L*ntl + t] list lengths
+  int ntl, cap;
   unsigned long long* dtmin;
   double* dt;        // device dt of the current step
   double* t;         // device time
   unsigned long long* ties;
 };
+__device__ __forceinline__ int cnt_idx(const Work3& W, int L, int t) { return kCnt0 + L * W.ntl + t; }
+__device__ __forceinline__ int32_t* list_of(const Work3& W, int L, int t) {
+  return W.lists + (static_cast<size_t>(L) * W.ntl + t) * W.cap;
+}
+
 
 // dynamic shared memory of the reconstruction kernels: the cp.async stencil
 // gather [G][160] and, after the solve, the face values [Q][5][33] (union)
-constexpr size_t smem3_bytes(int G, int Q) {
+__host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
   return 8 * static_cast<size_t>((G * 160 > Q * V5 * 33) ? G * 160 : Q * V5 * 33);
 }
 
@@ -172,7 +178,8 @@ constexpr size_t smem3_bytes(int G, int Q) {
 template <int K, int NQ, int NF>
 __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
                                            double u0, const double* a, double (*sval)[V5][33], bool chk,
-                                           double blo, double bhi, double& viol, const int* sl) {
+                                           double blo, double bhi, double& viol, const int* sl,
+                                           const double* phs = nullptr) {
   constexpr int Q = NF * NQ;
   constexpr int QG = (Q % 4 == 0) ? 4 : ((Q % 3 == 0) ? 3 : 1);  // independent fma chains in flight
   for (int q0 = 0; q0 < Q; q0 += QG) {
@@ -182,10 +189,22 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
     double val[QG];
 #pragma unroll
     for (int j = 0; j < QG; ++j) val[j] = u0;
+    if (phs) {  // the block's operator row staged in shared memory (broadcast 16-byte reads)
+      double2 w[QG];
 #pragma unroll
-    for (int k = 0; k < K; ++k)
+      for (int k = 0; k < K; ++k)
 #pragma unroll
-      for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], D.phi[ao(op, (q0 + j) * K + k, Q * K)], val[j]);
+        for (int j = 0; j < QG; ++j) {
+          const int e = (q0 + j) * K + k;
+          if ((e & 1) == 0 || k == 0) w[j] = reinterpret_cast<const double2*>(phs)[e >> 1];
+          val[j] = __fma_rn(a[k], (e & 1) ? w[j].y : w[j].x, val[j]);
+        }
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], D.phi[ao(op, (q0 + j) * K + k, Q * K)], val[j]);
+    }
 #pragma unroll
     for (int j = 0; j < QG; ++j) {
       if (act) W.fp[static_cast<size_t>(gs[j]) * V5 + v] = val[j];
@@ -227,7 +246,11 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 }
 
 // ---- central: solve + evaluate + NAD + fallback pre-check -----------------------------
-template <int K, int M, int NF, int NQ>
+// STAGED: lattice-class operators on a type-blocked mesh (every chunk one
+// type): the grid is a multiple of the type count, so block b only ever sees
+// chunks of type b % 6 and stages that type's pinv and phi rows in shared
+// memory once, read as broadcast 16-byte loads
+template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
@@ -235,10 +258,17 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
+  double* sp = smem3 + smem3_bytes(G, Q) / 8;  // STAGED: pinv row [M][K] then phi row [Q][K]
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
-  if (blockIdx.x == 0 && threadIdx.x < 2) W.counters[threadIdx.x] = 0;  // list counters of this stage
+  if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
   const int nch = (D.n + 31) >> 5;
+  if (STAGED) {
+    const int t = blockIdx.x % D.n_ops;
+    for (int e = threadIdx.x; e < M * K; e += 160) sp[e] = D.pinv[ao(t, e, M * K)];
+    for (int e = threadIdx.x; e < Q * K; e += 160) sp[M * K + e] = D.phi[ao(t, e, Q * K)];
+    __syncthreads();
+  }
   for (int ch = blockIdx.x; ch < nch; ch += gridDim.x) {
     const int c = (ch << 5) + lane;
     const bool act = c < D.n;
@@ -284,16 +314,26 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
     double a[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) a[k] = 0.0;
+    double2 w = make_double2(0.0, 0.0);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const double x = xs[m * 160 + threadIdx.x] - u0;
+      if (STAGED) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
+        for (int k = 0; k < K; ++k) {
+          const int e = m * K + k;
+          if ((e & 1) == 0) w = reinterpret_cast<const double2*>(sp)[e >> 1];
+          a[k] = __fma_rn((e & 1) ? w.y : w.x, x, a[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
+      }
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
     const bool chk = (v == 0 || v == 4);
     double viol = -1e300;
-    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl);
+    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl, STAGED ? sp + M * K : nullptr);
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
       const int t = v == 0 ? 0 : 1;
@@ -372,35 +412,54 @@ __global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* 
     const unsigned b = __ballot_sync(0xffffffffu, mine);
     if (!b) continue;
     int base = 0;
-    if (lane == 0) base = atomicAdd(&W.counters[L], __popc(b));
+    // type-blocked meshes: the warp's 32 cells share one lattice type
+    const int t = W.ntl > 1 ? ((c >> 5) % W.ntl) : 0;
+    if (lane == 0) base = atomicAdd(&W.counters[cnt_idx(W, L, t)], __popc(b));
     base = __shfl_sync(0xffffffffu, base, 0);
-    if (mine) W.lists[static_cast<size_t>(L) * D.n + base + __popc(b & ((1u << lane) - 1u))] = c;
+    if (mine) list_of(W, L, t)[base + __popc(b & ((1u << lane) - 1u))] = c;
   }
 }
 
 // forced modes: every cell in one list (SchemeMode::Cwenoz / Muscl, solver.cpp:322-328)
 __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c == 0) W.counters[which] = n;
+  if (c == 0)
+    for (int t = 0; t < W.ntl; ++t) W.counters[cnt_idx(W, which, t)] = n / W.ntl;
   if (c < n) {
-    W.lists[static_cast<size_t>(which) * n + c] = c;
+    const int t = W.ntl > 1 ? ((c >> 5) % W.ntl) : 0;
+    const int i = W.ntl > 1 ? ((c >> 5) / W.ntl) * 32 + (c & 31) : c;
+    list_of(W, which, t)[i] = c;
     W.labels[c] = lab;
   }
 }
 
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
-template <int K, int M, int NF, int NQ>
+template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
+  constexpr int EP = M * K, ED = NF * 3 * MD3, EO = (K * K + 1) & ~1;  // region sizes (even: phi is read as double2)
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
+  // STAGED: this block's lattice type's rows: pinv | pinv_dir | OI | phi | dir members
+  double* sp = smem3 + smem3_bytes(G, Q) / 8;
+  int* sdm = reinterpret_cast<int*>(sp + EP + ED + EO + Q * K);
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
-  const int cnt = W.counters[kCwList];
-  const int32_t* list = W.lists;
-  for (int base = blockIdx.x * 32; base < cnt; base += gridDim.x * 32) {
+  const int t = STAGED ? blockIdx.x % W.ntl : 0;
+  const int b0 = STAGED ? blockIdx.x / W.ntl : blockIdx.x, nb = STAGED ? gridDim.x / W.ntl : gridDim.x;
+  const int cnt = W.counters[cnt_idx(W, kCwList, t)];
+  const int32_t* list = list_of(W, kCwList, t);
+  if (STAGED) {
+    for (int e = threadIdx.x; e < EP; e += 160) sp[e] = D.pinv[ao(t, e, EP)];
+    for (int e = threadIdx.x; e < ED; e += 160) sp[EP + e] = D.pinv_dir[ao(t, e, ED)];
+    for (int e = threadIdx.x; e < K * K; e += 160) sp[EP + ED + e] = D.oi[ao(t, e, K * K)];
+    for (int e = threadIdx.x; e < Q * K; e += 160) sp[EP + ED + EO + e] = D.phi[ao(t, e, Q * K)];
+    for (int e = threadIdx.x; e < NF * MD3; e += 160) sdm[e] = D.dirm[ao(t, e, NF * MD3)];
+    __syncthreads();
+  }
+  for (int base = b0 * 32; base < cnt; base += nb * 32) {
     const bool act = base + lane < cnt;
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
@@ -427,20 +486,23 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     for (int m = 0; m < M; ++m) {
       const double x = xs[m * 160 + threadIdx.x] - u0;
 #pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
+      for (int k = 0; k < K; ++k)
+        p1[k] = __fma_rn(STAGED ? sp[m * K + k] : D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
     }
     double dir[NF][3];
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
       double x[MD3];
 #pragma unroll
-      for (int m = 0; m < MD3; ++m) x[m] = xs[(D.dirm[ao(op, s * MD3 + m, NF * MD3)] - 1) * 160 + threadIdx.x] - u0;
+      for (int m = 0; m < MD3; ++m)
+        x[m] = xs[((STAGED ? sdm[s * MD3 + m] : D.dirm[ao(op, s * MD3 + m, NF * MD3)]) - 1) * 160 + threadIdx.x] - u0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double acc = 0.0;
 #pragma unroll
         for (int m = 0; m < MD3; ++m)
-          acc = __fma_rn(D.pinv_dir[ao(op, (s * 3 + k) * MD3 + m, NF * 3 * MD3)], x[m], acc);
+          acc = __fma_rn(STAGED ? sp[EP + (s * 3 + k) * MD3 + m] : D.pinv_dir[ao(op, (s * 3 + k) * MD3 + m, ED)],
+                         x[m], acc);
         dir[s][k] = acc;
       }
     }
@@ -457,13 +519,13 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     for (int k = 0; k < K; ++k) {
       double t = 0.0;
 #pragma unroll
-      for (int q = 0; q < K; ++q) t += D.oi[ao(op, k * K + q, K * K)] * p1[q];
+      for (int q = 0; q < K; ++q) t += (STAGED ? sp[EP + ED + k * K + q] : (STAGED ? sp[EP + ED + (k * K + q)] : D.oi[ao(op, k * K + q, K * K)])) * p1[q];
       si0 += p1[k] * t;
     }
-    const double o00 = D.oi[ao(op, 0, K * K)], o01 = D.oi[ao(op, 1, K * K)], o02 = D.oi[ao(op, 2, K * K)];
-    const double o10 = D.oi[ao(op, K, K * K)], o11 = D.oi[ao(op, K + 1, K * K)], o12 = D.oi[ao(op, K + 2, K * K)];
-    const double o20 = D.oi[ao(op, 2 * K, K * K)], o21 = D.oi[ao(op, 2 * K + 1, K * K)],
-                 o22 = D.oi[ao(op, 2 * K + 2, K * K)];
+    const double o00 = (STAGED ? sp[EP + ED + (0)] : D.oi[ao(op, 0, K * K)]), o01 = (STAGED ? sp[EP + ED + (1)] : D.oi[ao(op, 1, K * K)]), o02 = (STAGED ? sp[EP + ED + (2)] : D.oi[ao(op, 2, K * K)]);
+    const double o10 = (STAGED ? sp[EP + ED + (K)] : D.oi[ao(op, K, K * K)]), o11 = (STAGED ? sp[EP + ED + (K + 1)] : D.oi[ao(op, K + 1, K * K)]), o12 = (STAGED ? sp[EP + ED + (K + 2)] : D.oi[ao(op, K + 2, K * K)]);
+    const double o20 = (STAGED ? sp[EP + ED + (2 * K)] : D.oi[ao(op, 2 * K, K * K)]), o21 = (STAGED ? sp[EP + ED + (2 * K + 1)] : D.oi[ao(op, 2 * K + 1, K * K)]),
+                 o22 = (STAGED ? sp[EP + ED + (2 * K + 2)] : D.oi[ao(op, 2 * K + 2, K * K)]);
     double si[NF];
     double tau = 0.0;
 #pragma unroll
@@ -507,24 +569,33 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl);
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
+                          STAGED ? sp + EP + ED + EO : nullptr);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
 
 // ---- MUSCL (solver.cpp:189-221; reconstruct.cpp:30-86) ---------------------------------
-template <int K, int M, int NF, int NQ>
+template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M + NF;
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
+  double* sp = smem3 + smem3_bytes(G, Q) / 8;  // STAGED: pinv_lin [3][M] | phi [Q][K]
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
-  const int cnt = W.counters[kMuList];
-  const int32_t* list = W.lists + D.n;
-  for (int base = blockIdx.x * 32; base < cnt; base += gridDim.x * 32) {
+  const int t = STAGED ? blockIdx.x % W.ntl : 0;
+  const int b0 = STAGED ? blockIdx.x / W.ntl : blockIdx.x, nb = STAGED ? gridDim.x / W.ntl : gridDim.x;
+  const int cnt = W.counters[cnt_idx(W, kMuList, t)];
+  const int32_t* list = list_of(W, kMuList, t);
+  if (STAGED) {
+    for (int e = threadIdx.x; e < 3 * M; e += 160) sp[e] = D.pinv_lin[ao(t, e, 3 * M)];
+    for (int e = threadIdx.x; e < Q * K; e += 160) sp[3 * M + e] = D.phi[ao(t, e, Q * K)];
+    __syncthreads();
+  }
+  for (int base = b0 * 32; base < cnt; base += nb * 32) {
     const bool act = base + lane < cnt;
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
@@ -547,9 +618,9 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
 #pragma unroll
     for (int m = 0; m < M; ++m) {
       const double x = xs[m * 160 + threadIdx.x] - u0;
-      l0 = __fma_rn(D.pinv_lin[ao(op, 0 * M + m, 3 * M)], x, l0);
-      l1 = __fma_rn(D.pinv_lin[ao(op, 1 * M + m, 3 * M)], x, l1);
-      l2 = __fma_rn(D.pinv_lin[ao(op, 2 * M + m, 3 * M)], x, l2);
+      l0 = __fma_rn((STAGED ? sp[0 * M + m] : D.pinv_lin[ao(op, 0 * M + m, 3 * M)]), x, l0);
+      l1 = __fma_rn((STAGED ? sp[1 * M + m] : D.pinv_lin[ao(op, 1 * M + m, 3 * M)]), x, l1);
+      l2 = __fma_rn((STAGED ? sp[2 * M + m] : D.pinv_lin[ao(op, 2 * M + m, 3 * M)]), x, l2);
     }
     double lo = u0, hi = u0;
 #pragma unroll
@@ -562,9 +633,9 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     double th = 1.0;
     const double e2 = D.eps2[c];
     for (int q = 0; q < Q; ++q) {
-      const double uq = __fma_rn(l2, D.phi[ao(op, q * K + 2, Q * K)],
-                                 __fma_rn(l1, D.phi[ao(op, q * K + 1, Q * K)],
-                                          __fma_rn(l0, D.phi[ao(op, q * K + 0, Q * K)], u0)));
+      const double uq = __fma_rn(l2, (STAGED ? sp[3 * M + q * K + 2] : D.phi[ao(op, q * K + 2, Q * K)]),
+                                 __fma_rn(l1, (STAGED ? sp[3 * M + q * K + 1] : D.phi[ao(op, q * K + 1, Q * K)]),
+                                          __fma_rn(l0, (STAGED ? sp[3 * M + q * K + 0] : D.phi[ao(op, q * K + 0, Q * K)]), u0)));
       th = (P.limiter == UCFVB_BARTH_JESPERSEN) ? bj_update(th, u0, lo, hi, uq) : venkat_update(th, u0, lo, hi, uq, e2);
     }
     if (P.limiter == UCFVB_BARTH_JESPERSEN) th = smax(th, 0.0);
@@ -580,7 +651,8 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl);
+    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
+                          STAGED ? sp + 3 * M : nullptr);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
@@ -703,11 +775,15 @@ __global__ void k3_time_add(Work3 W) { *W.t += W.dt[0]; }
 
 // ---- dispatch ----------------------------------------------------------------------------------
 struct Kern3 {
-  size_t smem_central, smem_cwenoz, smem_muscl;
+  size_t smem_central, smem_cwenoz, smem_muscl, smem_central_staged;
   void (*central)(Dev3, Phys3, Work3, const double*, int, int);
+  void (*central_staged)(Dev3, Phys3, Work3, const double*, int, int);
   void (*spread)(Dev3, Work3, const double*);
   void (*cwenoz)(Dev3, Phys3, Work3, const double*);
   void (*muscl)(Dev3, Phys3, Work3, const double*);
+  void (*cwenoz_staged)(Dev3, Phys3, Work3, const double*);
+  void (*muscl_staged)(Dev3, Phys3, Work3, const double*);
+  size_t smem_cwenoz_staged, smem_muscl_staged;
   void (*constant)(Dev3, Work3, const double*);
   void (*flux)(Dev3, Phys3, Work3);
   void (*gather)(Dev3, Work3, const double*, const double*, double*, double*, double, double, double, int);
@@ -715,9 +791,26 @@ struct Kern3 {
 
 template <int K, int M, int NF, int NQ>
 Kern3 kern3() {
-  return Kern3{smem3_bytes(M + NF, NF * NQ), smem3_bytes(M, NF * NQ), smem3_bytes(M + NF, NF * NQ),
-               k3_central<K, M, NF, NQ>, k3_spread<NF, NQ>, k3_cwenoz<K, M, NF, NQ>, k3_muscl<K, M, NF, NQ>,
-               k3_constant<NF, NQ>, k3_face_flux<NQ>, k3_gather_rk<NF>};
+  constexpr int Q = NF * NQ;
+  Kern3 k{};
+  k.smem_central = smem3_bytes(M + NF, Q);
+  k.smem_cwenoz = smem3_bytes(M, Q);
+  k.smem_muscl = smem3_bytes(M + NF, Q);
+  k.smem_central_staged = k.smem_central + 8 * static_cast<size_t>(M * K + Q * K);
+  k.smem_cwenoz_staged = k.smem_cwenoz + 8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K) +
+                         4 * static_cast<size_t>(NF * MD3);
+  k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);
+  k.central = k3_central<K, M, NF, NQ, false>;
+  k.central_staged = k3_central<K, M, NF, NQ, true>;
+  k.spread = k3_spread<NF, NQ>;
+  k.cwenoz = k3_cwenoz<K, M, NF, NQ, false>;
+  k.muscl = k3_muscl<K, M, NF, NQ, false>;
+  k.cwenoz_staged = k3_cwenoz<K, M, NF, NQ, true>;
+  k.muscl_staged = k3_muscl<K, M, NF, NQ, true>;
+  k.constant = k3_constant<NF, NQ>;
+  k.flux = k3_face_flux<NQ>;
+  k.gather = k3_gather_rk<NF>;
+  return k;
 }
 
 bool pick3(int K, int M, int NF, int NQ, Kern3& k) {
@@ -770,6 +863,7 @@ struct GpuSolver3::Impl {
   double* h_dt = nullptr;
   int64_t launches = 0, graph_launches = 0;
   int central_grid = 0, cw_grid = 0, mu_grid = 0;
+  bool staged = false;  // lattice-class operators on a type-blocked mesh
   cudaGraphExec_t step_graph = nullptr;
   int graph_rk = -1;
   // per-kernel-group timing (central, detect, weights, flux, gather+RK) with
@@ -797,7 +891,10 @@ struct GpuSolver3::Impl {
     const int nblk = (n + 255) / 256;
     mark(0);
     if (mode == UCFVB_LINEAR || mode == UCFVB_HYBRID) {  // forced CWENOZ solves inside k3_cwenoz
-      kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
+      if (staged)
+        kern.central_staged<<<central_grid, 160, kern.smem_central_staged, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
+      else
+        kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
       ++launches;
     }
     mark(1);
@@ -816,11 +913,17 @@ struct GpuSolver3::Impl {
     }
     mark(2);
     if (mode == UCFVB_HYBRID || mode == UCFVB_CWENOZ) {
-      kern.cwenoz<<<cw_grid, 160, kern.smem_cwenoz, st>>>(D, P, W, Us);
+      if (staged)
+        kern.cwenoz_staged<<<cw_grid, 160, kern.smem_cwenoz_staged, st>>>(D, P, W, Us);
+      else
+        kern.cwenoz<<<cw_grid, 160, kern.smem_cwenoz, st>>>(D, P, W, Us);
       ++launches;
     }
     if (mode == UCFVB_HYBRID || mode == UCFVB_MUSCL) {
-      kern.muscl<<<mu_grid, 160, kern.smem_muscl, st>>>(D, P, W, Us);
+      if (staged)
+        kern.muscl_staged<<<mu_grid, 160, kern.smem_muscl_staged, st>>>(D, P, W, Us);
+      else
+        kern.muscl<<<mu_grid, 160, kern.smem_muscl, st>>>(D, P, W, Us);
       ++launches;
     }
     mark(3);
@@ -976,15 +1079,18 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     W.bounds = dalloc<double>(static_cast<size_t>(nch) * 32 * 4, I.owned);
     W.raw = dalloc<uint8_t>(n, I.owned);
     W.labels = dalloc<uint8_t>(n, I.owned);
-    W.lists = dalloc<int32_t>(static_cast<size_t>(2) * n, I.owned);
-    W.counters = dalloc<int32_t>(4, I.owned);
+    const bool staged_lists = (nops == m.n_types && m.cell_order == 1 && nops > 1);
+    W.ntl = staged_lists ? nops : 1;
+    W.cap = staged_lists ? n / nops : n;
+    W.lists = dalloc<int32_t>(static_cast<size_t>(2) * W.ntl * W.cap, I.owned);
+    W.counters = dalloc<int32_t>(kCnt0 + 2 * W.ntl, I.owned);
     W.dtmin = dalloc<unsigned long long>(1, I.owned);
     W.dt = dalloc<double>(1, I.owned);
     W.t = dalloc<double>(1, I.owned);
     W.ties = dalloc<unsigned long long>(1, I.owned);
     CK3(cudaMemset(W.fp, 0, sizeof(double) * static_cast<size_t>(I.nF) * NQ * 2 * V5));
     CK3(cudaMemset(W.labels, 0, n));
-    CK3(cudaMemset(W.counters, 0, 4 * sizeof(int32_t)));
+    CK3(cudaMemset(W.counters, 0, (kCnt0 + 2 * W.ntl) * sizeof(int32_t)));
     CK3(cudaMemset(W.ties, 0, sizeof(unsigned long long)));
     I.step_labels = dalloc<uint8_t>(n, I.owned);
     CK3(cudaMemset(I.step_labels, 0, n));
@@ -1007,9 +1113,22 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
       CK3(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, 160, smem));
       return std::max(1, static_cast<int>(std::min<int64_t>(nch, static_cast<int64_t>(sms) * std::max(1, per))));
     };
-    I.central_grid = grid_for(I.kern.central, I.kern.smem_central);
-    I.cw_grid = grid_for(I.kern.cwenoz, I.kern.smem_cwenoz);
-    I.mu_grid = grid_for(I.kern.muscl, I.kern.smem_muscl);
+    I.staged = (nops == m.n_types && m.cell_order == 1 && nops > 1);
+    if (I.staged) {
+      I.central_grid = grid_for(I.kern.central_staged, I.kern.smem_central_staged);
+      I.central_grid = std::max(nops, I.central_grid - I.central_grid % nops);  // block b <-> type b % n_ops
+    } else {
+      I.central_grid = grid_for(I.kern.central, I.kern.smem_central);
+    }
+    if (I.staged) {
+      I.cw_grid = grid_for(I.kern.cwenoz_staged, I.kern.smem_cwenoz_staged);
+      I.cw_grid = std::max(nops, I.cw_grid - I.cw_grid % nops);
+      I.mu_grid = grid_for(I.kern.muscl_staged, I.kern.smem_muscl_staged);
+      I.mu_grid = std::max(nops, I.mu_grid - I.mu_grid % nops);
+    } else {
+      I.cw_grid = grid_for(I.kern.cwenoz, I.kern.smem_cwenoz);
+      I.mu_grid = grid_for(I.kern.muscl, I.kern.smem_muscl);
+    }
     I.reset_errors();
     CK3(cudaStreamSynchronize(I.st));
   } catch (...) {

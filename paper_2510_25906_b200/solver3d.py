@@ -25,7 +25,7 @@ _i32p, _i8p, _dp = P(C.c_int32), P(C.c_int8), P(C.c_double)
 
 class MeshView3(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("kind", "nx", "ny", "nz", "n_types", "n_cells", "n_faces", "nf", "nq",
-                                         "nvc")] + [
+                                         "nvc", "cell_order")] + [
         ("period", C.c_double * 3),
         ("cell_vtx", _dp), ("cell_centroid", _dp), ("cell_volume", _dp), ("cell_h", _dp),
         ("cell_faces", _i32p), ("cell_nbr", _i32p), ("cell_nbr_shift", _i32p), ("cell_side", _i8p),
@@ -130,6 +130,14 @@ class Mesh3:
     @property
     def centroid(self):
         return np.ctypeslib.as_array(self.view.cell_centroid, shape=(self.n_cells, 3))
+
+    def cube_and_type(self):
+        """lattice cube and type of every cell (ucfvb3_mesh_view.cell_order)"""
+        c = np.arange(self.n_cells, dtype=np.int64)
+        nt = self.view.n_types
+        if self.view.cell_order:
+            return ((c >> 5) // nt) * 32 + (c & 31), (c >> 5) % nt
+        return c // nt, c % nt
 
     def arr(self, name, shape, dtype=None):
         a = np.ctypeslib.as_array(getattr(self.view, name), shape=shape)

@@ -69,7 +69,7 @@ def test_linear_exactness(kind, order, jitter, classes):
     P.compute_residual(u)
     fv = P.face_values()
     nq, nf = m.nq, m.nf
-    cube = np.arange(m.n_cells) // (1 if kind == HEX else 6)
+    cube, _ = m.cube_and_type()
     ijk = np.stack([cube % n_c, (cube // n_c) % n_c, cube // (n_c * n_c)], 1)
     inner = np.all((ijk >= 3) & (ijk <= 4), axis=1)
     fq = m.arr("face_qp", (m.n_faces, nq, 3))
@@ -157,3 +157,16 @@ def test_lattice_classes_need_unjittered_mesh():
     assert s.n_ops == 6
     with pytest.raises(A.InvalidArgument):
         Mesh3(2, kind=HEX)
+
+
+def test_blocked_cell_order():
+    """4^3 = 64 cubes of tetrahedra: type-major numbering in blocks of 32 cubes
+    (every 32-cell chunk one type); 5^3 keeps the cube-major numbering."""
+    m = Mesh3(4, kind=TET, order=2)
+    assert m.view.cell_order == 1
+    cube, typ = m.cube_and_type()
+    assert np.array_equal(np.sort(cube * 6 + typ), np.arange(m.n_cells))
+    assert np.all(typ.reshape(-1, 32) == typ.reshape(-1, 32)[:, :1])
+    st = Stencils3(m, 2, lattice_classes=True)
+    assert np.array_equal(st.arr("op_index", (m.n_cells,)), typ)
+    assert Mesh3(5, kind=TET, order=2).view.cell_order == 0

@@ -119,7 +119,8 @@ def test_run_steps_matches_advance():
 
 
 def test_lattice_classes_match_port():
-    m, st, o, u0, gpu, cpu = build(TET, 3, 0.0, IC_RANDOM_PHASE, n=6, classes=True, mode="hybrid", weno_b=1.0)
+    m, st, o, u0, gpu, cpu = build(TET, 3, 0.0, IC_RANDOM_PHASE, n=8, classes=True, mode="hybrid", weno_b=1.0)
+    assert m.view.cell_order == 1  # type-blocked numbering: the staged kernels run
     assert st.n_ops == 6
     gpu.state = u0
     cpu.state = u0.copy()

@@ -198,9 +198,9 @@ def scaled_config(cfg, world):
     return c
 
 
-def build_case(cfg, n_threads=0, world=1):
+def build_case(cfg, n_threads=0, world=1, strong=False):
     from paper_2510_25906_b200.mesh import Mesh, Stencils
-    c = scaled_config(cfg, world)
+    c = CONFIGS[cfg] if strong else scaled_config(cfg, world)
     nq = (c["order"] + 2) // 2
     t0 = time.perf_counter()
     mesh = Mesh.structured_tri(c["nx"], c["ny"], c["rect"], jitter=c["jitter"], seed=SEED, periodic=c["periodic"],
@@ -283,7 +283,8 @@ def run_b200_arm(args):
     cfg = args.config
     c = CONFIGS[cfg]
     threads = max(1, (os.cpu_count() or 1) // max(1, world))
-    mesh, st, u0, setup_s = build_case(cfg, n_threads=threads, world=world)
+    strong = args.scaling == "strong"
+    mesh, st, u0, setup_s = build_case(cfg, n_threads=threads, world=world, strong=strong)
     opts = A.options_from_dict(order=c["order"], mode="hybrid", **c["opts"])
     bcs = make_bcs(c["bcs"])
     sub = None
@@ -433,10 +434,13 @@ def run_b200_arm(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["desc"] + (f"; weak scaling: domain repeated {world}x in y, RCB-partitioned, "
-                                                 f"one {n}-cell block per GPU" if world > 1 else ""),
+            "config": {"workload": c["desc"] + ((f"; strong scaling: the config's mesh RCB-partitioned into {world} "
+                                                  f"subdomains ({n} owned cells on rank 0)" if strong else
+                                                  f"; weak scaling: domain repeated {world}x in y, RCB-partitioned, "
+                                                  f"one {n}-cell block per GPU") if world > 1 else ""),
                        "cells": owned_total, "cells_per_gpu": n, "order": c["order"], "K": K, "M": MM,
                        "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid",
                        "parallelism": f"domain decomposition x{world}, NCCL halo exchange per stage" if world > 1
@@ -625,6 +629,8 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="2", choices=sorted(CONFIGS) + sorted(CONFIGS3))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak (config domain repeated per GPU, default) or strong (the config's mesh split N ways)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -502,14 +502,12 @@ def run_arm_3d(args):
 
     import torch
     rank, world, local = env_rank()
-    if world > 1:
-        if rank == 0:
-            print(json.dumps({"impl": args.impl, "unavailable": "3D configs run on one GPU (no 3D decomposition)"}))
-        return
     cfg = args.config
     c = CONFIGS3[cfg]
     from paper_2510_25906_b200 import _abi as A
     if args.impl == "reference":
+        if rank != 0:
+            return
         rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "20")))
         sample = (f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle restatement "
                   f"oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has {os.cpu_count()} cores")
@@ -521,27 +519,61 @@ def run_arm_3d(args):
                           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
     from paper_2510_25906_b200 import solver3d as S3
+    import torch.distributed as dist
     torch.cuda.set_device(local)
-    threads = os.cpu_count() or 1
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    threads = max(1, (os.cpu_count() or 1) // world)
     mesh, st, u0, setup_s = build_case3(cfg, n_threads=threads)
     opts = A.options_from_dict(order=c["order"], mode=c["mode"], cfl=0.5)
-    solver = S3.Solver3(mesh, opts, st, device=local)
-    n = mesh.n_cells
+    n_global = mesh.n_cells
+    if world == 1:
+        solver = S3.Solver3(mesh, opts, st, device=local)
+        n = mesh.n_cells
+    else:  # strong scaling: the config's mesh RCB-split, NCCL halo exchange every stage
+        from paper_2510_25906_b200.solver import nccl_unique_id
+        t0 = time.perf_counter()
+        sub = S3.Subdomain3(mesh, st, S3.partition_rcb3(mesh, world), world, rank)
+        solver = S3.Solver3.on_subdomain(sub, opts, device=local)
+        ids = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(ids, src=0)
+        solver.attach_nccl(ids[0], rank, world)
+        u0 = sub.local_state(u0)
+        setup_s += time.perf_counter() - t0
+        n = sub.n_local
     stream = torch.cuda.ExternalStream(solver.stream(), device=local)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
     solver.state = u0
     solver.run_steps(args.warmup)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ev0.record(stream)
         solver.run_steps(args.steps)
         ev1.record(stream)
         ev1.synchronize()
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = solver.launch_count()
-    value = n * 3 * args.steps / (ms * 1e-3)
+    value = n_global * 3 * args.steps / (ms * 1e-3)
     census = np.array(solver.census(), dtype=float)
+    if world > 1:
+        tc = torch.tensor(census, device="cuda", dtype=torch.float64)
+        dist.all_reduce(tc)
+        census = tc.cpu().numpy()
     mix = census / census.sum()
     ties = solver.nad_ties()
     # per-kernel-group durations (events between groups, un-graphed stages)
@@ -576,8 +608,8 @@ def run_arm_3d(args):
         e2e_step(i)
     e1.record(stream)
     e1.synchronize()
-    e2e_ms = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - w0))
-    e2e_value = n * 3 * e2e_steps / (e2e_ms * 1e-3)
+    e2e_ms = max_over_ranks(max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - w0)))
+    e2e_value = n_global * 3 * e2e_steps / (e2e_ms * 1e-3)
     kb = kernel_bytes3(st.K, st.M, mesh.nf, mesh.nq, st.MD, not c["classes"])
     names = ["central (reconstruct)", "spread+compaction (detect)", "cwenoz+muscl (weights)", "flux", "gather+RK"]
     if c["mode"] == "cwenoz":
@@ -590,20 +622,25 @@ def run_arm_3d(args):
     achieved = phase_bytes[dom] / phases[dom] / 1e9
     stage_achieved = sum(phase_bytes) / phases.sum() / 1e9
     cpu_baseline = None
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "12")))
         cpu_baseline = {"value": rate, "unit": UNIT, "cores": 1, "kind": "port",
                         "sample": f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle "
                                   f"restatement oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has "
                                   f"{os.cpu_count()} cores"}
+    if rank != 0:
+        dist.destroy_process_group()
+        return
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c["desc"], "cells": n, "order": c["order"], "K": st.K, "M": st.M, "nf": mesh.nf,
+        "config": {"workload": c["desc"] + (f"; strong scaling: RCB-split into {world} subdomains, NCCL halo "
+                                            f"exchange every stage ({n} local cells on rank 0)" if world > 1 else ""),
+                   "cells": n_global, "order": c["order"], "K": st.K, "M": st.M, "nf": mesh.nf,
                    "nq": mesh.nq, "integrator": "SSP-RK3 (3 stages/step)", "mode": c["mode"],
                    "operator_rows": "lattice classes (6 shared rows)" if c["classes"] else "per cell",
-                   "parallelism": "single",
+                   "parallelism": f"domain decomposition x{world}" if world > 1 else "single",
                    "l2": "inputs larger than L2 (face values alone %.0f MB)" % (mesh.n_faces * mesh.nq * 80 / 1e6),
                    "class_mix_last_step": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
                                            "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
@@ -619,6 +656,8 @@ def run_arm_3d(args):
         "cpu_baseline": cpu_baseline,
     }
     print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():

@@ -165,6 +165,30 @@ int64_t ucfvb3_launch_count(const ucfvb3_solver* h);
 /* stream the solver launches on (cudaStream_t as void*) */
 void* ucfvb3_stream(const ucfvb3_solver* h);
 
+/* ---- domain decomposition (1/2/4/8 GPUs; decompose3.cpp) ------------------ */
+/* recursive coordinate bisection of the cell centroids into n_parts parts */
+int32_t ucfvb3_partition_rcb(const ucfvb3_mesh_view* mesh, int32_t n_parts, int32_t* part);
+typedef struct ucfvb3_subdomain ucfvb3_subdomain;
+/* rank `rank`'s owned cells + stencil-depth halo as a self-contained local
+ * mesh/stencil pair; local order [owned | halo grouped by owner] */
+int32_t ucfvb3_subdomain_build(const ucfvb3_mesh_view* mesh, const ucfvb3_stencil_view* stencils,
+                               const int32_t* part, int32_t n_parts, int32_t rank, ucfvb3_subdomain** out);
+int32_t ucfvb3_subdomain_views(const ucfvb3_subdomain* s, ucfvb3_mesh_view* mesh, ucfvb3_stencil_view* stencils);
+int32_t ucfvb3_subdomain_info(const ucfvb3_subdomain* s, int32_t* n_owned, int32_t* n_local, int32_t* n_peers);
+int32_t ucfvb3_subdomain_global_ids(const ucfvb3_subdomain* s, int32_t* gid);
+int32_t ucfvb3_subdomain_peer(const ucfvb3_subdomain* s, int32_t i, int32_t* rank, int32_t* n_send,
+                              int32_t* n_recv, int32_t* recv_begin);
+int32_t ucfvb3_subdomain_send_list(const ucfvb3_subdomain* s, int32_t i, int32_t* local_ids);
+void ucfvb3_subdomain_free(ucfvb3_subdomain* s);
+const char* ucfvb3_decomp_last_error(void);
+/* solver over a subdomain (borrowed; must outlive the solver): RK updates
+ * and census cover the owned cells, errors only owned faces; after
+ * ucfvb3_attach_nccl every stage ends with an NCCL halo exchange and dt is a
+ * min all-reduce, all inside the captured step graph */
+int32_t ucfvb3_create_sub(const ucfvb3_subdomain* sub, const ucfvb_options* opt, int32_t device,
+                          ucfvb3_solver** out);
+int32_t ucfvb3_attach_nccl(ucfvb3_solver* h, const uint8_t unique_id[128], int32_t rank, int32_t world);
+
 #ifdef __cplusplus
 }
 #endif

@@ -440,6 +440,12 @@ static int assemble_fluxes(port3* P, double* out) {
   const int nq = P->nq;
   for (int f = 0; f < P->nF; ++f) {
     double total[NV] = {0, 0, 0, 0, 0};
+    /* subdomain boundary faces (decompose3.cpp: both sides the same halo cell)
+     * carry no flux; they never touch an owned residual */
+    if (P->m.face_left[f] == P->m.face_right[f]) {
+      memcpy(&P->ff[(int64_t)f * NV], total, sizeof total);
+      continue;
+    }
     for (int q = 0; q < nq; ++q) {
       const double* UL = slot_ptr(P, (f * nq + q) * 2);
       const double* UR = slot_ptr(P, (f * nq + q) * 2 + 1);

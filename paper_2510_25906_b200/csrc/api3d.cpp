@@ -4,6 +4,7 @@
 #include <new>
 #include <string>
 
+#include "decompose3.hpp"
 #include "layout.hpp"
 #include "setup3d.hpp"
 #include "solver3d.hpp"
@@ -149,6 +150,24 @@ int32_t ucfvb3_get_census(ucfvb3_solver* h, int64_t out[4]) {
 int32_t ucfvb3_get_nad_ties(ucfvb3_solver* h, int64_t* out) {
   NEED(h);
   return guard3(h, [&] { *out = h->s->nad_ties(); });
+}
+int32_t ucfvb3_create_sub(const ucfvb3_subdomain* sub, const ucfvb_options* opt, int32_t device,
+                          ucfvb3_solver** out) {
+  return guard3(nullptr, [&] {
+    if (!sub || !opt || !out) throw ucfvb::ApiError(UCFVB_INVALID, "null pointer");
+    auto* h = new ucfvb3_solver;
+    try {
+      h->s = new ucfvb::GpuSolver3(sub->mv, sub->sv, *opt, device, sub);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+int32_t ucfvb3_attach_nccl(ucfvb3_solver* h, const uint8_t unique_id[128], int32_t rank, int32_t world) {
+  NEED(h);
+  return guard3(h, [&] { h->s->attach_nccl(unique_id, rank, world); });
 }
 int32_t ucfvb3_set_phase_timing(ucfvb3_solver* h, int32_t on) {
   NEED(h);

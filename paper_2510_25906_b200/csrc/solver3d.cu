@@ -30,6 +30,8 @@
 #include "device_math.cuh"
 #include "layout.hpp"
 #include "solver3d.hpp"
+#include "decompose3.hpp"
+#include "nccl_dl.hpp"
 #include "tma.cuh"
 
 namespace ucfvb {
@@ -121,7 +123,7 @@ __device__ __forceinline__ bool riemann3(bool hll, const double* UL, const doubl
 }
 
 struct Dev3 {
-  int n, nF, n_ops;
+  int n, nF, n_ops, n_owned;
   // per cell, 32-cell AoSoA
   const int32_t* central;  // [M+1]
   const int32_t* nbr;      // [NF]
@@ -139,6 +141,7 @@ struct Dev3 {
   // faces
   const double* fnrm;  // [nF][NQ][3]
   const double* fwa;   // [nF][NQ]
+  const uint8_t* fown; // subdomains: 1 for faces of owned cells (the only ones that may report errors)
 };
 
 struct Phys3 {
@@ -676,6 +679,11 @@ __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
   if (f >= D.nF) return;
   double tot[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool ok = true;
+  if (D.fown && D.fown[f] == 2) {  // subdomain boundary face of a halo cell: no flux, never owned
+#pragma unroll
+    for (int v = 0; v < V5; ++v) W.ff[static_cast<size_t>(f) * V5 + v] = 0.0;
+    return;
+  }
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const double* UL = &W.fp[(static_cast<size_t>(f) * NQ + q) * 2 * V5];
@@ -689,7 +697,7 @@ __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
 #pragma unroll
     for (int v = 0; v < V5; ++v) tot[v] += w * fl[v];
   }
-  if (!ok) atomicMin(&W.counters[kBadFace], f);
+  if (!ok && (!D.fown || D.fown[f] == 1)) atomicMin(&W.counters[kBadFace], f);
 #pragma unroll
   for (int v = 0; v < V5; ++v) W.ff[static_cast<size_t>(f) * V5 + v] = tot[v];
 }
@@ -745,7 +753,7 @@ __global__ void k3_rk54_final(int64_t N, double* u, const double* ub, const doub
 __global__ void __launch_bounds__(256) k3_dt(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double dt = 1e300;
-  if (c < D.n) {
+  if (c < D.n_owned) {
     const double* s = &U[static_cast<size_t>(c) * V5];
     bool ok = s[0] > 0.0;
     if (ok) {
@@ -761,6 +769,13 @@ __global__ void __launch_bounds__(256) k3_dt(Dev3 D, Phys3 P, Work3 W, const dou
   }
   for (int o = 16; o; o >>= 1) dt = smin(dt, __shfl_xor_sync(0xffffffffu, dt, o));
   if ((threadIdx.x & 31) == 0) atomicMin(W.dtmin, static_cast<unsigned long long>(__double_as_longlong(dt)));
+}
+
+// halo exchange: owned values a peer holds as halo, packed in its order
+__global__ void k3_halo_pack(const double* __restrict__ U, const int32_t* __restrict__ idx, int n, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * V5) return;
+  out[i] = U[static_cast<size_t>(idx[i / V5]) * V5 + i % V5];
 }
 
 __global__ void k3_dt_init(Work3 W) { *W.dtmin = static_cast<unsigned long long>(__double_as_longlong(1e300)); }
@@ -863,6 +878,33 @@ struct GpuSolver3::Impl {
   double* h_dt = nullptr;
   int64_t launches = 0, graph_launches = 0;
   int central_grid = 0, cw_grid = 0, mu_grid = 0;
+  // decomposition: owned cells first; NCCL halo exchange after every stage
+  int n_owned = 0;
+  struct DevPeer {
+    int rank, n_send, n_recv, recv_begin;
+    size_t send_off;
+    int32_t* send_idx;
+  };
+  std::vector<DevPeer> peers;
+  double* sendbuf = nullptr;
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+  void exchange(double* buf) {
+    if (!comm || peers.empty()) return;
+    for (const DevPeer& p : peers)
+      if (p.n_send) {
+        k3_halo_pack<<<(p.n_send * V5 + 255) / 256, 256, 0, st>>>(buf, p.send_idx, p.n_send, sendbuf + p.send_off);
+        ++launches;
+      }
+    NK(nccl().GroupStart());
+    for (const DevPeer& p : peers) {
+      if (p.n_send) NK(nccl().Send(sendbuf + p.send_off, V5 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm, st));
+      if (p.n_recv)
+        NK(nccl().Recv(buf + static_cast<size_t>(p.recv_begin) * V5, V5 * static_cast<size_t>(p.n_recv), ncclDouble,
+                       p.rank, comm, st));
+    }
+    NK(nccl().GroupEnd());
+  }
   bool staged = false;  // lattice-class operators on a type-blocked mesh
   cudaGraphExec_t step_graph = nullptr;
   int graph_rk = -1;
@@ -931,8 +973,9 @@ struct GpuSolver3::Impl {
     kern.flux<<<(nF + 127) / 128, 128, 0, st>>>(D, P, W);
     mark(4);
     kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine);
-    mark(5);
     launches += 2;
+    if (combine && out) exchange(out);
+    mark(5);
     collect();
   }
 
@@ -956,11 +999,13 @@ struct GpuSolver3::Impl {
     const int64_t N = static_cast<int64_t>(n) * V5;
     k3_rk54_final<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(N, U, ub, uc, rhs3, ud, rhs, W.dt);
     ++launches;
+    exchange(U);
   }
 
   void dt_kernels(bool advance_time) {
     k3_dt_init<<<1, 1, 0, st>>>(W);
     k3_dt<<<(n + 255) / 256, 256, 0, st>>>(D, P, W, U);
+    if (comm) NK(nccl().AllReduce(W.dtmin, W.dtmin, 1, ncclUint64, ncclMin, comm, st));  // positive doubles order as bits
     k3_dt_finalize<<<1, 1, 0, st>>>(W, o.cfl, advance_time ? 1 : 0);
     launches += 3;
   }
@@ -981,7 +1026,8 @@ struct GpuSolver3::Impl {
   }
 };
 
-GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device)
+GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device,
+                       const ucfvb3_subdomain* sub)
     : p_(new Impl) {
   Impl& I = *p_;
   try {
@@ -1019,6 +1065,27 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     };
     Dev3& D = I.D;
     D.n = n, D.nF = I.nF, D.n_ops = nops;
+    I.n_owned = D.n_owned = sub ? sub->n_owned : n;
+    D.fown = nullptr;
+    if (sub) {
+      std::vector<uint8_t> fo(I.nF, 0);
+      for (int f = 0; f < I.nF; ++f)
+        fo[f] = m.face_left[f] == m.face_right[f] ? 2 : ((m.face_left[f] < I.n_owned || m.face_right[f] < I.n_owned) ? 1 : 0);
+      uint8_t* d = dalloc<uint8_t>(fo.size(), I.owned);
+      up(d, fo);
+      D.fown = d;
+      size_t off = 0;
+      for (const auto& pr : sub->peers) {
+        Impl::DevPeer dp{pr.rank, static_cast<int>(pr.send.size()), pr.n_recv, pr.recv_begin, off, nullptr};
+        if (dp.n_send) {
+          dp.send_idx = dalloc<int32_t>(pr.send.size(), I.owned);
+          up(dp.send_idx, pr.send);
+        }
+        off += static_cast<size_t>(dp.n_send) * V5;
+        I.peers.push_back(dp);
+      }
+      I.sendbuf = dalloc<double>(std::max<size_t>(off, 1), I.owned);
+    }
     D.central = upload_ao(s.central, n, M + 1);
     D.nbr = upload_ao(m.cell_nbr, n, NF);
     D.slot = upload_ao(s.qp_slot, n, Q);
@@ -1148,6 +1215,7 @@ GpuSolver3::~GpuSolver3() {
   if (I.st) cudaStreamSynchronize(I.st);
   for (auto& e : I.ev)
     if (e) cudaEventDestroy(e);
+  if (I.comm) nccl().CommDestroy(I.comm);
   for (void* q : I.owned) cudaFree(q);
   if (I.h_counters) cudaFreeHost(I.h_counters);
   if (I.h_dt) cudaFreeHost(I.h_dt);
@@ -1276,7 +1344,20 @@ void GpuSolver3::census(int64_t out[4]) {
   std::vector<uint8_t> l(p_->n);
   get_labels(1, l.data());
   for (int i = 0; i < 4; ++i) out[i] = 0;
-  for (uint8_t x : l) ++out[x & 3];
+  for (int c = 0; c < p_->n_owned; ++c) ++out[l[c] & 3];  // owned cells (the whole mesh on one domain)
+}
+
+void GpuSolver3::attach_nccl(const uint8_t id[128], int rank, int world) {
+  Impl& I = *p_;
+  CK3(cudaSetDevice(I.device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof u);
+  if (I.comm) NK(nccl().CommDestroy(I.comm));
+  I.comm = nullptr;
+  NK(nccl().CommInitRank(&I.comm, world, u, rank));
+  I.world = world, I.rank = rank;
+  if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
+  I.step_graph = nullptr;
 }
 
 int64_t GpuSolver3::nad_ties() {

@@ -11,7 +11,9 @@ namespace ucfvb {
 
 class GpuSolver3 {
  public:
-  GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device);
+  GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, const ucfvb_options& o, int device,
+             const ucfvb3_subdomain* sub = nullptr);
+  void attach_nccl(const uint8_t id[128], int rank, int world);
   ~GpuSolver3();
   GpuSolver3(const GpuSolver3&) = delete;
   GpuSolver3& operator=(const GpuSolver3&) = delete;

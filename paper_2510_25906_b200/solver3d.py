@@ -74,6 +74,18 @@ def lib():
             "ucfvb3_get_census": (C.c_int32, [H, P(C.c_int64)]),
             "ucfvb3_get_nad_ties": (C.c_int32, [H, P(C.c_int64)]),
             "ucfvb3_launch_count": (C.c_int64, [H]),
+            "ucfvb3_partition_rcb": (C.c_int32, [P(MeshView3), C.c_int32, _i32p]),
+            "ucfvb3_subdomain_build": (C.c_int32, [P(MeshView3), P(StencilView3), _i32p, C.c_int32, C.c_int32,
+                                                   P(H)]),
+            "ucfvb3_subdomain_views": (C.c_int32, [H, P(MeshView3), P(StencilView3)]),
+            "ucfvb3_subdomain_info": (C.c_int32, [H, _i32p, _i32p, _i32p]),
+            "ucfvb3_subdomain_global_ids": (C.c_int32, [H, _i32p]),
+            "ucfvb3_subdomain_peer": (C.c_int32, [H, C.c_int32, _i32p, _i32p, _i32p, _i32p]),
+            "ucfvb3_subdomain_send_list": (C.c_int32, [H, C.c_int32, _i32p]),
+            "ucfvb3_subdomain_free": (None, [H]),
+            "ucfvb3_decomp_last_error": (C.c_char_p, []),
+            "ucfvb3_create_sub": (C.c_int32, [H, P(A.Options), C.c_int32, P(H)]),
+            "ucfvb3_attach_nccl": (C.c_int32, [H, P(C.c_uint8), C.c_int32, C.c_int32]),
             "ucfvb3_set_phase_timing": (C.c_int32, [H, C.c_int32]),
             "ucfvb3_get_phase_times": (C.c_int32, [H, _dp]),
             "ucfvb3_stream": (C.c_void_p, [H]),
@@ -172,6 +184,70 @@ class Stencils3:
         return np.ctypeslib.as_array(getattr(self.view, name), shape=shape)
 
 
+def _ckd(rc):
+    if rc != A.OK:
+        raise A.error_for(rc, lib().ucfvb3_decomp_last_error().decode())
+
+
+def partition_rcb3(mesh: Mesh3, n_parts: int) -> np.ndarray:
+    """recursive coordinate bisection of the cell centroids into n_parts parts"""
+    part = np.zeros(mesh.n_cells, dtype=np.int32)
+    _ckd(lib().ucfvb3_partition_rcb(C.byref(mesh.view), int(n_parts), part.ctypes.data_as(_i32p)))
+    return part
+
+
+class Peer3:
+    def __init__(self, rank, send, recv_begin, n_recv):
+        self.rank, self.send, self.recv_begin, self.n_recv = rank, send, recv_begin, n_recv
+
+
+class Subdomain3:
+    """Rank `rank`'s owned cells + stencil-depth halo (csrc/decompose3.cpp) as
+    a local mesh/stencil pair; local order [owned | halo grouped by owner].
+    Keeps the global mesh and stencils alive (lattice-class rows are borrowed)."""
+
+    def __init__(self, mesh: Mesh3, stencils: Stencils3, part, n_parts: int, rank: int):
+        self._keep = (mesh, stencils)
+        part = np.ascontiguousarray(part, dtype=np.int32)
+        h = C.c_void_p()
+        _ckd(lib().ucfvb3_subdomain_build(C.byref(mesh.view), C.byref(stencils.view), part.ctypes.data_as(_i32p),
+                                          int(n_parts), int(rank), C.byref(h)))
+        self._h = h
+        self.rank, self.n_parts = rank, n_parts
+        self.mesh_view, self.stencil_view = MeshView3(), StencilView3()
+        _ckd(lib().ucfvb3_subdomain_views(h, C.byref(self.mesh_view), C.byref(self.stencil_view)))
+        no, nl, npr = C.c_int32(), C.c_int32(), C.c_int32()
+        _ckd(lib().ucfvb3_subdomain_info(h, C.byref(no), C.byref(nl), C.byref(npr)))
+        self.n_owned, self.n_local = no.value, nl.value
+        self.gid = np.zeros(self.n_local, dtype=np.int32)
+        _ckd(lib().ucfvb3_subdomain_global_ids(h, self.gid.ctypes.data_as(_i32p)))
+        self.peers = []
+        for i in range(npr.value):
+            r, ns, nr, rb = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+            _ckd(lib().ucfvb3_subdomain_peer(h, i, C.byref(r), C.byref(ns), C.byref(nr), C.byref(rb)))
+            send = np.zeros(ns.value, dtype=np.int32)
+            if ns.value:
+                _ckd(lib().ucfvb3_subdomain_send_list(h, i, send.ctypes.data_as(_i32p)))
+            self.peers.append(Peer3(r.value, send, rb.value, nr.value))
+        # a Mesh3-like facade for the port and the solver
+        self.view = self.mesh_view
+        self.n_cells, self.n_faces = self.n_local, self.mesh_view.n_faces
+        self.nf, self.nq = self.mesh_view.nf, self.mesh_view.nq
+
+    def local_state(self, u_global):
+        return np.ascontiguousarray(u_global[self.gid])
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().ucfvb3_subdomain_free(self._h)
+            self._h = None
+
+
+class _StencilFacade:
+    def __init__(self, view):
+        self.view = view
+
+
 class Solver3:
     """ucfv::Solver API (solver.hpp:52-100) for the 3D stage pass on one GPU."""
 
@@ -181,6 +257,22 @@ class Solver3:
         self.n = mesh.n_cells
         _ck(lib().ucfvb3_create(C.byref(mesh.view), C.byref(stencils.view), C.byref(opt), device, C.byref(h)))
         self._h = h
+
+    @classmethod
+    def on_subdomain(cls, sub: "Subdomain3", opt: A.Options, device=0):
+        """Solver over a Subdomain3: census and errors cover owned cells;
+        attach_nccl adds the per-stage halo exchange and the dt all-reduce."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        self.mesh, self.stencils, self.sub = sub, _StencilFacade(sub.stencil_view), sub
+        self.n = sub.n_local
+        _ck(lib().ucfvb3_create_sub(sub._h, C.byref(opt), device, C.byref(h)))
+        self._h = h
+        return self
+
+    def attach_nccl(self, unique_id: bytes, rank: int, world: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        _ck(lib().ucfvb3_attach_nccl(self._h, buf, rank, world), self._h)
 
     def close(self):
         if getattr(self, "_h", None):

@@ -178,3 +178,69 @@ def test_larger_mesh_parity_and_conservation(kind, order, n, classes):
     tot0 = (u0 * m.volume[:, None]).sum(0)
     tot = (gpu.state * m.volume[:, None]).sum(0)
     assert np.all(np.abs(tot - tot0) <= 1e-13 * np.abs(u0).max() * m.volume.sum())
+
+
+class GpuRank3:
+    def __init__(self, sub, opts):
+        self.g = Solver3.on_subdomain(sub, opts)
+        self.sub = sub
+        self.last_census = np.zeros(4, dtype=np.int64)
+
+    def max_stable_dt(self, u):
+        self.g.state = u
+        return self.g.max_stable_dt()
+
+    def residual(self, u, t, first):
+        return self.g.compute_residual(u, t)
+
+    def record_census(self):
+        self.last_census = np.bincount(self.g.labels()[: self.sub.n_owned], minlength=4)
+
+
+@pytest.mark.parametrize("name", ["hex-p2-blast", "tet-p2-classes"])
+@pytest.mark.parametrize("n_parts", [2, 4])
+def test_gpu_subdomains_match_single_domain3(name, n_parts):
+    from paper_2510_25906_b200.solver3d import Subdomain3, partition_rcb3
+    from tests.decomp_driver import local_exchange, run_rk3
+    from tests.test_decompose3 import setup3
+
+    c, m, st, o, u0 = setup3(name)
+    single = Solver3(m, o, st)
+    single.state = u0
+    t_ref, cen_ref = 0.0, []
+    for _ in range(2):
+        dt = single.max_stable_dt()
+        single.advance(dt, t_ref)
+        t_ref += dt
+        cen_ref.append(single.census())
+    part = partition_rcb3(m, n_parts)
+    subs = [Subdomain3(m, st, part, n_parts, r) for r in range(n_parts)]
+    ranks = [GpuRank3(s, o) for s in subs]
+    states = [s.local_state(u0) for s in subs]
+    t, census = run_rk3(ranks, subs, states, 2, local_exchange, min)
+    assert t == t_ref
+    out = np.zeros_like(u0)
+    for s, u in zip(subs, states):
+        out[s.gid[: s.n_owned]] = u[: s.n_owned]
+    np.testing.assert_array_equal(out, single.state)
+    for a, b in zip(census, cen_ref):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_nccl_single_rank_path3():
+    from paper_2510_25906_b200.solver import nccl_unique_id
+    from paper_2510_25906_b200.solver3d import Subdomain3, partition_rcb3
+    from tests.test_decompose3 import setup3
+
+    c, m, st, o, u0 = setup3("hex-p2-blast")
+    sub = Subdomain3(m, st, partition_rcb3(m, 1), 1, 0)
+    g = Solver3.on_subdomain(sub, o)
+    g.attach_nccl(nccl_unique_id(), 0, 1)
+    g.state = sub.local_state(u0)
+    plain = Solver3(m, o, st)
+    plain.state = u0
+    t1 = g.run_steps(3)
+    t2 = plain.run_steps(3)
+    assert t1 == t2
+    np.testing.assert_array_equal(g.state[np.argsort(sub.gid)], plain.state)
+    assert g.census() == plain.census()

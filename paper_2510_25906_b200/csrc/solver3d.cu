@@ -185,7 +185,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
                                            const double* phs = nullptr) {
   constexpr int Q = NF * NQ;
   constexpr int QG = (Q % 4 == 0) ? 4 : ((Q % 3 == 0) ? 3 : 1);  // independent fma chains in flight
-  for (int q0 = 0; q0 < Q; q0 += QG) {
+  auto group = [&](int q0) {
     int gs[QG];  // this group's slots (issued before the fma chains)
 #pragma unroll
     for (int j = 0; j < QG; ++j) gs[j] = sl ? sl[q0 + j] : D.slot[ao(c, q0 + j, Q)];
@@ -214,6 +214,15 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
       sval[q0 + j][v][lane] = val[j];
       if (chk) viol = smax(viol, smax(blo - val[j], val[j] - bhi));
     }
+  };
+  // p = 3: fully unrolled (the slot array stays in registers); p <= 2: rolled
+  // (measured faster there: fewer live registers, slots from L1-resident stack)
+  if (K >= 19) {
+#pragma unroll
+    for (int q0 = 0; q0 < Q; q0 += QG) group(q0);
+  } else {
+#pragma unroll 1
+    for (int q0 = 0; q0 < Q; q0 += QG) group(q0);
   }
 }
 
@@ -519,6 +528,7 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     for (int k = 0; k < K; ++k) p1[k] /= P.lam0;
     // SI_0 = p1' OI p1 (row then dot) and the directional SI from the 3x3 block
     double si0 = 0.0;
+#pragma unroll
     for (int k = 0; k < K; ++k) {
       double t = 0.0;
 #pragma unroll

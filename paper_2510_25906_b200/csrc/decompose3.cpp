@@ -163,7 +163,7 @@ ucfvb3_subdomain* build_subdomain3(const ucfvb3_mesh_view& m, const ucfvb3_stenc
       const size_t gi = g * nf + i, li = static_cast<size_t>(l) * nf + i;
       D->cell_faces[li] = lface[m.cell_faces[gi]];
       const int x = lid[m.cell_nbr[gi]];
-      D->cell_nbr[li] = (classify[g] && x >= 0) ? x : (x >= 0 ? x : l);
+      D->cell_nbr[li] = x >= 0 ? x : l;  // classification cells have every neighbour local
       for (int d = 0; d < 3; ++d) D->cell_nbr_shift[li * 3 + d] = m.cell_nbr_shift[gi * 3 + d];
       D->cell_side[li] = m.cell_side[gi];
     }

@@ -392,9 +392,9 @@ def run_b200_arm(args):
     e2e_steps = args.steps
 
     def e2e_step(i):
-        rc = lib.ucfvb_set_state(solver._h, hptr[i & 1])
-        rc |= lib.ucfvb_run_steps(solver._h, 1, A.RK3, 0.0, float("inf"), C.byref(t_dev), None)
-        rc |= lib.ucfvb_get_state(solver._h, hptr[(i + 1) & 1])
+        # the host-state call: H2D of this step's input, one RK3 step (device
+        # dt), D2H of the result, one synchronisation (include/ucfvb.h)
+        rc = lib.ucfvb_advance_host(solver._h, hptr[i & 1], hptr[(i + 1) & 1], 1, A.RK3, 0.0, C.byref(t_dev))
         if rc:
             raise RuntimeError(lib.ucfvb_last_error(solver._h).decode())
 

@@ -221,6 +221,14 @@ int32_t ucfvb_compute_residual(ucfvb_solver* h, const double* u, double t, doubl
 int32_t ucfvb_run_steps(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end,
                         double* t_out, int64_t* census_out);
 
+/* Host state in, host state out: u_in -> n_steps steps of ucfvb_run_steps
+ * (dt = max_stable_dt() each step) -> u_out, with a single synchronisation
+ * (state() + the advance loop of run_simulation, run.cpp:96-132, for callers
+ * that keep the state on the host). u_in / u_out ([n_cells][4]) should be
+ * pinned for asynchronous PCIe transfers; u_out may alias u_in. On failure the
+ * device state is the failing step's input (as ucfvb_run_steps). */
+int32_t ucfvb_advance_host(ucfvb_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
+                           double t0, double* t_out);
 /* ucfvb_run_steps plus each step's dt (run.cpp:99-112 CensusRow::dt): dt_out
  * (nullable) receives [n_steps] doubles; step k's end time is t0 + dt_0 + ...
  * + dt_k summed in step order, exactly as run_simulation's `t += dt`. */

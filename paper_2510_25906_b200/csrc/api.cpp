@@ -161,6 +161,13 @@ int32_t ucfvb_run_steps(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0,
     if (t_out) *t_out = t;
   });
 }
+int32_t ucfvb_advance_host(ucfvb_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
+                           double t0, double* t_out) {
+  return guard(h, [&] {
+    const double t = h->s->advance_host(u_in, u_out, n_steps, rk, t0);
+    if (t_out) *t_out = t;
+  });
+}
 int32_t ucfvb_run_steps_log(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end, double* t_out,
                             int64_t* census_out, double* dt_out) {
   return guard(h, [&] {

@@ -500,6 +500,7 @@ struct GpuSolver::Impl {
   }
 
   int err_step = 0;
+  char* host_stage = nullptr;  // pinned DtState + error word for advance_host
   int read_error(int* kind, int* face, int* cell) {
     int e[4];
     CK(cudaMemcpyAsync(e, S.err, sizeof e, cudaMemcpyDeviceToHost, stream));
@@ -741,6 +742,7 @@ GpuSolver::~GpuSolver() {
   for (void* p : I.owned) cudaFree(p);
   if (I.census_dev) cudaFree(I.census_dev);
   if (I.dtlog_dev) cudaFree(I.dtlog_dev);
+  if (I.host_stage) cudaFreeHost(I.host_stage);
   for (auto& e : I.ev)
     if (e) cudaEventDestroy(e);
   if (I.stream) cudaStreamDestroy(I.stream);
@@ -939,6 +941,56 @@ double GpuSolver::run_impl(int n_steps, int rk, double t0, double t_end, bool un
   I.stage_is_first = false;
   CK(cudaStreamSynchronize(I.stream));
   return h.t + h.dt;
+}
+
+// Everything is enqueued before the single synchronisation: H2D of the state,
+// the dt-state reset (from pinned staging), the step graphs, the error word
+// and dt-state read-back (pinned) and the D2H of the result. u_in / u_out
+// should be pinned host memory for truly asynchronous PCIe transfers.
+double GpuSolver::advance_host(const double* u_in, double* u_out, int n_steps, int rk, double t0) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance_host: unknown integrator");
+  if (n_steps <= 0) throw ApiError(UCFVB_INVALID, "advance_host: n_steps must be >= 1");
+  if (!I.host_stage) CK(cudaMallocHost(&I.host_stage, sizeof(DtState) + 4 * sizeof(int)));
+  auto* hs = reinterpret_cast<DtState*>(I.host_stage);
+  int* he = reinterpret_cast<int*>(I.host_stage + sizeof(DtState));
+  const size_t bytes = sizeof(double4) * I.L.n;
+  CK(cudaMemcpyAsync(I.ubuf[I.cur], u_in, bytes, cudaMemcpyHostToDevice, I.stream));
+  *hs = DtState{};
+  hs->dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);  // bits of 1e300
+  hs->t = t0;
+  hs->step = -1;
+  hs->t_end = INFINITY;
+  hs->cfl = I.opt.cfl;
+  CK(cudaMemcpyAsync(I.ds, hs, sizeof(DtState), cudaMemcpyHostToDevice, I.stream));
+  I.S.step = &I.ds->step;
+  const int cur0 = I.cur;
+  int64_t nl = I.launch_dt_reduce(I.ubuf[I.cur]);
+  for (int s = 0; s < n_steps; ++s) {
+    if (I.opt.use_graphs && !I.timing) {
+      cudaGraphExec_t g = I.get_graph(rk, true, I.cur);
+      CK(cudaGraphLaunch(g, I.stream));
+      nl += I.graph_launches[rk][1][I.cur];
+    } else {
+      nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], false);
+    }
+    I.cur ^= 1;
+  }
+  I.launches = nl;
+  I.S.step = I.step_zero;
+  I.allreduce_error();
+  CK(cudaMemcpyAsync(he, I.S.err, 4 * sizeof(int), cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaMemcpyAsync(hs, I.ds, sizeof(DtState), cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaMemcpyAsync(u_out, I.ubuf[I.cur], bytes, cudaMemcpyDeviceToHost, I.stream));
+  CK(cudaStreamSynchronize(I.stream));
+  CK(cudaGetLastError());
+  I.stage_is_first = false;
+  if (he[0]) {
+    const int failed = std::min(std::max(0, he[3]), n_steps - 1);
+    I.cur = (cur0 + failed) & 1;
+    I.raise_device_error(he[0], he[1], he[2]);
+  }
+  return hs->t + hs->dt;
 }
 
 void GpuSolver::get_labels(uint8_t* out, bool step) {

@@ -26,6 +26,9 @@ class GpuSolver {
   void advance(double dt, double t, int rk);                         // solver.cpp:381-387
   void compute_residual(const double* u, double t, double* out);     // solver.cpp:316-379
   double run_steps(int n_steps, int rk, double t0, double t_end, int64_t* census, double* dt_out = nullptr);
+  // host state in -> n_steps graph-replayed steps -> host state out, with one
+  // synchronisation (the host-buffer form of state() + advance loop)
+  double advance_host(const double* u_in, double* u_out, int n_steps, int rk, double t0);
   // run_simulation's loop condition (run.cpp:96): steps while t < t_end - 1e-14 t_end, at most max_steps
   double run_until(int max_steps, int rk, double t0, double t_end, int64_t* census, double* dt_out, int* n_done);  // run.cpp:97-132
 

@@ -139,6 +139,14 @@ class Solver:
                                            cen.ctypes.data_as(A.c_i64p) if census else None))
         return t.value, cen
 
+    def advance_host(self, u_in, n_steps: int = 1, rk: int = A.RK3, t0: float = 0.0, u_out=None):
+        """host state in -> n_steps steps (device dt) -> host state out, one synchronisation"""
+        u_in = np.ascontiguousarray(u_in, dtype=np.float64).reshape(self.n_cells, 4)
+        out = np.empty_like(u_in) if u_out is None else u_out
+        t = C.c_double()
+        self._ck(self._lib.ucfvb_advance_host(self._h, _dp(u_in), _dp(out), n_steps, rk, t0, C.byref(t)))
+        return out, t.value
+
     def run_log(self, n_steps: int, rk: int = A.RK3, t0: float = 0.0, t_end: float = float("inf")):
         """run_steps that also returns each step's dt: (t, census[n,4], dt[n])."""
         t = C.c_double()

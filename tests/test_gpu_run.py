@@ -125,3 +125,29 @@ def test_run_simulation_phase_timing_rows(tmp_path):
     assert res.steps >= 3 and len(lines) == 1 + res.steps
     vals = np.array([[float(x) for x in ln.split(",")] for ln in lines[1:]])
     assert np.all(vals[:, 2:] > 0.0) and np.all(np.diff(vals[:, 1]) > 0.0)
+
+
+def test_advance_host_matches_run_steps():
+    """ucfvb_advance_host (host state in/out, one synchronisation) is the same
+    computation as set_state + run_steps + get_state."""
+    import numpy as np
+    from paper_2510_25906_b200 import _abi as A
+    from paper_2510_25906_b200.mesh import Mesh, Stencils
+    from paper_2510_25906_b200.solver import Solver
+
+    mesh = Mesh.structured_tri(24, 24, (0.0, 0.0, 1.0, 1.0), jitter=0.1, seed=1, periodic="both", n_qp=2)
+    st = Stencils(mesh, 2)
+    o = A.options_from_dict(order=2, mode="hybrid", lambda1p=1e3, cfl=0.5)
+    u0 = mesh.project_initial(2, [0.5, 0.5, 0.01], seed=3, degree=4)
+    a = Solver(mesh, o, stencils=st)
+    out, t = a.advance_host(u0, 3)
+    b = Solver(mesh, o, stencils=st)
+    b.state = u0
+    t2, _ = b.run_steps(3, A.RK3)
+    assert t == t2
+    np.testing.assert_array_equal(out, b.state)
+    bad = u0.copy()
+    bad[5, 0] = -1.0
+    import pytest
+    with pytest.raises(A.NonPhysicalError):
+        a.advance_host(bad, 1)

@@ -611,9 +611,7 @@ def run_arm_3d(args):
     tt = C.c_double()
 
     def e2e_step(i):
-        rc = L.ucfvb3_set_state(solver._h, hp[i & 1])
-        rc |= L.ucfvb3_run_steps(solver._h, 1, 0.0, A.RK3, C.byref(tt))
-        rc |= L.ucfvb3_get_state(solver._h, hp[(i + 1) & 1])
+        rc = L.ucfvb3_advance_host(solver._h, hp[i & 1], hp[(i + 1) & 1], 1, A.RK3, 0.0, C.byref(tt))
         if rc:
             raise RuntimeError(L.ucfvb3_last_error(solver._h).decode())
 

@@ -147,6 +147,10 @@ int32_t ucfvb3_advance(ucfvb3_solver* h, double dt, double t, int32_t rk);
  * (run_simulation's loop, run.cpp:92-139, without a host round trip); the
  * final time is returned in *t_out. */
 int32_t ucfvb3_run_steps(ucfvb3_solver* h, int32_t n_steps, double t0, int32_t rk, double* t_out);
+/* host state in ([n_cells][5], pinned for async copies) -> n_steps steps
+ * -> host state out, one synchronisation (as ucfvb_advance_host) */
+int32_t ucfvb3_advance_host(ucfvb3_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
+                            double t0, double* t_out);
 int32_t ucfvb3_compute_residual(ucfvb3_solver* h, const double* u, double t, double* out);
 /* which = 0: labels of the last stage; 1: step labels (first stage of the last step) */
 int32_t ucfvb3_get_labels(ucfvb3_solver* h, int32_t which, uint8_t* out);

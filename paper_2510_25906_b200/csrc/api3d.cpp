@@ -131,6 +131,14 @@ int32_t ucfvb3_run_steps(ucfvb3_solver* h, int32_t n_steps, double t0, int32_t r
     if (t_out) *t_out = t;
   });
 }
+int32_t ucfvb3_advance_host(ucfvb3_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
+                            double t0, double* t_out) {
+  NEED(h);
+  return guard3(h, [&] {
+    const double t = h->s->advance_host(u_in, u_out, n_steps, rk, t0);
+    if (t_out) *t_out = t;
+  });
+}
 int32_t ucfvb3_compute_residual(ucfvb3_solver* h, const double* u, double t, double* out) {
   NEED(h);
   return guard3(h, [&] { h->s->compute_residual(u, t, out); });

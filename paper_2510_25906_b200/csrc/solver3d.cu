@@ -1020,6 +1020,25 @@ struct GpuSolver3::Impl {
     launches += 3;
   }
 
+  // one RK step (device dt, time advance) captured as a CUDA graph
+  void capture(int rk) {
+    if (step_graph) cudaGraphExecDestroy(step_graph);
+    step_graph = nullptr;
+    cudaGraph_t g = nullptr;
+    const int64_t before = launches;
+    CK3(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    dt_kernels(false);
+    step(rk);
+    k3_time_add<<<1, 1, 0, st>>>(W);
+    ++launches;
+    CK3(cudaStreamEndCapture(st, &g));
+    CK3(cudaGraphInstantiate(&step_graph, g, 0));
+    CK3(cudaGraphDestroy(g));
+    graph_launches = launches - before;
+    launches = before;
+    graph_rk = rk;
+  }
+
   void reset_errors() {
     const int32_t init[2] = {0x7fffffff, 0x7fffffff};
     CK3(cudaMemcpyAsync(W.counters + 2, init, sizeof init, cudaMemcpyHostToDevice, st));
@@ -1284,29 +1303,50 @@ double GpuSolver3::run_steps(int n_steps, double t0, int rk) {
     I.check_errors();
     return I.h_dt[0];
   }
-  if (!I.step_graph || I.graph_rk != rk) {
-    if (I.step_graph) cudaGraphExecDestroy(I.step_graph);
-    I.step_graph = nullptr;
-    cudaGraph_t g = nullptr;
-    const int64_t before = I.launches;
-    CK3(cudaStreamBeginCapture(I.st, cudaStreamCaptureModeThreadLocal));
-    I.dt_kernels(false);
-    I.step(rk);
-    k3_time_add<<<1, 1, 0, I.st>>>(I.W);
-    ++I.launches;
-    CK3(cudaStreamEndCapture(I.st, &g));
-    CK3(cudaGraphInstantiate(&I.step_graph, g, 0));
-    CK3(cudaGraphDestroy(g));
-    I.graph_launches = I.launches - before;
-    I.launches = before;
-    I.graph_rk = rk;
-  }
+  if (!I.step_graph || I.graph_rk != rk) I.capture(rk);
   for (int i = 0; i < n_steps; ++i) {
     CK3(cudaGraphLaunch(I.step_graph, I.st));
     I.launches += I.graph_launches;
   }
   CK3(cudaMemcpyAsync(I.h_dt, I.W.t, sizeof(double), cudaMemcpyDeviceToHost, I.st));
   I.check_errors();
+  return I.h_dt[0];
+}
+
+// host state in -> n_steps graph-replayed steps -> host state out, one synchronisation
+double GpuSolver3::advance_host(const double* u_in, double* u_out, int n_steps, int rk, double t0) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance_host: unknown integrator");
+  if (n_steps <= 0) throw ApiError(UCFVB_INVALID, "advance_host: n_steps must be >= 1");
+  CK3(cudaSetDevice(I.device));
+  const size_t bytes = sizeof(double) * static_cast<size_t>(I.n) * V5;
+  CK3(cudaMemcpyAsync(I.U, u_in, bytes, cudaMemcpyHostToDevice, I.st));
+  const int32_t init[2] = {0x7fffffff, 0x7fffffff};
+  std::memcpy(I.h_counters + 2, init, sizeof init);
+  I.h_dt[1] = t0;
+  CK3(cudaMemcpyAsync(I.W.counters + 2, I.h_counters + 2, sizeof init, cudaMemcpyHostToDevice, I.st));
+  CK3(cudaMemcpyAsync(I.W.t, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
+  if (!I.timing && (!I.step_graph || I.graph_rk != rk)) I.capture(rk);
+  for (int i = 0; i < n_steps; ++i) {
+    if (I.timing) {
+      I.dt_kernels(false);
+      I.step(rk);
+      k3_time_add<<<1, 1, 0, I.st>>>(I.W);
+      ++I.launches;
+    } else {
+      CK3(cudaGraphLaunch(I.step_graph, I.st));
+      I.launches += I.graph_launches;
+    }
+  }
+  CK3(cudaMemcpyAsync(I.h_dt, I.W.t, sizeof(double), cudaMemcpyDeviceToHost, I.st));
+  CK3(cudaMemcpyAsync(I.h_counters, I.W.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, I.st));
+  CK3(cudaMemcpyAsync(u_out, I.U, bytes, cudaMemcpyDeviceToHost, I.st));
+  CK3(cudaStreamSynchronize(I.st));
+  CK3(cudaGetLastError());
+  if (I.h_counters[kBadFace] != 0x7fffffff)
+    throw ApiError(UCFVB_NONPHYSICAL, "non-physical state at face " + std::to_string(I.h_counters[kBadFace]));
+  if (I.h_counters[kBadCell] != 0x7fffffff)
+    throw ApiError(UCFVB_NONPHYSICAL, "non-physical state in cell " + std::to_string(I.h_counters[kBadCell]));
   return I.h_dt[0];
 }
 

@@ -69,6 +69,7 @@ def lib():
             "ucfvb3_advance": (C.c_int32, [H, C.c_double, C.c_double, C.c_int32]),
             "ucfvb3_run_steps": (C.c_int32, [H, C.c_int32, C.c_double, C.c_int32, _dp]),
             "ucfvb3_compute_residual": (C.c_int32, [H, _dp, C.c_double, _dp]),
+            "ucfvb3_advance_host": (C.c_int32, [H, _dp, _dp, C.c_int32, C.c_int32, C.c_double, _dp]),
             "ucfvb3_get_labels": (C.c_int32, [H, C.c_int32, P(C.c_uint8)]),
             "ucfvb3_get_face_values": (C.c_int32, [H, _dp]),
             "ucfvb3_get_census": (C.c_int32, [H, P(C.c_int64)]),
@@ -304,6 +305,15 @@ class Solver3:
         t = C.c_double()
         _ck(lib().ucfvb3_run_steps(self._h, n_steps, t0, rk, C.byref(t)), self._h)
         return t.value
+
+    def advance_host(self, u_in, n_steps=1, rk=A.RK3, t0=0.0, u_out=None):
+        """host state in -> n_steps steps (device dt) -> host state out, one synchronisation"""
+        u_in = np.ascontiguousarray(u_in, dtype=np.float64).reshape(self.n, NV)
+        out = np.empty_like(u_in) if u_out is None else u_out
+        t = C.c_double()
+        _ck(lib().ucfvb3_advance_host(self._h, u_in.ctypes.data_as(_dp), out.ctypes.data_as(_dp), n_steps, rk, t0,
+                                      C.byref(t)), self._h)
+        return out, t.value
 
     def compute_residual(self, u, t=0.0):
         u = np.ascontiguousarray(u, dtype=np.float64)

@@ -267,3 +267,17 @@ def test_configured_step_count_reduced_mesh(cfg, n, steps):
     l1g = (np.abs(gpu.state) * m.volume[:, None]).sum(0)
     l1c = (np.abs(cpu.state) * m.volume[:, None]).sum(0)
     assert np.all(np.abs(l1g - l1c) <= 1e-8 * np.abs(l1c).max())
+
+
+def test_advance_host_matches_run_steps3():
+    m, st, o, u0, gpu, cpu = build(TET, 2, 0.05, IC_BLAST, mode="hybrid")
+    out, t = gpu.advance_host(u0, 3)
+    g2 = Solver3(m, o, st)
+    g2.state = u0
+    t2 = g2.run_steps(3)
+    assert t == t2
+    np.testing.assert_array_equal(out, g2.state)
+    bad = u0.copy()
+    bad[3, 0] = -1.0
+    with pytest.raises(A.NonPhysicalError):
+        gpu.advance_host(bad, 1)

@@ -287,10 +287,10 @@ __global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, cons
     const int cc = act ? c : (D.n - 1);
     const int op = D.opi[cc];
     if (D.n_ops == D.n && threadIdx.x == 0 && ch + static_cast<int>(gridDim.x) < nch) {
-      // per-cell operator rows of this block's next chunk -> L2 (TMA prefetch)
+      // this block's next chunk's pinv rows and stencil ids -> L2 (TMA prefetch;
+      // measured: prefetching phi as well thrashes L2 and is slower)
       const int nx = ch + gridDim.x;
       bulk_prefetch_l2(D.pinv + static_cast<size_t>(nx) * M * K * 32, M * K * 32 * 8);
-      bulk_prefetch_l2(D.phi + static_cast<size_t>(nx) * Q * K * 32, Q * K * 32 * 8);
       bulk_prefetch_l2(D.central + static_cast<size_t>(nx) * (M + 1) * 32, (M + 1) * 32 * 4);
     }
     // every stencil and neighbour value of this (cell, variable) in flight at

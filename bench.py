@@ -594,6 +594,18 @@ def run_arm_3d(args):
         tc = torch.tensor(census, device="cuda", dtype=torch.float64)
         dist.all_reduce(tc)
         census = tc.cpu().numpy()
+    # NAD class fractions per step (BASELINE config 5 asks for them), from the
+    # initial state, outside the timed region
+    per_step = []
+    solver.state = u0
+    for _ in range(min(args.steps, 10)):
+        solver.run_steps(1)
+        cs = np.array(solver.census(), dtype=float)
+        if world > 1:
+            tc = torch.tensor(cs, device="cuda", dtype=torch.float64)
+            dist.all_reduce(tc)
+            cs = tc.cpu().numpy()
+        per_step.append([round(float(x), 4) for x in cs / cs.sum()])
     mix = census / census.sum()
     ties = solver.nad_ties()
     # per-kernel-group durations (events between groups, un-graphed stages)
@@ -673,6 +685,7 @@ def run_arm_3d(args):
                    "l2": "inputs larger than L2 (face values alone %.0f MB)" % (mesh.n_faces * mesh.nq * 80 / 1e6),
                    "class_mix_last_step": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
                                            "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
+                   "class_mix_per_step_LCMF": per_step,
                    "nad_ties": int(ties), "setup_s": round(setup_s, 2)},
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 40)},

@@ -487,9 +487,15 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
       for (int m = 0; m < M; ++m) cp_async8(&xs[m * 160 + threadIdx.x], &U[static_cast<size_t>(id[m]) * V5 + v]);
       cp_async_commit();
     }
-    int sl[NF * NQ];  // face-point slots, loaded while the gather is in flight
+    // face-point slots, loaded while the gather is in flight (p <= 2; for p = 3
+    // per face-point group: register pressure)
+    constexpr bool kHoist = K * M <= 200;
+    int slh[kHoist ? NF * NQ : 1];
+    if (kHoist) {
 #pragma unroll
-    for (int q = 0; q < NF * NQ; ++q) sl[q] = D.slot[ao(c, q, NF * NQ)];
+      for (int q = 0; q < (kHoist ? NF * NQ : 0); ++q) slh[q] = D.slot[ao(c, q, NF * NQ)];
+    }
+    const int* sl = kHoist ? slh : nullptr;
     cp_async_wait_all();
     double p1[K];
 #pragma unroll
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     om0 /= wsum;
 #pragma unroll
     for (int s = 0; s < NF; ++s) om[s] /= wsum;
-    double bl[K];
+    double* bl = p1;  // blended in place (same operations; saves K registers)
 #pragma unroll
     for (int k = 0; k < K; ++k) bl[k] = om0 * p1[k];
 #pragma unroll
@@ -623,9 +629,15 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
       cp_async_commit();
     }
-    int sl[NF * NQ];  // face-point slots, loaded while the gather is in flight
+    // face-point slots, loaded while the gather is in flight (p <= 2; for p = 3
+    // per face-point group: register pressure)
+    constexpr bool kHoist = K * M <= 200;
+    int slh[kHoist ? NF * NQ : 1];
+    if (kHoist) {
 #pragma unroll
-    for (int q = 0; q < NF * NQ; ++q) sl[q] = D.slot[ao(c, q, NF * NQ)];
+      for (int q = 0; q < (kHoist ? NF * NQ : 0); ++q) slh[q] = D.slot[ao(c, q, NF * NQ)];
+    }
+    const int* sl = kHoist ? slh : nullptr;
     cp_async_wait_all();
     double l0 = 0.0, l1 = 0.0, l2 = 0.0;
 #pragma unroll

@@ -58,7 +58,6 @@ typedef struct port3 {
   int n, nF, nf, nq, Q, K, M, MD;
   double *dofs, *fp, *ff, *bounds, *thr, *eps2;
   uint8_t *labels, *step_labels;
-  int stage_is_first;
   int64_t bad_face;
   double *ua, *ub, *uc, *ud, *rhs, *rhs3;
 } port3;
@@ -475,7 +474,10 @@ static int assemble_fluxes(port3* P, double* out) {
 }
 
 /* compute_residual (solver.cpp:316-379) */
-int port3_compute_residual(port3* P, const double* u, double t, double* out) {
+/* one stage; `first` = first stage of a step (stage_is_first_, solver.cpp:371-374):
+ * with detect_every_stage = 0 the later stages keep the labels and only
+ * refresh the bounds (solver.cpp:343-361) */
+static int stage3(port3* P, const double* u, double t, double* out, int first) {
   (void)t;
   const int n = P->n, K = P->K, mode = P->o.mode;
   if (mode == UCFVB_FIRST) memset(P->labels, UCFVB_SCHEME_FIRST, (size_t)n);
@@ -487,18 +489,23 @@ int port3_compute_residual(port3* P, const double* u, double t, double* out) {
       solve_dofs(P, c, u, dofs);
       if (mode != UCFVB_CWENOZ) evaluate_cell(P, u, c, dofs);
     }
-  if (mode == UCFVB_HYBRID) classify_cells(P, u);
+  if (mode == UCFVB_HYBRID) {
+    if (first || P->o.detect_every_stage)
+      classify_cells(P, u);
+    else
+      for (int c = 0; c < n; ++c) cell_bounds(P, u, c, &P->bounds[(int64_t)c * 4]);
+  }
   if (mode != UCFVB_LINEAR) {
     const int rc = apply_troubled(P, u);
     if (rc) return rc;
   }
   if (mode == UCFVB_HYBRID) fallback_check(P, u);
-  if (P->stage_is_first) {
-    memcpy(P->step_labels, P->labels, (size_t)n);
-    P->stage_is_first = 0;
-  }
+  if (first) memcpy(P->step_labels, P->labels, (size_t)n);
   return assemble_fluxes(P, out);
 }
+
+/* compute_residual (solver.cpp:316-379) called on its own: a first stage */
+int port3_compute_residual(port3* P, const double* u, double t, double* out) { return stage3(P, u, t, out, 1); }
 
 /* max_stable_dt (solver.cpp:103-111) */
 int port3_max_stable_dt(port3* P, const double* u, double* out) {
@@ -526,13 +533,12 @@ static void combine2(int64_t n, double* out, double wa, const double* ua, double
 int port3_advance(port3* P, double* u, double dt, double t, int rk) {
   const int64_t n = P->n;
   int rc;
-  P->stage_is_first = 1;
   if (rk == UCFVB_RK3) {
-    if ((rc = port3_compute_residual(P, u, t, P->rhs))) return rc;
+    if ((rc = stage3(P, u, t, P->rhs, 1))) return rc;
     combine2(n, P->ua, 1.0, u, 0.0, u, 1.0, P->rhs, dt);
-    if ((rc = port3_compute_residual(P, P->ua, t + dt, P->rhs))) return rc;
+    if ((rc = stage3(P, P->ua, t + dt, P->rhs, 0))) return rc;
     combine2(n, P->ub, 0.75, u, 0.25, P->ua, 0.25, P->rhs, dt);
-    if ((rc = port3_compute_residual(P, P->ub, t + 0.5 * dt, P->rhs))) return rc;
+    if ((rc = stage3(P, P->ub, t + 0.5 * dt, P->rhs, 0))) return rc;
     combine2(n, u, 1.0 / 3.0, u, 2.0 / 3.0, P->ub, 2.0 / 3.0, P->rhs, dt);
     return 0;
   }
@@ -542,15 +548,15 @@ int port3_advance(port3* P, double* u, double dt, double t, int rk) {
   const double b40 = 0.178079954393132, b43 = 0.821920045606868, a43 = 0.544974750228521;
   const double c52 = 0.517231671970585, c53 = 0.096059710526147, a53 = 0.063692468666290;
   const double c54 = 0.386708617503269, a54 = 0.226007483236906;
-  if ((rc = port3_compute_residual(P, u, t, P->rhs))) return rc;
+  if ((rc = stage3(P, u, t, P->rhs, 1))) return rc;
   combine2(n, P->ua, 1.0, u, 0.0, u, a10, P->rhs, dt);
-  if ((rc = port3_compute_residual(P, P->ua, t, P->rhs))) return rc;
+  if ((rc = stage3(P, P->ua, t, P->rhs, 0))) return rc;
   combine2(n, P->ub, b20, u, b21, P->ua, a21, P->rhs, dt);
-  if ((rc = port3_compute_residual(P, P->ub, t, P->rhs))) return rc;
+  if ((rc = stage3(P, P->ub, t, P->rhs, 0))) return rc;
   combine2(n, P->uc, b30, u, b32, P->ub, a32, P->rhs, dt);
-  if ((rc = port3_compute_residual(P, P->uc, t, P->rhs3))) return rc;
+  if ((rc = stage3(P, P->uc, t, P->rhs3, 0))) return rc;
   combine2(n, P->ud, b40, u, b43, P->uc, a43, P->rhs3, dt);
-  if ((rc = port3_compute_residual(P, P->ud, t, P->rhs))) return rc;
+  if ((rc = stage3(P, P->ud, t, P->rhs, 0))) return rc;
   for (int64_t i = 0; i < NV * n; ++i)
     u[i] = c52 * P->ub[i] + c53 * P->uc[i] + a53 * dt * P->rhs3[i] + c54 * P->ud[i] + a54 * dt * P->rhs[i];
   return 0;
@@ -586,7 +592,6 @@ int port3_create(const ucfvb3_mesh_view* m, const ucfvb3_stencil_view* s, const 
   P->step_labels = (uint8_t*)calloc((size_t)n, 1);
   double** ws[] = {&P->ua, &P->ub, &P->uc, &P->ud, &P->rhs, &P->rhs3};
   for (int i = 0; i < 6; ++i) *ws[i] = (double*)calloc((size_t)n * NV, sizeof(double));
-  P->stage_is_first = 1;
   P->bad_face = -1;
   *out = P;
   return 0;

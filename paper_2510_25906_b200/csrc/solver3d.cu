@@ -395,7 +395,9 @@ __device__ __forceinline__ int sev_of(int s) { return s == 0 ? 0 : (s == 1 ? 1 :
 
 // ---- spread + lists (hybrid detection stage) ------------------------------------------
 template <int NF, int NQ>
-__global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* __restrict__ U) {
+// detect = 0: frozen classification (detect_every_stage = false, later stages
+// of a step): the labels stay as the previous stage left them (solver.cpp:343-361)
+__global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* __restrict__ U, int detect) {
   constexpr int Q = NF * NQ;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
@@ -403,12 +405,17 @@ __global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* 
   bool ok = c < D.n;
   if (ok) {
     const int r = W.raw[c];
-    int sev = r & 3;
+    if (detect) {
+      int sev = r & 3;
 #pragma unroll
-    for (int i = 0; i < NF; ++i) sev = max(sev, static_cast<int>(W.raw[D.nbr[ao(c, i, NF)]] & 3));
-    lab = sev == 0 ? UCFVB_SCHEME_LINEAR : (sev == 1 ? UCFVB_SCHEME_CWENOZ : UCFVB_SCHEME_MUSCL);
-    if (lab == UCFVB_SCHEME_LINEAR && (r >> 2)) {
-      // fallback_check demotes the Linear candidate: first-order values (solver.cpp:256-262)
+      for (int i = 0; i < NF; ++i) sev = max(sev, static_cast<int>(W.raw[D.nbr[ao(c, i, NF)]] & 3));
+      lab = sev == 0 ? UCFVB_SCHEME_LINEAR : (sev == 1 ? UCFVB_SCHEME_CWENOZ : UCFVB_SCHEME_MUSCL);
+    } else {
+      lab = W.labels[c];
+    }
+    if ((lab == UCFVB_SCHEME_LINEAR && (r >> 2)) || lab == UCFVB_SCHEME_FIRST) {
+      // fallback_check demotes the Linear candidate (solver.cpp:256-262), or a
+      // frozen FirstOrder label (apply_troubled's constant branch): first-order values
       lab = UCFVB_SCHEME_FIRST;
       for (int q = 0; q < Q; ++q) {
         double* dst = &W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5];
@@ -815,7 +822,7 @@ struct Kern3 {
   size_t smem_central, smem_cwenoz, smem_muscl, smem_central_staged;
   void (*central)(Dev3, Phys3, Work3, const double*, int, int);
   void (*central_staged)(Dev3, Phys3, Work3, const double*, int, int);
-  void (*spread)(Dev3, Work3, const double*);
+  void (*spread)(Dev3, Work3, const double*, int);
   void (*cwenoz)(Dev3, Phys3, Work3, const double*);
   void (*muscl)(Dev3, Phys3, Work3, const double*);
   void (*cwenoz_staged)(Dev3, Phys3, Work3, const double*);
@@ -963,7 +970,7 @@ struct GpuSolver3::Impl {
     }
     mark(1);
     if (nad) {
-      kern.spread<<<nblk, 256, 0, st>>>(D, W, Us);
+      kern.spread<<<nblk, 256, 0, st>>>(D, W, Us, (first || o.detect_every_stage) ? 1 : 0);
       ++launches;
     } else if (mode == UCFVB_CWENOZ || mode == UCFVB_MUSCL) {
       k3_fill_list<<<nblk, 256, 0, st>>>(n, mode == UCFVB_CWENOZ ? kCwList : kMuList,
@@ -1075,8 +1082,6 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     if (m.n_cells != s.n_cells || m.nf != s.nf || m.nq != s.nq || s.MD != MD3)
       throw ApiError(UCFVB_INVALID, "solver3d: stencils do not match the mesh");
     if (o.mode < UCFVB_LINEAR || o.mode > UCFVB_FIRST) throw ApiError(UCFVB_INVALID, "solver3d: unknown mode");
-    if (!o.detect_every_stage && o.mode == UCFVB_HYBRID)
-      throw ApiError(UCFVB_UNSUPPORTED, "solver3d: frozen detection (detect_every_stage = 0) is 2D-only");
     if (!(o.lambda1p > 1.0)) throw ApiError(UCFVB_INVALID, "cwenoz: central linear weight lambda1' must exceed 1");
     if (o.margins.alpha_m < 0.0 || o.margins.beta_m < 0.0)
       throw ApiError(UCFVB_INVALID, "NAD margins: alpha_m and beta_m must be non-negative");

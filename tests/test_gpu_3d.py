@@ -47,6 +47,7 @@ CASES = [
     (HEX, 2, 0.0, IC_TGV, "linear", {}),
     (TET, 2, 0.0, IC_BLAST, "first", {}),
     (HEX, 2, 0.05, IC_BLAST, "hybrid", {"weno_b": 1.0}),
+    (TET, 2, 0.05, IC_BLAST, "hybrid", {"detect_every_stage": 0, "weno_b": 1.0}),
 ]
 
 
@@ -75,7 +76,7 @@ def test_stage_parity(kind, order, jitter, ic, mode, extra):
     assert gpu.nad_ties() == 0
 
 
-@pytest.mark.parametrize("kind,order,jitter,ic,mode,extra", CASES[:8])
+@pytest.mark.parametrize("kind,order,jitter,ic,mode,extra", CASES[:8] + CASES[-1:])
 def test_rk3_steps(kind, order, jitter, ic, mode, extra):
     m, st, o, u0, gpu, cpu = build(kind, order, jitter, ic, mode=mode, **extra)
     gpu.state = u0

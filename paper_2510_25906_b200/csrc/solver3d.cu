@@ -263,7 +263,7 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // chunks of type b % 6 and stages that type's pinv and phi rows in shared
 // memory once, read as broadcast 16-byte loads
 template <int K, int M, int NF, int NQ, bool STAGED>
-__global__ void __launch_bounds__(160) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
+__global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
   constexpr int G = M + NF;  // stencil members + face neighbours

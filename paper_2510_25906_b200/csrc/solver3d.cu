@@ -605,7 +605,8 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
 template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
-  constexpr int G = M + NF;
+  constexpr int H1 = M / 2, H2 = M - H1 + NF;  // the two gathers
+  constexpr int G = H2;
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
@@ -626,14 +627,14 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    // two gathers of H1 and H2 values (all of each in flight), so the gather
+    // buffer fits inside the face-value buffer: twice the resident blocks
     {
-      int id[G];
+      int id[H1];
 #pragma unroll
-      for (int m = 0; m < M; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
+      for (int m = 0; m < H1; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
 #pragma unroll
-      for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(c, i, NF)];
-#pragma unroll
-      for (int g = 0; g < G; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      for (int g = 0; g < H1; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
       cp_async_commit();
     }
     // face-point slots, loaded while the gather is in flight (p <= 2; for p = 3
@@ -647,9 +648,31 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     const int* sl = kHoist ? slh : nullptr;
     cp_async_wait_all();
     double l0 = 0.0, l1 = 0.0, l2 = 0.0;
+    double xv[H1];  // first half consumed into registers before the buffer is reused
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const double x = xs[m * 160 + threadIdx.x] - u0;
+    for (int m = 0; m < H1; ++m) xv[m] = xs[m * 160 + threadIdx.x];
+    {
+      int id[H2];
+#pragma unroll
+      for (int m = H1; m < M; ++m) id[m - H1] = D.central[ao(c, m + 1, M + 1)];
+#pragma unroll
+      for (int i = 0; i < NF; ++i) id[M - H1 + i] = D.nbr[ao(c, i, NF)];
+      __syncwarp();
+#pragma unroll
+      for (int g = 0; g < H2; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      cp_async_commit();
+    }
+#pragma unroll
+    for (int m = 0; m < H1; ++m) {
+      const double x = xv[m] - u0;
+      l0 = __fma_rn((STAGED ? sp[0 * M + m] : D.pinv_lin[ao(op, 0 * M + m, 3 * M)]), x, l0);
+      l1 = __fma_rn((STAGED ? sp[1 * M + m] : D.pinv_lin[ao(op, 1 * M + m, 3 * M)]), x, l1);
+      l2 = __fma_rn((STAGED ? sp[2 * M + m] : D.pinv_lin[ao(op, 2 * M + m, 3 * M)]), x, l2);
+    }
+    cp_async_wait_all();
+#pragma unroll
+    for (int m = H1; m < M; ++m) {
+      const double x = xs[(m - H1) * 160 + threadIdx.x] - u0;
       l0 = __fma_rn((STAGED ? sp[0 * M + m] : D.pinv_lin[ao(op, 0 * M + m, 3 * M)]), x, l0);
       l1 = __fma_rn((STAGED ? sp[1 * M + m] : D.pinv_lin[ao(op, 1 * M + m, 3 * M)]), x, l1);
       l2 = __fma_rn((STAGED ? sp[2 * M + m] : D.pinv_lin[ao(op, 2 * M + m, 3 * M)]), x, l2);
@@ -657,7 +680,7 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
-      const double x = xs[(M + i) * 160 + threadIdx.x];
+      const double x = xs[(M - H1 + i) * 160 + threadIdx.x];
       lo = smin(lo, x);
       hi = smax(hi, x);
     }
@@ -839,7 +862,7 @@ Kern3 kern3() {
   Kern3 k{};
   k.smem_central = smem3_bytes(M + NF, Q);
   k.smem_cwenoz = smem3_bytes(M, Q);
-  k.smem_muscl = smem3_bytes(M + NF, Q);
+  k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   k.smem_central_staged = k.smem_central + 8 * static_cast<size_t>(M * K + Q * K);
   k.smem_cwenoz_staged = k.smem_cwenoz + 8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K) +
                          4 * static_cast<size_t>(NF * MD3);

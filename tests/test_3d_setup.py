@@ -170,3 +170,34 @@ def test_blocked_cell_order():
     st = Stencils3(m, 2, lattice_classes=True)
     assert np.array_equal(st.arr("op_index", (m.n_cells,)), typ)
     assert Mesh3(5, kind=TET, order=2).view.cell_order == 0
+
+
+def test_solver3_argument_validation_without_gpu():
+    """ucfvb3_create validates its arguments before touching the device (the
+    reference's constructor / cwenoz_blend_scalar exceptions): lambda1' <= 1,
+    bad margins, an unknown mode, and a stencil set of another mesh."""
+    from paper_2510_25906_b200.solver3d import Solver3
+    m = Mesh3(4, kind=HEX, order=2)
+    st = Stencils3(m, 2)
+    for kw in (dict(lambda1p=1.0), dict(margins=(-1.0, 0.5, 0.0, 0.0, 5.0, 2.0)), dict(mode=7),
+               dict(margins=(1e-4, 0.5, 1e-3, 0.6, 5.0, 2.0))):
+        o = A.options_from_dict(order=2, **kw)
+        with pytest.raises(A.InvalidArgument):
+            Solver3(m, o, st)
+    other = Mesh3(5, kind=HEX, order=2)
+    with pytest.raises(A.InvalidArgument):
+        Solver3(other, A.options_from_dict(order=2), st)
+
+
+def test_mesh3_and_stencils3_argument_errors():
+    with pytest.raises(A.InvalidArgument):
+        Mesh3(4, kind=7)
+    with pytest.raises(A.InvalidArgument):
+        Mesh3(4, kind=HEX, order=0)
+    with pytest.raises(A.InvalidArgument):
+        Mesh3(4, kind=HEX, jitter=0.3)
+    m = Mesh3(4, kind=HEX, order=2)
+    with pytest.raises(A.InvalidArgument):
+        Stencils3(m, 1)  # the mesh face rule was built for order 2 (2x2 points; order 1 needs 1)
+    with pytest.raises(A.InvalidArgument):
+        m.project_initial(99, [1.0])

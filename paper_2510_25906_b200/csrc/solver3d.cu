@@ -170,6 +170,17 @@ __device__ __forceinline__ int32_t* list_of(const Work3& W, int L, int t) {
 }
 
 
+// fp64 tensor-core tile D(8x8) += A(8x4) B(4x8) (DMMA). Measured on B200
+// (scripts/dmma_order.cu, profiles/dmma_order.json): every element equals the
+// sequential chain fma(a3,b3,fma(a2,b2,fma(a1,b1,fma(a0,b0,c)))), i.e. the
+// oracle's fma accumulation in k order, so tensor-core solves stay bit-exact.
+// Fragments (lane l): a = A[l/4][l%4], b = B[l%4][l/4], d = D[l/4][2(l%4) + {0,1}].
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // dynamic shared memory of the reconstruction kernels: the cp.async stencil
 // gather [G][160] and, after the solve, the face values [Q][5][33] (union)
 __host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
@@ -270,7 +281,12 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
-  double* sp = smem3 + smem3_bytes(G, Q) / 8;  // STAGED: pinv row [M][K] then phi row [Q][K]
+  // STAGED: pinv row [M][K], phi row [Q][K] and the centre values [5][32] past the union buffer
+  constexpr size_t kUnion = (STAGED && K >= 8) ? ((smem3_bytes(G, Q) / 8 > static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
+                                                      ? smem3_bytes(G, Q) / 8
+                                                      : static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
+                                               : smem3_bytes(G, Q) / 8;
+  double* sp = smem3 + kUnion;
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
@@ -326,26 +342,129 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
     double a[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) a[k] = 0.0;
-    double2 w = make_double2(0.0, 0.0);
+    if constexpr (STAGED && K >= 8) {
+      // the block's 32 cells share one operator row: the K x M solve of warp v
+      // (variable v) is the GEMM a(K x 32) = pinv(K x M) . dU(M x 32) on the
+      // fp64 tensor cores, m in k-steps of 4 (the oracle's fma order)
+      constexpr int MT = (K + 7) / 8, KS = (M + 3) / 4;
+      double* su0 = sp + M * K + Q * K;  // [5][32] centre values
+      su0[threadIdx.x] = u0;
+      __syncthreads();  // every thread's gather landed (fragments read other lanes' columns)
+      double dacc[MT][4][2];
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const double x = xs[m * 160 + threadIdx.x] - u0;
-      if (STAGED) {
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const int e = m * K + k;
-          if ((e & 1) == 0) w = reinterpret_cast<const double2*>(sp)[e >> 1];
-          a[k] = __fma_rn((e & 1) ? w.y : w.x, x, a[k]);
+        for (int t = 0; t < 4; ++t) dacc[i][t][0] = dacc[i][t][1] = 0.0;
+      const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int m = 4 * ks + fc;
+        double af[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int k = 8 * i + fr;
+          af[i] = (k < K && m < M) ? sp[m * K + k] : 0.0;
         }
-      } else {
 #pragma unroll
-        for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
+        for (int t = 0; t < 4; ++t) {
+          const int cl = 8 * t + fr;
+          const double bf = m < M ? xs[m * 160 + v * 32 + cl] - su0[v * 32 + cl] : 0.0;
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma884(dacc[i][t][0], dacc[i][t][1], af[i], bf);
+        }
+      }
+      __syncthreads();  // gather buffer consumed: it carries the dofs back to their lanes
+      double* sd = xs + Q * V5 * 33;  // [5][K][32], past the face-value buffer
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int k = 8 * i + fr;
+          if (k < K) {
+            sd[(v * K + k) * 32 + 8 * t + 2 * fc] = dacc[i][t][0];
+            sd[(v * K + k) * 32 + 8 * t + 2 * fc + 1] = dacc[i][t][1];
+          }
+        }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) a[k] = sd[(v * K + k) * 32 + lane];
+    } else {
+      double2 w = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const double x = xs[m * 160 + threadIdx.x] - u0;
+        if (STAGED) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) {
+            const int e = m * K + k;
+            if ((e & 1) == 0) w = reinterpret_cast<const double2*>(sp)[e >> 1];
+            a[k] = __fma_rn((e & 1) ? w.y : w.x, x, a[k]);
+          }
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
+        }
       }
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
     const bool chk = (v == 0 || v == 4);
     double viol = -1e300;
-    if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl, STAGED ? sp + M * K : nullptr);
+    if constexpr (STAGED && K >= 8) {
+      if (eval) {
+        // face values of warp v's 32 cells: F(Q x 32) = u0 + phi(Q x K) . a(K x 32) on
+        // the tensor cores, k in steps of 4 from C = u0 (evaluate_cell's fma order)
+        constexpr int QT = (Q + 7) / 8, KS2 = (K + 3) / 4;
+        const double* sd = xs + Q * V5 * 33;
+        const double* sph = sp + M * K;
+        const double* su0 = sp + M * K + Q * K;
+        const int fr = lane >> 2, fc = lane & 3;
+        double f[QT][4][2];
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            f[i][t][0] = su0[v * 32 + 8 * t + 2 * fc];
+            f[i][t][1] = su0[v * 32 + 8 * t + 2 * fc + 1];
+          }
+#pragma unroll
+        for (int ks = 0; ks < KS2; ++ks) {
+          const int k = 4 * ks + fc;
+          double af[QT];
+#pragma unroll
+          for (int i = 0; i < QT; ++i) {
+            const int q = 8 * i + fr;
+            af[i] = (q < Q && k < K) ? sph[q * K + k] : 0.0;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const double bf = k < K ? sd[(v * K + k) * 32 + 8 * t + fr] : 0.0;
+#pragma unroll
+            for (int i = 0; i < QT; ++i) dmma884(f[i][t][0], f[i][t][1], af[i], bf);
+          }
+        }
+        const int cb = ch << 5;
+#pragma unroll
+        for (int i = 0; i < QT; ++i)
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int q = 8 * i + fr, cl = 8 * t + 2 * fc + j;
+              if (q < Q) {
+                sval[q][v][cl] = f[i][t][j];
+                if (cb + cl < D.n) W.fp[static_cast<size_t>(D.slot[ao(cb + cl, q, Q)]) * V5 + v] = f[i][t][j];
+              }
+            }
+        __syncthreads();  // every face value of the block in sval
+        if (chk)
+          for (int q = 0; q < Q; ++q) {
+            const double val = sval[q][v][lane];
+            viol = smax(viol, smax(lo - val, val - hi));
+          }
+      }
+    } else {
+      if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl, STAGED ? sp + M * K : nullptr);
+    }
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
       const int t = v == 0 ? 0 : 1;
@@ -863,7 +982,9 @@ Kern3 kern3() {
   k.smem_central = smem3_bytes(M + NF, Q);
   k.smem_cwenoz = smem3_bytes(M, Q);
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
-  k.smem_central_staged = k.smem_central + 8 * static_cast<size_t>(M * K + Q * K);
+  // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
+  k.smem_central_staged = std::max(k.smem_central, 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32)) +
+                          8 * static_cast<size_t>(M * K + Q * K + 160);
   k.smem_cwenoz_staged = k.smem_cwenoz + 8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K) +
                          4 * static_cast<size_t>(NF * MD3);
   k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);

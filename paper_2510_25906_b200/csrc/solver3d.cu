@@ -577,12 +577,20 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
   constexpr int EP = M * K, ED = NF * 3 * MD3, EO = (K * K + 1) & ~1;  // region sizes (even: phi is read as double2)
+  // DM: lattice-class chunks (one operator row per block) run the central
+  // solve and the face evaluation on the fp64 tensor cores (see k3_central)
+  constexpr bool DM = STAGED && K >= 8;
+  constexpr size_t kU0 = smem3_bytes(G, Q) / 8, kU1 = static_cast<size_t>(Q * V5 * 33 + V5 * K * 32);
+  constexpr size_t kUnion = (DM && kU1 > kU0) ? kU1 : kU0;
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
-  // STAGED: this block's lattice type's rows: pinv | pinv_dir | OI | phi | dir members
-  double* sp = smem3 + smem3_bytes(G, Q) / 8;
-  int* sdm = reinterpret_cast<int*>(sp + EP + ED + EO + Q * K);
+  double* sd = xs + Q * V5 * 33;  // DM: dofs [5][K][32] past the face values
+  // STAGED: this block's lattice type's rows: pinv | pinv_dir | OI | phi | (DM: centre values [5][32]) | dir members
+  double* sp = smem3 + kUnion;
+  double* su0 = sp + EP + ED + EO + Q * K;
+  int* sdm = reinterpret_cast<int*>(su0 + (DM ? 160 : 0));
+  int* scell = sdm + NF * MD3;  // DM: the chunk's cells
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int t = STAGED ? blockIdx.x % W.ntl : 0;
@@ -626,12 +634,18 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     double p1[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) p1[k] = 0.0;
+    if constexpr (!DM) {
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const double x = xs[m * 160 + threadIdx.x] - u0;
+      for (int m = 0; m < M; ++m) {
+        const double x = xs[m * 160 + threadIdx.x] - u0;
 #pragma unroll
-      for (int k = 0; k < K; ++k)
-        p1[k] = __fma_rn(STAGED ? sp[m * K + k] : D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
+        for (int k = 0; k < K; ++k)
+          p1[k] = __fma_rn(STAGED ? sp[m * K + k] : D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
+      }
+    } else {
+      su0[threadIdx.x] = u0;
+      if (v == 0) scell[lane] = act ? c : -1;
+      __syncthreads();  // every gather landed and the centre values are shared
     }
     double dir[NF][3];
 #pragma unroll
@@ -649,6 +663,48 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
                          x[m], acc);
         dir[s][k] = acc;
       }
+    }
+    const int fr = lane >> 2, fc = lane & 3;
+    if constexpr (DM) {
+      // central solve p1(K x 32) = pinv(K x M) . dU(M x 32) for warp v's variable
+      constexpr int MT = (K + 7) / 8, KS = (M + 3) / 4;
+      double dacc[MT][4][2];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) dacc[i][tt][0] = dacc[i][tt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const int m = 4 * ks + fc;
+        double af[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int k = 8 * i + fr;
+          af[i] = (k < K && m < M) ? sp[m * K + k] : 0.0;
+        }
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const int cl = 8 * tt + fr;
+          const double bf = m < M ? xs[m * 160 + v * 32 + cl] - su0[v * 32 + cl] : 0.0;
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma884(dacc[i][tt][0], dacc[i][tt][1], af[i], bf);
+        }
+      }
+      __syncthreads();  // the gather buffer is dead: the dofs travel through sd
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const int k = 8 * i + fr;
+          if (k < K) {
+            sd[(v * K + k) * 32 + 8 * tt + 2 * fc] = dacc[i][tt][0];
+            sd[(v * K + k) * 32 + 8 * tt + 2 * fc + 1] = dacc[i][tt][1];
+          }
+        }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) p1[k] = sd[(v * K + k) * 32 + lane];
+      __syncwarp();
     }
 #pragma unroll
     for (int s = 0; s < NF; ++s) {
@@ -713,9 +769,61 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    __syncthreads();  // the gather buffer becomes the face-value buffer
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
-                          STAGED ? sp + EP + ED + EO : nullptr);
+    if constexpr (DM) {
+      // face values F(Q x 32) = u0 + phi(Q x K) . bl(K x 32) on the tensor cores
+      constexpr int QT = (Q + 7) / 8, KS2 = (K + 3) / 4;
+#pragma unroll
+      for (int k = 0; k < K; ++k) sd[(v * K + k) * 32 + lane] = bl[k];
+      __syncwarp();
+      const double* sph = sp + EP + ED + EO;
+      double f[QT][4][2];
+#pragma unroll
+      for (int i = 0; i < QT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          f[i][tt][0] = su0[v * 32 + 8 * tt + 2 * fc];
+          f[i][tt][1] = su0[v * 32 + 8 * tt + 2 * fc + 1];
+        }
+#pragma unroll
+      for (int ks = 0; ks < KS2; ++ks) {
+        const int k = 4 * ks + fc;
+        double af[QT];
+#pragma unroll
+        for (int i = 0; i < QT; ++i) {
+          const int q = 8 * i + fr;
+          af[i] = (q < Q && k < K) ? sph[q * K + k] : 0.0;
+        }
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const double bf = k < K ? sd[(v * K + k) * 32 + 8 * tt + fr] : 0.0;
+#pragma unroll
+          for (int i = 0; i < QT; ++i) dmma884(f[i][tt][0], f[i][tt][1], af[i], bf);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < QT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int q = 8 * i + fr, cl = 8 * tt + 2 * fc + j;
+            if (q < Q) {
+              sval[q][v][cl] = f[i][tt][j];
+              const int cc2 = scell[cl];
+              if (cc2 >= 0) W.fp[static_cast<size_t>(D.slot[ao(cc2, q, Q)]) * V5 + v] = f[i][tt][j];
+            }
+          }
+      __syncthreads();  // every face value of the chunk in sval
+      if (chk)
+        for (int q = 0; q < Q; ++q) {
+          const double val = sval[q][v][lane];
+          viol = smax(viol, smax(blo - val, val - bhi));
+        }
+    } else {
+      __syncthreads();  // the gather buffer becomes the face-value buffer
+      eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
+                            STAGED ? sp + EP + ED + EO : nullptr);
+    }
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
@@ -985,8 +1093,11 @@ Kern3 kern3() {
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
   k.smem_central_staged = std::max(k.smem_central, 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32)) +
                           8 * static_cast<size_t>(M * K + Q * K + 160);
-  k.smem_cwenoz_staged = k.smem_cwenoz + 8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K) +
-                         4 * static_cast<size_t>(NF * MD3);
+  k.smem_cwenoz_staged = (K >= 8 ? std::max(k.smem_cwenoz, 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
+                                  : k.smem_cwenoz) +
+                         8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K +
+                                                 (K >= 8 ? 160 : 0)) +
+                         4 * static_cast<size_t>(NF * MD3 + 32);
   k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);
   k.central = k3_central<K, M, NF, NQ, false>;
   k.central_staged = k3_central<K, M, NF, NQ, true>;

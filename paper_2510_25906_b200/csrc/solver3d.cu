@@ -147,7 +147,7 @@ struct Dev3 {
 struct Phys3 {
   double gamma, cfl, lambda1p, weno_eps, weno_b, lam0, lams;
   MarginParams mg;
-  int mode, limiter, hll, detect;
+  int mode, limiter, hll;
 };
 
 struct Work3 {
@@ -1059,11 +1059,7 @@ __global__ void k3_halo_pack(const double* __restrict__ U, const int32_t* __rest
 
 __global__ void k3_dt_init(Work3 W) { *W.dtmin = static_cast<unsigned long long>(__double_as_longlong(1e300)); }
 
-__global__ void k3_dt_finalize(Work3 W, double cfl, int advance_time) {
-  const double dt = cfl * __longlong_as_double(static_cast<long long>(*W.dtmin));
-  if (advance_time) *W.t += W.dt[0];  // previous step's dt
-  W.dt[0] = dt;
-}
+__global__ void k3_dt_finalize(Work3 W, double cfl) { W.dt[0] = cfl * __longlong_as_double(static_cast<long long>(*W.dtmin)); }
 
 __global__ void k3_time_add(Work3 W) { *W.t += W.dt[0]; }
 
@@ -1286,11 +1282,11 @@ struct GpuSolver3::Impl {
     exchange(U);
   }
 
-  void dt_kernels(bool advance_time) {
+  void dt_kernels() {
     k3_dt_init<<<1, 1, 0, st>>>(W);
     k3_dt<<<(n + 255) / 256, 256, 0, st>>>(D, P, W, U);
     if (comm) NK(nccl().AllReduce(W.dtmin, W.dtmin, 1, ncclUint64, ncclMin, comm, st));  // positive doubles order as bits
-    k3_dt_finalize<<<1, 1, 0, st>>>(W, o.cfl, advance_time ? 1 : 0);
+    k3_dt_finalize<<<1, 1, 0, st>>>(W, o.cfl);
     launches += 3;
   }
 
@@ -1301,7 +1297,7 @@ struct GpuSolver3::Impl {
     cudaGraph_t g = nullptr;
     const int64_t before = launches;
     CK3(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    dt_kernels(false);
+    dt_kernels();
     step(rk);
     k3_time_add<<<1, 1, 0, st>>>(W);
     ++launches;
@@ -1439,7 +1435,7 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     P.lams = (1.0 - P.lam0) / (I.NF + 1 - 1);   // reconstruct.cpp:114
     P.mg = MarginParams{o.margins.alpha_m, o.margins.beta_m, o.margins.alpha_w, o.margins.beta_w, o.margins.kappa,
                         o.margins.deact_n};
-    P.mode = o.mode, P.limiter = o.limiter, P.hll = o.riemann == UCFVB_HLL ? 1 : 0, P.detect = 1;
+    P.mode = o.mode, P.limiter = o.limiter, P.hll = o.riemann == UCFVB_HLL ? 1 : 0;
     Work3& W = I.W;
     const int64_t nch = (n + 31) / 32;
     W.fp = dalloc<double>(static_cast<size_t>(I.nF) * NQ * 2 * V5, I.owned);
@@ -1539,7 +1535,7 @@ double GpuSolver3::max_stable_dt() {
   Impl& I = *p_;
   CK3(cudaSetDevice(I.device));
   I.reset_errors();
-  I.dt_kernels(false);
+  I.dt_kernels();
   CK3(cudaMemcpyAsync(I.h_dt, I.W.dt, sizeof(double), cudaMemcpyDeviceToHost, I.st));
   I.check_errors();
   return I.h_dt[0];
@@ -1566,7 +1562,7 @@ double GpuSolver3::run_steps(int n_steps, double t0, int rk) {
   CK3(cudaMemcpyAsync(I.W.t, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
   if (I.timing) {
     for (int i = 0; i < n_steps; ++i) {
-      I.dt_kernels(false);
+      I.dt_kernels();
       I.step(rk);
       k3_time_add<<<1, 1, 0, I.st>>>(I.W);
       ++I.launches;
@@ -1601,7 +1597,7 @@ double GpuSolver3::advance_host(const double* u_in, double* u_out, int n_steps, 
   if (!I.timing && (!I.step_graph || I.graph_rk != rk)) I.capture(rk);
   for (int i = 0; i < n_steps; ++i) {
     if (I.timing) {
-      I.dt_kernels(false);
+      I.dt_kernels();
       I.step(rk);
       k3_time_add<<<1, 1, 0, I.st>>>(I.W);
       ++I.launches;

@@ -201,3 +201,32 @@ def test_mesh3_and_stencils3_argument_errors():
         Stencils3(m, 1)  # the mesh face rule was built for order 2 (2x2 points; order 1 needs 1)
     with pytest.raises(A.InvalidArgument):
         m.project_initial(99, [1.0])
+
+
+def test_3d_riemann_flux_reduces_to_the_pinned_2d_flux():
+    """With w = 0 and an in-plane normal the 3D HLLC/HLL (Cartesian form) is
+    the reference's 2D flux (euler.cpp:40-89, rotated frame) -- checked against
+    the 2D port, which is pinned bit-exactly to the compiled reference."""
+    import ctypes as C
+
+    from oracle import port as P2
+    rng = np.random.default_rng(3)
+    g = 1.4
+    dp = C.POINTER(C.c_double)
+    for kind in (A.HLLC, A.HLL):
+        for _ in range(200):
+            def state2():
+                rho, p = rng.uniform(0.2, 2.0), rng.uniform(0.2, 3.0)
+                u, v = rng.uniform(-2, 2, 2)
+                return np.array([rho, rho * u, rho * v, p / (g - 1) + 0.5 * rho * (u * u + v * v)])
+            ul2, ur2 = state2(), state2()
+            th = rng.uniform(0, 2 * np.pi)
+            nx, ny = np.cos(th), np.sin(th)
+            f2 = np.zeros(4)
+            rc = P2.lib().port_flux(ul2.ctypes.data_as(dp), ur2.ctypes.data_as(dp), nx, ny, g, kind,
+                                    f2.ctypes.data_as(dp))
+            assert rc == 0
+            up = lambda s: np.array([s[0], s[1], s[2], 0.0, s[3]])
+            f3 = flux(up(ul2), up(ur2), np.array([nx, ny, 0.0]), g, kind)
+            np.testing.assert_allclose(f3[[0, 1, 2, 4]], f2, rtol=1e-12, atol=1e-12 * np.abs(f2).max())
+            assert abs(f3[3]) <= 1e-14 * np.abs(f2).max()

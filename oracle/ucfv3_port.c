@@ -177,8 +177,10 @@ static void solve_dofs(const port3* P, int c, const double* u, double* dofs) {
   }
 }
 
-/* evaluate_cell (solver.cpp:76-89) with eval_poly (reconstruct.hpp:26-36) */
-static void evaluate_cell(port3* P, const double* u, int c, const double* dofs) {
+/* evaluate_cell (solver.cpp:76-89) with eval_poly (reconstruct.hpp:26-36) over
+ * the first ke dofs (ke = K; MUSCL's limited r = 1 polynomial passes ke = 3:
+ * its dofs k >= 3 are zero and those terms are left out) */
+static void evaluate_cell_n(port3* P, const double* u, int c, const double* dofs, int ke) {
   const int K = P->K, Q = P->Q;
   const double* phi = &P->s.phi[(int64_t)opi(P, c) * Q * K];
   const int32_t* slots = &P->s.qp_slot[(int64_t)c * Q];
@@ -186,13 +188,14 @@ static void evaluate_cell(port3* P, const double* u, int c, const double* dofs) 
   for (int q = 0; q < Q; ++q) {
     double out[NV];
     for (int v = 0; v < NV; ++v) out[v] = u0[v];
-    for (int k = 0; k < K; ++k) {
+    for (int k = 0; k < ke; ++k) {
       const double p = phi[q * K + k];
       for (int v = 0; v < NV; ++v) out[v] = fma(dofs[k * NV + v], p, out[v]);
     }
     memcpy(slot_ptr(P, slots[q]), out, sizeof out);
   }
 }
+static void evaluate_cell(port3* P, const double* u, int c, const double* dofs) { evaluate_cell_n(P, u, c, dofs, P->K); }
 static void evaluate_constant(port3* P, const double* u, int c) {
   const int32_t* slots = &P->s.qp_slot[(int64_t)c * P->Q];
   for (int q = 0; q < P->Q; ++q) memcpy(slot_ptr(P, slots[q]), &u[(int64_t)c * NV], sizeof(double) * NV);
@@ -395,7 +398,7 @@ static int apply_troubled(port3* P, const double* u) {
         for (int k = 0; k < 3; ++k) dofs[k * NV + v] = th * lin[k][v];
         for (int k = 3; k < K; ++k) dofs[k * NV + v] = 0.0;
       }
-      evaluate_cell(P, u, c, dofs);
+      evaluate_cell_n(P, u, c, dofs, 3);
     } else {
       for (int k = 0; k < K * NV; ++k) dofs[k] = 0.0;
       evaluate_constant(P, u, c);

@@ -189,7 +189,9 @@ __host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
 
 // evaluate the reconstruction of (cell, var) at its Q face points, stage the
 // values for the positivity check, and report the bounds failure (fallback_check)
-template <int K, int NQ, int NF>
+// KE: number of leading dofs evaluated (MUSCL's limited r = 1 polynomial: 3, the
+// rest are zero; oracle evaluate_cell_n)
+template <int K, int NQ, int NF, int KE = K>
 __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
                                            double u0, const double* a, double (*sval)[V5][33], bool chk,
                                            double blo, double bhi, double& viol, const int* sl,
@@ -206,7 +208,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
     if (phs) {  // the block's operator row staged in shared memory (broadcast 16-byte reads)
       double2 w[QG];
 #pragma unroll
-      for (int k = 0; k < K; ++k)
+      for (int k = 0; k < KE; ++k)
 #pragma unroll
         for (int j = 0; j < QG; ++j) {
           const int e = (q0 + j) * K + k;
@@ -215,7 +217,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
         }
     } else {
 #pragma unroll
-      for (int k = 0; k < K; ++k)
+      for (int k = 0; k < KE; ++k)
 #pragma unroll
         for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], D.phi[ao(op, (q0 + j) * K + k, Q * K)], val[j]);
     }
@@ -933,8 +935,8 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
-                          STAGED ? sp + 3 * M : nullptr);
+    eval_store<K, NQ, NF, 3>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
+                             STAGED ? sp + 3 * M : nullptr);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }

@@ -11,12 +11,18 @@
 // the reference's 2D functions); kernels are compiled with --fmad=false and
 // the K x M / Q x K contractions use explicit __fma_rn, as the restatement
 // does with fma() (no reference arithmetic exists in 3D; see its header).
+// Stencil values arrive by 8-byte cp.async (all in flight at once).
+// Lattice-class meshes (config 5) number their cells type-blocked, so a block
+// sees one operator row: it is staged in shared memory once per kernel
+// (STAGED) and the contractions run as fp64 tensor-core tiles (DMMA
+// m8n8k4, bit-identical to the fma chain in k order; dmma884 below).
 //
 //   k3_central   solve_dofs + evaluate_cell + NAD raw label + fallback pre-check  (solver.cpp:336-349, 113-149, 229-264)
 //   k3_spread    spread_flags (pull form) + class lists + Linear-cell demotion    (detector.cpp:37-53)
 //   k3_cwenoz    directional solves + CWENOZ blend + evaluate + fallback          (solver.cpp:167-188, reconstruct.cpp:43-150)
 //   k3_muscl     r=1 solve + BJ/Venkatakrishnan limiter + evaluate + fallback    (solver.cpp:189-221)
 //   k3_face_flux HLLC/HLL at every face Gauss point, summed in qp order          (solver.cpp:266-295)
+//                (k3_face_flux_lanes: one lane per point, shuffle sum, for power-of-two point counts)
 //   k3_gather_rk owner-ordered face->cell sum + SSP-RK combination               (solver.cpp:296-311, time_integrator.cpp:31-38)
 //   k3_dt        max_stable_dt                                                   (solver.cpp:103-111)
 #include <cuda_runtime.h>

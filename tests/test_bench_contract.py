@@ -1,0 +1,41 @@
+"""The driver's bench contract for the reference arm (runs on CPU): one JSON
+line with the documented keys, the BASELINE metric and the impl tag; the 3D
+configurations' reference arm (the 3D oracle restatement) likewise."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _run(args, env_extra):
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], capture_output=True, text=True, env=env,
+                       timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+def test_reference_arm_json_line():
+    from oracle import ref as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "3"], {"UCFVB_REF_BUDGET_S": "1"})
+    import bench
+    assert d["impl"] == "reference" and d["metric"] == bench.METRIC and d["unit"] == bench.UNIT
+    for k in ("value", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling", "dtype", "data",
+              "config", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_3d_json_line():
+    d = _run(["--impl", "reference", "--config", "5", "--steps", "1", "--warmup", "3"], {"UCFVB_CPU_S": "0.5"})
+    assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"

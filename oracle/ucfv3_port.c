@@ -27,9 +27,10 @@
  *
  * Arithmetic: the 2D path keeps the reference's unfused x86-64 arithmetic
  * (no FMA) for bit parity. The 3D discretisation has no reference
- * arithmetic to match, so its least-squares solves and polynomial
- * evaluations (the K x M and Q x K contractions) accumulate with fused
- * multiply-adds, acc = fma(a, b, acc) in the same term order -- one rounding
+ * arithmetic to match, so its least-squares solves, polynomial
+ * evaluations and the K x K smoothness-indicator form (the contractions)
+ * accumulate with fused multiply-adds, acc = fma(a, b, acc) in the same term
+ * order -- one rounding
  * per term and half the fp64 instructions on the device; every other
  * operation is unfused as in 2D. C's fma() and CUDA's __fma_rn are both the
  * correctly rounded fused operation, so the device matches this restatement
@@ -280,13 +281,15 @@ static double limiter_venkat(double u0, double umin, double umax, const double* 
   return theta;
 }
 
+/* smoothness_indicator (reconstruct.cpp:88-97): row then dot, each a fused
+ * accumulation in the reference's order (the 3D contraction rule of the header) */
 static double smoothness_indicator(const double* oi, const double* a, int K) {
   double s = 0.0;
   for (int k = 0; k < K; ++k) {
     const double* row = &oi[(int64_t)k * K];
     double t = 0.0;
-    for (int q = 0; q < K; ++q) t += row[q] * a[q];
-    s += a[k] * t;
+    for (int q = 0; q < K; ++q) t = fma(row[q], a[q], t);
+    s = fma(a[k], t, s);
   }
   return s;
 }

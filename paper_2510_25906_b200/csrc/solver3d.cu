@@ -723,13 +723,58 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
 #pragma unroll
     for (int k = 0; k < K; ++k) p1[k] /= P.lam0;
     // SI_0 = p1' OI p1 (row then dot) and the directional SI from the 3x3 block
+    // SI_0 = p1' OI p1: t_k = sum_q OI_kq p1_q, si0 = sum_k p1_k t_k, fused, in the oracle's order
     double si0 = 0.0;
+    if constexpr (DM) {
+      // t(K x 32) = OI(K x K) . p1(K x 32) on the tensor cores (warp v's variable)
+      constexpr int MT = (K + 7) / 8, KS3 = (K + 3) / 4;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      double t = 0.0;
+      for (int k = 0; k < K; ++k) sd[(v * K + k) * 32 + lane] = p1[k];
+      __syncwarp();
+      double tacc[MT][4][2];
 #pragma unroll
-      for (int q = 0; q < K; ++q) t += (STAGED ? sp[EP + ED + k * K + q] : (STAGED ? sp[EP + ED + (k * K + q)] : D.oi[ao(op, k * K + q, K * K)])) * p1[q];
-      si0 += p1[k] * t;
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) tacc[i][tt][0] = tacc[i][tt][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KS3; ++ks) {
+        const int q = 4 * ks + fc;
+        double af[MT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int k = 8 * i + fr;
+          af[i] = (k < K && q < K) ? sp[EP + ED + k * K + q] : 0.0;
+        }
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const double bf = q < K ? sd[(v * K + q) * 32 + 8 * tt + fr] : 0.0;
+#pragma unroll
+          for (int i = 0; i < MT; ++i) dmma884(tacc[i][tt][0], tacc[i][tt][1], af[i], bf);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int tt = 0; tt < 4; ++tt) {
+          const int k = 8 * i + fr;
+          if (k < K) {
+            sd[(v * K + k) * 32 + 8 * tt + 2 * fc] = tacc[i][tt][0];
+            sd[(v * K + k) * 32 + 8 * tt + 2 * fc + 1] = tacc[i][tt][1];
+          }
+        }
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < K; ++k) si0 = __fma_rn(p1[k], sd[(v * K + k) * 32 + lane], si0);
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        double t = 0.0;
+#pragma unroll
+        for (int q = 0; q < K; ++q) t = __fma_rn(STAGED ? sp[EP + ED + k * K + q] : D.oi[ao(op, k * K + q, K * K)], p1[q], t);
+        si0 = __fma_rn(p1[k], t, si0);
+      }
     }
     const double o00 = (STAGED ? sp[EP + ED + (0)] : D.oi[ao(op, 0, K * K)]), o01 = (STAGED ? sp[EP + ED + (1)] : D.oi[ao(op, 1, K * K)]), o02 = (STAGED ? sp[EP + ED + (2)] : D.oi[ao(op, 2, K * K)]);
     const double o10 = (STAGED ? sp[EP + ED + (K)] : D.oi[ao(op, K, K * K)]), o11 = (STAGED ? sp[EP + ED + (K + 1)] : D.oi[ao(op, K + 1, K * K)]), o12 = (STAGED ? sp[EP + ED + (K + 2)] : D.oi[ao(op, K + 2, K * K)]);

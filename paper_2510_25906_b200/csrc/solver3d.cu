@@ -295,6 +295,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
                                                       : static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
                                                : smem3_bytes(G, Q) / 8;
   double* sp = smem3 + kUnion;
+  // per-cell operator rows (p <= 2): the chunk's pinv block is copied to shared
+  // memory with 16-byte cp.async at the chunk start (all in flight at once)
+  constexpr bool PCS = !STAGED && K * M <= 200;
+  double* spc = smem3 + kUnion;
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
@@ -316,6 +320,11 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       const int nx = ch + gridDim.x;
       bulk_prefetch_l2(D.pinv + static_cast<size_t>(nx) * M * K * 32, M * K * 32 * 8);
       bulk_prefetch_l2(D.central + static_cast<size_t>(nx) * (M + 1) * 32, (M + 1) * 32 * 4);
+    }
+    const bool pcs = PCS && D.n_ops == D.n;
+    if (pcs) {
+      const double* src = D.pinv + static_cast<size_t>(ch) * M * K * 32;
+      for (int e = threadIdx.x; e < M * K * 32 / 2; e += 160) cp_async16(spc + 2 * e, src + 2 * e);
     }
     // every stencil and neighbour value of this (cell, variable) in flight at
     // once: G fire-and-forget 8-byte cp.async copies into shared memory
@@ -340,6 +349,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
     const int* sl = kHoist ? slh : nullptr;
     const double u0 = U[static_cast<size_t>(cc) * V5 + v];
     cp_async_wait_all();  // this thread's own copies
+    if (pcs) __syncthreads();  // the pinv block is copied by all threads
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
@@ -408,6 +418,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
             if ((e & 1) == 0) w = reinterpret_cast<const double2*>(sp)[e >> 1];
             a[k] = __fma_rn((e & 1) ? w.y : w.x, x, a[k]);
           }
+        } else if (PCS) {
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+            a[k] = __fma_rn(pcs ? spc[(m * K + k) * 32 + lane] : D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
         } else {
 #pragma unroll
           for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
@@ -1177,7 +1191,7 @@ template <int K, int M, int NF, int NQ>
 Kern3 kern3() {
   constexpr int Q = NF * NQ;
   Kern3 k{};
-  k.smem_central = smem3_bytes(M + NF, Q);
+  k.smem_central = smem3_bytes(M + NF, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
   k.smem_cwenoz = smem3_bytes(M, Q);
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)

@@ -613,6 +613,10 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
   double* su0 = sp + EP + ED + EO + Q * K;
   int* sdm = reinterpret_cast<int*>(su0 + (DM ? 160 : 0));
   int* scell = sdm + NF * MD3;  // DM: the chunk's cells
+  // forced CWENOZ on per-cell rows (p <= 2): the list is the identity, so each
+  // item is one AoSoA chunk whose pinv block is copied to shared memory first
+  constexpr bool PCS = !STAGED && K * M <= 200;
+  double* spc = smem3 + kUnion;
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int t = STAGED ? blockIdx.x % W.ntl : 0;
@@ -632,6 +636,11 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
     const int c = list[act ? base + lane : base];
     const int op = D.opi[c];
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
+    const bool pcs = PCS && P.mode == UCFVB_CWENOZ && D.n_ops == D.n && (base & 31) == 0;
+    if (pcs) {
+      const double* src = D.pinv + static_cast<size_t>(base >> 5) * M * K * 32;
+      for (int e = threadIdx.x; e < M * K * 32 / 2; e += 160) cp_async16(spc + 2 * e, src + 2 * e);
+    }
     // the M central-stencil values in flight at once (cp.async); the central
     // solve is recomputed here (bit-identical to k3_central's) instead of
     // storing K x 5 dofs for every cell
@@ -657,12 +666,15 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
 #pragma unroll
     for (int k = 0; k < K; ++k) p1[k] = 0.0;
     if constexpr (!DM) {
+      if (pcs) __syncthreads();  // the pinv block is copied by all threads
 #pragma unroll
       for (int m = 0; m < M; ++m) {
         const double x = xs[m * 160 + threadIdx.x] - u0;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          p1[k] = __fma_rn(STAGED ? sp[m * K + k] : D.pinv[ao(op, m * K + k, M * K)], x, p1[k]);
+          p1[k] = __fma_rn(STAGED ? sp[m * K + k]
+                                  : (pcs ? spc[(m * K + k) * 32 + lane] : D.pinv[ao(op, m * K + k, M * K)]),
+                           x, p1[k]);
       }
     } else {
       su0[threadIdx.x] = u0;
@@ -1192,13 +1204,13 @@ Kern3 kern3() {
   constexpr int Q = NF * NQ;
   Kern3 k{};
   k.smem_central = smem3_bytes(M + NF, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
-  k.smem_cwenoz = smem3_bytes(M, Q);
+  k.smem_cwenoz = smem3_bytes(M, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
-  k.smem_central_staged = std::max(k.smem_central, 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32)) +
+  k.smem_central_staged = std::max(smem3_bytes(M + NF, Q), 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32)) +
                           8 * static_cast<size_t>(M * K + Q * K + 160);
-  k.smem_cwenoz_staged = (K >= 8 ? std::max(k.smem_cwenoz, 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
-                                  : k.smem_cwenoz) +
+  k.smem_cwenoz_staged = (K >= 8 ? std::max(smem3_bytes(M, Q), 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
+                                  : smem3_bytes(M, Q)) +
                          8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K +
                                                  (K >= 8 ? 160 : 0)) +
                          4 * static_cast<size_t>(NF * MD3 + 32);

@@ -1192,7 +1192,7 @@ struct Kern3 {
   void (*muscl)(Dev3, Phys3, Work3, const double*);
   void (*cwenoz_staged)(Dev3, Phys3, Work3, const double*);
   void (*muscl_staged)(Dev3, Phys3, Work3, const double*);
-  size_t smem_cwenoz_staged, smem_muscl_staged;
+  size_t smem_cwenoz_staged, smem_muscl_staged, smem_cwenoz_base;
   void (*constant)(Dev3, Work3, const double*);
   void (*flux)(Dev3, Phys3, Work3);
   int flux_lanes = 1;
@@ -1204,6 +1204,7 @@ Kern3 kern3() {
   constexpr int Q = NF * NQ;
   Kern3 k{};
   k.smem_central = smem3_bytes(M + NF, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
+  k.smem_cwenoz_base = smem3_bytes(M, Q);
   k.smem_cwenoz = smem3_bytes(M, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
@@ -1618,6 +1619,8 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
       I.mu_grid = grid_for(I.kern.muscl_staged, I.kern.smem_muscl_staged);
       I.mu_grid = std::max(nops, I.mu_grid - I.mu_grid % nops);
     } else {
+      // the per-cell pinv staging region is only used by forced CWENOZ (identity list)
+      if (o.mode != UCFVB_CWENOZ) I.kern.smem_cwenoz = I.kern.smem_cwenoz_base;
       I.cw_grid = grid_for(I.kern.cwenoz, I.kern.smem_cwenoz);
       I.mu_grid = grid_for(I.kern.muscl, I.kern.smem_muscl);
     }

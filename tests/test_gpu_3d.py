@@ -282,3 +282,28 @@ def test_advance_host_matches_run_steps3():
     bad[3, 0] = -1.0
     with pytest.raises(A.NonPhysicalError):
         gpu.advance_host(bad, 1)
+
+
+@pytest.mark.parametrize("order", [2, 3])
+def test_staged_tensor_core_path_with_troubled_cells(order):
+    """Type-blocked lattice-class mesh (8^3 cubes x 6 tets: staged rows, DMMA
+    central / CWENOZ / OI.p1) with a blast, so the CWENOZ and MUSCL kernels have
+    real work: labels, face values and states bit-identical to the oracle
+    (weno_b = 1 keeps tau^b exact)."""
+    m, st, o, u0, gpu, cpu = build(TET, order, 0.0, IC_BLAST, n=8, classes=True, mode="hybrid", weno_b=1.0)
+    assert m.view.cell_order == 1 and st.n_ops == 6
+    rg, rc = gpu.compute_residual(u0), cpu.compute_residual(u0)
+    lab = cpu.labels()
+    counts = np.bincount(lab, minlength=4)
+    assert counts[1] > 50 and counts[2] > 50, counts  # CWENOZ and MUSCL cells present
+    assert np.array_equal(gpu.labels(), lab)
+    assert np.array_equal(gpu.face_values(), cpu.face_values())
+    assert np.array_equal(rg, rc)
+    gpu.state = u0
+    cpu.state = u0.copy()
+    for _ in range(2):
+        dt = cpu.max_stable_dt()
+        gpu.advance(dt)
+        cpu.advance(dt)
+        assert np.array_equal(gpu.step_labels(), cpu.labels(step=True))
+    assert np.array_equal(gpu.state, cpu.state)

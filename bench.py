@@ -347,6 +347,7 @@ def run_b200_arm(args):
     # ---- value leg: state resident in HBM, K graph-replayed RK3 steps
     solver.state = u0
     solver.run_steps(args.warmup, A.RK3)
+    lists_used = solver.list_stats()["lists"]
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -462,7 +463,7 @@ def run_b200_arm(args):
                                                   f"; weak scaling: domain repeated {world}x in y, RCB-partitioned, "
                                                   f"one {n}-cell block per GPU") if world > 1 else ""),
                        "cells": owned_total, "cells_per_gpu": n, "order": c["order"], "K": K, "M": MM,
-                       "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid",
+                       "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid", "class_lists": lists_used,
                        "parallelism": f"domain decomposition x{world}, NCCL halo exchange per stage" if world > 1
                        else "single",
                        "l2": "inputs larger than L2 (per-cell operator data %.0f MB)" % (

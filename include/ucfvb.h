@@ -270,6 +270,14 @@ int32_t ucfvb_get_step_labels(ucfvb_solver* h, uint8_t* labels);
 int32_t ucfvb_get_labels(ucfvb_solver* h, uint8_t* labels);
 /* label counts of step_labels: Linear, CWENOZ, MUSCL, FirstOrder */
 int32_t ucfvb_get_census(ucfvb_solver* h, int64_t counts[4]);
+/* Troubled-cell class lists (an implementation choice; results are identical):
+ * policy 0 = 32-cell chunk lists (default), 1 = dense per-cell lists. Stats of
+ * the last synchronised stage's lists: CWENOZ cells, MUSCL cells, CWENOZ
+ * chunks, MUSCL chunks, 1 if per-cell lists are in use (cells whose
+ * reconstruction fell back to first order stay counted in their list).
+ * No reference counterpart. */
+int32_t ucfvb_set_list_policy(ucfvb_solver* h, int32_t policy);
+int32_t ucfvb_get_list_stats(ucfvb_solver* h, int64_t stats[5]);
 /* cells whose NAD detector value lies within 1e-12 (relative) of a threshold
  * on the last detecting stage (north_star tie band) */
 int32_t ucfvb_get_nad_ties(ucfvb_solver* h, int64_t* ties);

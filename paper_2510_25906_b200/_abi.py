@@ -326,6 +326,8 @@ def _declare(lib):
         "ucfvb_get_labels": (C.c_int32, [H, P(C.c_uint8)]),
         "ucfvb_get_census": (C.c_int32, [H, c_i64p]),
         "ucfvb_get_nad_ties": (C.c_int32, [H, c_i64p]),
+        "ucfvb_set_list_policy": (C.c_int32, [H, C.c_int32]),
+        "ucfvb_get_list_stats": (C.c_int32, [H, c_i64p]),
         "ucfvb_get_face_values": (C.c_int32, [H, c_dp, c_dp]),
         "ucfvb_get_dofs": (C.c_int32, [H, c_dp]),
         "ucfvb_set_phase_timing": (C.c_int32, [H, C.c_int32]),
@@ -363,7 +365,7 @@ ABI_SYMBOLS = [
     "ucfvb_get_state", "ucfvb_max_stable_dt", "ucfvb_advance", "ucfvb_compute_residual",
     "ucfvb_run_steps", "ucfvb_run_steps_log", "ucfvb_run_until", "ucfvb_advance_host", "ucfvb_write_field_snapshot", "ucfvb_write_census_csv",
     "ucfvb_write_timing_csv", "ucfvb_get_step_labels", "ucfvb_get_labels", "ucfvb_get_census",
-    "ucfvb_get_nad_ties", "ucfvb_get_face_values", "ucfvb_get_dofs", "ucfvb_set_phase_timing",
+    "ucfvb_get_nad_ties", "ucfvb_set_list_policy", "ucfvb_get_list_stats", "ucfvb_get_face_values", "ucfvb_get_dofs", "ucfvb_set_phase_timing",
     "ucfvb_get_phase_times", "ucfvb_n_cells", "ucfvb_n_faces", "ucfvb_n_qp",
     "ucfvb_state_device_ptr", "ucfvb_stream", "ucfvb_launch_count",
     "ucfvb_partition_rcb", "ucfvb_subdomain_build", "ucfvb_subdomain_views", "ucfvb_subdomain_info",

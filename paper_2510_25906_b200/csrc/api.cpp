@@ -206,6 +206,12 @@ int32_t ucfvb_get_labels(ucfvb_solver* h, uint8_t* labels) {
 int32_t ucfvb_get_census(ucfvb_solver* h, int64_t counts[4]) {
   return guard(h, [&] { h->s->get_census(counts); });
 }
+int32_t ucfvb_set_list_policy(ucfvb_solver* h, int32_t policy) {
+  return guard(h, [&] { h->s->set_list_policy(policy); });
+}
+int32_t ucfvb_get_list_stats(ucfvb_solver* h, int64_t stats[5]) {
+  return guard(h, [&] { h->s->get_list_stats(stats); });
+}
 int32_t ucfvb_get_nad_ties(ucfvb_solver* h, int64_t* ties) {
   return guard(h, [&] { *ties = h->s->nad_ties(); });
 }

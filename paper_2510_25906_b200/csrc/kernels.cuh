@@ -105,7 +105,7 @@ struct Scratch {
   uint8_t* step_labels;
   int* list_c;
   int* list_m;
-  int* counts;       // [0] CWENOZ list length, [1] MUSCL list length, [2]/[3] chunk-list lengths
+  int* counts;       // [0]/[1] CWENOZ/MUSCL cells (per-cell list lengths), [2]/[3] CWENOZ/MUSCL chunks (chunk-list lengths)
   int2* chunks_c;    // (chunk, lane mask) of 32-cell chunks holding CWENOZ cells
   int2* chunks_m;    // ... MUSCL cells
   unsigned long long* ties;
@@ -388,21 +388,42 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
   if (flags & FL_CHUNKS) {  // one entry per 32-cell chunk (= this warp) with troubled cells
     // block-aggregated: one global atomic per block and class (the chunk lists
     // are unordered; per-cell results do not depend on the order)
-    __shared__ int s_nc, s_nm, s_bc, s_bm;
-    if (threadIdx.x == 0) s_nc = s_nm = 0;
+    // The cell totals (counts[0]/[1]) are not list lengths here (list
+    // statistics only).
+    __shared__ int s_nc, s_nm, s_bc, s_bm, s_cc, s_cm;
+    if (threadIdx.x == 0) s_nc = s_nm = s_cc = s_cm = 0;
     __syncthreads();
     int pc = -1, pm = -1;
-    if (lane == 0 && mc) pc = atomicAdd(&s_nc, 1);
-    if (lane == 0 && mm) pm = atomicAdd(&s_nm, 1);
+    if (lane == 0 && mc) {
+      pc = atomicAdd(&s_nc, 1);
+      atomicAdd(&s_cc, __popc(mc));
+    }
+    if (lane == 0 && mm) {
+      pm = atomicAdd(&s_nm, 1);
+      atomicAdd(&s_cm, __popc(mm));
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
       s_bc = s_nc ? atomicAdd(&S.counts[2], s_nc) : 0;
       s_bm = s_nm ? atomicAdd(&S.counts[3], s_nm) : 0;
+      if (s_cc) atomicAdd(&S.counts[0], s_cc);
+      if (s_cm) atomicAdd(&S.counts[1], s_cm);
     }
     __syncthreads();
     if (pc >= 0) S.chunks_c[s_bc + pc] = make_int2(c >> 5, static_cast<int>(mc));
     if (pm >= 0) S.chunks_m[s_bm + pm] = make_int2(c >> 5, static_cast<int>(mm));
     return;
+  }
+  // chunk totals (counts[2]/[3], list statistics only): one atomic per block
+  __shared__ int s_kc, s_km;
+  if (threadIdx.x == 0) s_kc = s_km = 0;
+  __syncthreads();
+  if (lane == 0 && mc) atomicAdd(&s_kc, 1);
+  if (lane == 0 && mm) atomicAdd(&s_km, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s_kc) atomicAdd(&S.counts[2], s_kc);
+    if (s_km) atomicAdd(&S.counts[3], s_km);
   }
   if (mc) {
     int base = 0;

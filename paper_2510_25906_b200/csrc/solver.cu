@@ -274,7 +274,22 @@ struct GpuSolver::Impl {
   int world = 1, rank = 0;
 
   size_t l2_window_bytes = 0, l2_persist_bytes = 0;
-  bool per_cell_lists = false;  // UCFVB_TROUBLED=lists: dense per-cell class lists instead of chunk lists
+  // Class lists for the troubled cells: 32-cell chunk lists (TMA-staged
+  // k_troubled_split, the default) or dense per-cell lists (k_cwenoz /
+  // k_muscl; UCFVB_TROUBLED=lists or set_list_policy). Chunks measured faster
+  // on configs 1-3, including config 3's half-full chunks (profiles/round1.md).
+  bool per_cell_lists = false;
+  int* hcounts = nullptr;  // pinned copy of S.counts after the last synchronising call
+  void fetch_counts() { CK(cudaMemcpyAsync(hcounts, S.counts, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream)); }
+  void drop_graphs() {
+    for (auto& a : graph)
+      for (auto& b : a)
+        for (auto& g : b)
+          if (g) {
+            CK(cudaGraphExecDestroy(g));
+            g = nullptr;
+          }
+  }
   dim3 grid_owned() const { return dim3((L.n_owned + kBlock - 1) / kBlock); }
 
   // halo exchange of a stage state: pack per peer, then one grouped send/recv
@@ -599,6 +614,8 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
   I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
   if (const char* tl = std::getenv("UCFVB_TROUBLED")) I.per_cell_lists = std::strcmp(tl, "lists") == 0;
+  CK(cudaMallocHost(&I.hcounts, 4 * sizeof(int)));
+  std::memset(I.hcounts, 0, 4 * sizeof(int));
   if (I.ks.central_tma) {
     const char* e1 = std::getenv("UCFVB_TMA_STAGES_CENTRAL");
     const char* e2 = std::getenv("UCFVB_TMA_STAGES_TROUBLED");
@@ -743,6 +760,7 @@ GpuSolver::~GpuSolver() {
   if (I.census_dev) cudaFree(I.census_dev);
   if (I.dtlog_dev) cudaFree(I.dtlog_dev);
   if (I.host_stage) cudaFreeHost(I.host_stage);
+  if (I.hcounts) cudaFreeHost(I.hcounts);
   for (auto& e : I.ev)
     if (e) cudaEventDestroy(e);
   if (I.stream) cudaStreamDestroy(I.stream);
@@ -807,6 +825,7 @@ void GpuSolver::advance(double dt, double t, int rk) {
     I.launches = I.launch_step(rk, false, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], false);
   }
   I.allreduce_error();
+  I.fetch_counts();
   int k, f, c;
   if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);  // state stays at t (reference semantics)
   I.cur ^= 1;
@@ -910,6 +929,7 @@ double GpuSolver::run_impl(int n_steps, int rk, double t0, double t_end, bool un
                         I.stream));
   if (!until) I.allreduce_error();
   CK(cudaMemcpyAsync(&h, I.ds, sizeof h, cudaMemcpyDeviceToHost, I.stream));
+  I.fetch_counts();
   I.read_error(&k, &f, &c);
   // steps that ran to completion: the device counter holds the last started step
   int ran = launched;
@@ -982,6 +1002,7 @@ double GpuSolver::advance_host(const double* u_in, double* u_out, int n_steps, i
   CK(cudaMemcpyAsync(he, I.S.err, 4 * sizeof(int), cudaMemcpyDeviceToHost, I.stream));
   CK(cudaMemcpyAsync(hs, I.ds, sizeof(DtState), cudaMemcpyDeviceToHost, I.stream));
   CK(cudaMemcpyAsync(u_out, I.ubuf[I.cur], bytes, cudaMemcpyDeviceToHost, I.stream));
+  I.fetch_counts();
   CK(cudaStreamSynchronize(I.stream));
   CK(cudaGetLastError());
   I.stage_is_first = false;
@@ -1087,13 +1108,22 @@ void GpuSolver::attach_nccl(const uint8_t id[128], int rank, int world, const uc
   }
   I.sendbuf = dalloc<double4>(std::max<size_t>(1, off), I.owned);
   // graphs captured before the exchange existed are stale
-  for (auto& a : I.graph)
-    for (auto& b : a)
-      for (auto& g : b)
-        if (g) {
-          cudaGraphExecDestroy(g);
-          g = nullptr;
-        }
+  I.drop_graphs();
+}
+
+void GpuSolver::set_list_policy(int policy) {
+  Impl& I = *p_;
+  if (policy < 0 || policy > 1) throw ApiError(UCFVB_INVALID, "set_list_policy: policy must be 0 or 1");
+  if ((policy == 1) != I.per_cell_lists) {
+    I.per_cell_lists = policy == 1;
+    I.drop_graphs();
+  }
+}
+
+void GpuSolver::get_list_stats(int64_t out[5]) {
+  Impl& I = *p_;
+  for (int i = 0; i < 4; ++i) out[i] = I.hcounts[i];
+  out[4] = I.per_cell_lists ? 1 : 0;
 }
 
 }  // namespace ucfvb

@@ -37,6 +37,10 @@ class GpuSolver {
   int64_t nad_ties();
   void get_face_values(double* left, double* right);
   void get_dofs(double* dofs);
+  // troubled-cell class lists: 0 chunk lists (default), 1 per-cell lists
+  void set_list_policy(int policy);
+  // last synchronised stage: CWENOZ cells, MUSCL cells, CWENOZ chunks, MUSCL chunks, per-cell lists in use
+  void get_list_stats(int64_t out[5]);
   void set_phase_timing(bool on);
   void get_phase_times(double t[4]);
 

@@ -189,6 +189,19 @@ class Solver:
         self._ck(self._lib.ucfvb_get_nad_ties(self._h, C.byref(t)))
         return t.value
 
+    LIST_POLICIES = {"chunks": 0, "lists": 1}
+
+    def set_list_policy(self, policy: str):
+        """Troubled-cell class lists: "chunks" (default) or "lists" (per cell)."""
+        self._ck(self._lib.ucfvb_set_list_policy(self._h, self.LIST_POLICIES[policy]))
+
+    def list_stats(self) -> dict:
+        """Class-list sizes of the last synchronised stage and the lists in use."""
+        s = np.zeros(5, dtype=np.int64)
+        self._ck(self._lib.ucfvb_get_list_stats(self._h, s.ctypes.data_as(A.c_i64p)))
+        return {"cwenoz_cells": int(s[0]), "muscl_cells": int(s[1]), "cwenoz_chunks": int(s[2]),
+                "muscl_chunks": int(s[3]), "lists": "per-cell" if s[4] else "chunks"}
+
     def face_values(self):
         L = np.zeros((self.n_faces * self.n_qp, 4))
         R = np.zeros_like(L)

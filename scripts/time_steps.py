@@ -36,4 +36,4 @@ p0 = s.phase_times().copy()
 s.run_steps(10, A.RK3)
 ph = (s.phase_times() - p0) / 30 * 1e6
 print(f"{a.tag} config{a.config}: {1e3 * ms / (3 * a.steps):.1f} us/stage  {n * 3 * a.steps / ms / 1e6:.3f} G/s  "
-      f"phases(us) central {ph[0]:.1f} detect {ph[1]:.1f} weights {ph[2]:.1f} flux {ph[3]:.1f}")
+      f"phases(us) central {ph[0]:.1f} detect {ph[1]:.1f} weights {ph[2]:.1f} flux {ph[3]:.1f}  {s.list_stats()}")

@@ -116,3 +116,31 @@ def test_config3_quarter_scale_decomposition_bit_exact():
     for s, u in zip(subs, states):
         out[s.gid[: s.n_owned]] = u[: s.n_owned]
     np.testing.assert_array_equal(out, ref)
+
+
+@pytest.mark.parametrize("name,scale", [("config2", 1), ("config3", 4)])
+def test_class_list_policies_bit_identical(name, scale):
+    """Chunk lists and per-cell lists give the same state and the same list
+    statistics; the statistics agree with the last stage's labels (a listed
+    cell whose reconstruction fell back to first order is labelled 3)."""
+    mk, order, ic, prm, opts, bcs, mesh, st, u0 = product_case(name, scale)
+    o = A.options_from_dict(order=order, **opts)
+    g = Solver(mesh, o, make_bcs(bcs), stencils=st)
+    out = {}
+    for pol in ("lists", "chunks"):
+        g.set_list_policy(pol)
+        g.state = u0
+        g.run_steps(2, A.RK3)
+        out[pol] = (g.state, g.list_stats(), g.labels())
+    np.testing.assert_array_equal(out["lists"][0], out["chunks"][0])
+    np.testing.assert_array_equal(out["lists"][2], out["chunks"][2])
+    sl, sc, lab = out["lists"][1], out["chunks"][1], out["chunks"][2]
+    assert sl.pop("lists") == "per-cell" and sc.pop("lists") == "chunks"
+    assert sl == sc
+    pad = lambda m: np.pad(m, (0, -len(m) % 32)).reshape(-1, 32)
+    n1, n2, n3 = (int((lab == k).sum()) for k in (1, 2, 3))
+    assert n1 <= sc["cwenoz_cells"] and n2 <= sc["muscl_cells"]
+    assert sc["cwenoz_cells"] + sc["muscl_cells"] <= n1 + n2 + n3
+    assert int(pad(lab == 1).any(1).sum()) <= sc["cwenoz_chunks"] <= int(pad(lab >= 1).any(1).sum())
+    assert int(pad(lab == 2).any(1).sum()) <= sc["muscl_chunks"] <= int(pad(lab >= 1).any(1).sum())
+    assert 32 * sc["cwenoz_chunks"] >= sc["cwenoz_cells"] and 32 * sc["muscl_chunks"] >= sc["muscl_cells"]

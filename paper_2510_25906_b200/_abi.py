@@ -13,7 +13,7 @@ from pathlib import Path
 import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "lib" / "libucfvb.so"
+LIB_PATH = Path(os.environ["UCFVB_LIB"]) if os.environ.get("UCFVB_LIB") else PKG_DIR / "lib" / "libucfvb.so"  # UCFVB_LIB: A/B builds
 
 # enums (ucfvb.h)
 OK, NONPHYSICAL, INVALID, CUDA_ERR, UNSUPPORTED = 0, 1, 2, 3, 4

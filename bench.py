@@ -230,9 +230,9 @@ def build_case(cfg, n_threads=0, world=1, strong=False):
     return mesh, st, u0, time.perf_counter() - t0
 
 
-def cpu_reference_run(cfg, steps, budget_s=None):
+def cpu_reference_run(cfg, steps, budget_s=None, warmup=0):
     """The reference's own CPU path (oracle/_ref) on the same mesh, seed, RK3 driver.
-    Returns (cell-stage/s, steps timed, kind, setup seconds)."""
+    `warmup` untimed RK3 steps run first. Returns (cell-stage/s, steps timed, setup seconds, cells)."""
     from oracle import ref as R
     from paper_2510_25906_b200 import _abi as A
     from paper_2510_25906_b200.solver import make_bcs
@@ -248,6 +248,8 @@ def cpu_reference_run(cfg, steps, budget_s=None):
     rs.set_state(u0)
     setup = time.perf_counter() - t0
     done, wall, t = 0, 0.0, 0.0
+    for _ in range(warmup):
+        t, _, _ = rs.run_steps(1, A.RK3, t0=t)
     while done < steps:
         t, w, _ = rs.run_steps(1, A.RK3, t0=t)
         wall += w
@@ -273,11 +275,11 @@ def run_reference_arm(args):
     # warm-up steps are untimed; each timed step is one full RK3 step of the config,
     # bounded by a wall budget so the run ends within minutes
     budget = float(os.environ.get("UCFVB_REF_BUDGET_S", "60"))
-    rate, done, setup, n = cpu_reference_run(cfg, max(1, args.steps), budget_s=budget)
+    rate, done, setup, n = cpu_reference_run(cfg, max(1, args.steps), budget_s=budget, warmup=args.warmup)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
-        "warmup": 0, "ms_per_step": 1e3 * n * 3 / rate, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * n * 3 / rate, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": c["desc"], "cells": n, "order": c["order"], "integrator": "SSP-RK3",
                    "timed_steps": done, "requested_steps": args.steps, "setup_s": round(setup, 3)},
@@ -499,15 +501,18 @@ def build_case3(cfg, n_threads=0, n=None):
     return mesh, st, u0, time.perf_counter() - t0
 
 
-def port3_rate(cfg, budget_s):
+def port3_rate(cfg, budget_s, warmup=0):
     """The 3D oracle restatement (oracle/ucfv3_port.c, 1 thread) on a bounded
-    sample: the same config on a 12^3-cube mesh, RK3 steps until `budget_s`."""
+    sample: the same config on a 12^3-cube mesh, `warmup` untimed RK3 steps,
+    then RK3 steps until `budget_s`."""
     from oracle.port3 import Port3Solver
     from paper_2510_25906_b200 import _abi as A
     c = CONFIGS3[cfg]
     mesh, st, u0, _ = build_case3(cfg, n=12)
     P = Port3Solver(mesh, st, A.options_from_dict(order=c["order"], mode=c["mode"], cfl=0.5))
     P.state = u0.copy()
+    for _ in range(warmup):
+        P.advance(P.max_stable_dt(), rk=A.RK3)
     done, t0 = 0, time.perf_counter()
     while done < 2 or (time.perf_counter() - t0 < budget_s and done < 200):
         P.advance(P.max_stable_dt(), rk=A.RK3)
@@ -529,10 +534,10 @@ def run_arm_3d(args):
     if args.impl == "reference":
         if rank != 0:
             return
-        rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "20")))
+        rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "20")), warmup=args.warmup)
         sample = (f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle restatement "
                   f"oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has {os.cpu_count()} cores")
-        print(json.dumps({"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 1, "steps": done, "warmup": 0,
+        print(json.dumps({"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 1, "steps": done, "warmup": args.warmup,
                           "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
                           "dtype": "f64", "data": "synthetic", "impl": "reference",
                           "config": {"workload": c["desc"]},

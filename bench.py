@@ -522,8 +522,9 @@ def port3_rate(cfg, budget_s, warmup=0):
 
 
 def run_arm_3d(args):
-    """3D configurations 4 / 4c / 5 on one GPU (the 3D path has no domain
-    decomposition yet)."""
+    """3D configurations 4 / 4c / 5: one GPU, or (torchrun, N>1) strong scaling
+    of the config's mesh RCB-split into N subdomains with an NCCL halo exchange
+    every stage."""
     import ctypes as C
 
     import torch

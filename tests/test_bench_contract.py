@@ -34,8 +34,10 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["value"] > 0 and d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["warmup"] == 3  # untimed warm-up steps actually run (timing rule: W >= 3)
 
 
 def test_reference_arm_3d_json_line():
     d = _run(["--impl", "reference", "--config", "5", "--steps", "1", "--warmup", "3"], {"UCFVB_CPU_S": "0.5"})
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "port"
+    assert d["warmup"] == 3

@@ -1,20 +1,28 @@
 #!/usr/bin/env python3
 """Benchmark of the hybrid NAD stage pass (BASELINE.json metric) on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 2]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference] [--config 3]
 
-One bench "step" is one SSP-RK3 time step of BASELINE config 2 (262,144
-jittered triangles, p=2, shock into a sine wave; 3 stages = 786,432
-cell-stage updates): device dt (max_stable_dt) + 3 x (central LSQ + NAD +
-spread/compaction + CWENOZ + MUSCL + fallback + HLLC flux + RK update).
+One bench "step" is one SSP-RK3 time step of BASELINE config 3 by default
+(8,388,608 triangles on the periodic unit square, p=3, random quadrants + 1 %
+noise; 3 stages = 25,165,824 cell-stage updates): device dt (max_stable_dt) +
+3 x (central LSQ + NAD + spread/compaction + CWENOZ + MUSCL + fallback + HLLC
+flux + RK update). Config 3 is the largest 2D configuration, the one BASELINE
+quotes at 1/2/4/8 GPUs; configs 1 and 2 (`--config 1|2`) and the 3D configs
+4, 4c (forced all-CWENOZ) and 5 are selectable.
 `value` = cell-stage updates / s with the state resident in HBM (device
 timed with CUDA events on the solver's stream, max over ranks); `e2e` = the
 same metric through the C ABI with the state copied host->device (pinned)
 before and device->host after every step, inside the timed region.
+N > 1 (torchrun): strong scaling by default -- the config's mesh RCB-split
+into N subdomains, NCCL halo exchange every stage (`--scaling weak` repeats
+the config's domain per GPU instead).
 
 --impl reference times the reference's own CPU code (oracle/_ref: the
 unmodified /root/reference sources compiled here; single-threaded -- it has
-no parallel regions) on the same config, mesh, seed and RK3 driver.
+no parallel regions) on the same config, seed and RK3 driver; for config 3 on
+a bounded sample (a 512x512x2 tile of the same configuration, because the
+reference's single-threaded setup of the full mesh alone takes ~8 min).
 """
 from __future__ import annotations
 
@@ -49,6 +57,55 @@ CONFIGS = {
               desc="BASELINE config 3: periodic unit square, 2048x2048x2 tris, p=3, random quadrants + 1% noise"),
 }
 SEED = 1
+# CPU legs (cpu_baseline, --impl reference) run the reference on a bounded
+# sample of the workload: configs 1-2 whole; config 3 as a 512x512x2 tile of
+# the same configuration (same p, IC, seed, margins; per-cell work identical,
+# the mesh 16x smaller so the reference's single-threaded setup takes ~30 s)
+CPU_SAMPLE = {"3": dict(nx=512, ny=512)}
+
+
+def workload_config(cfg, world=1, strong=True):
+    """The static `config` dict of a 2D bench line -- identical in both arms."""
+    c = CONFIGS[cfg]
+    cells = 2 * c["nx"] * c["ny"] * (1 if (strong or world == 1) else world)
+    K = (c["order"] + 1) * (c["order"] + 2) // 2 - 1
+    par = "single"
+    wl = c["desc"]
+    if world > 1:
+        par = f"domain decomposition x{world} (RCB), NCCL halo exchange every stage"
+        wl += (f"; strong scaling: the config's mesh split into {world} subdomains" if strong else
+               f"; weak scaling: the config's domain repeated {world}x in y, one block per GPU")
+    return {"workload": wl, "config": cfg, "cells": cells, "order": c["order"], "K": K, "M": 2 * K,
+            "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid", "parallelism": par,
+            "l2": "inputs larger than L2 (per-cell operator data >= 0.7 GB)"}
+
+
+def cpu_sample_case(cfg):
+    """(config dict of the CPU sample, description) for the CPU legs."""
+    c = dict(CONFIGS[cfg])
+    if cfg in CPU_SAMPLE:
+        c.update(CPU_SAMPLE[cfg])
+        return c, (f"a {c['nx']}x{c['ny']}x2 tile of config {cfg} ({2 * c['nx'] * c['ny']} cells; same p, IC, "
+                   f"seed and options)")
+    return c, f"config {cfg} itself ({2 * c['nx'] * c['ny']} cells)"
+
+
+def env_overrides():
+    """UCFVB_* diagnostics knobs set in the environment (none in a benchmark run)."""
+    return {k: v for k, v in sorted(os.environ.items()) if k.startswith("UCFVB_")}
+
+
+def traffic_for(cfg, cells, phase):
+    """ncu DRAM bytes (read + write) per launch of `phase` measured on this
+    config and size (profiles/traffic.json, keyed by config), else None."""
+    tf = ROOT / "profiles" / "traffic.json"
+    try:
+        t = json.loads(tf.read_text()).get(f"config{cfg}")
+        if t and int(t.get("cells", -1)) == int(cells):
+            return t.get(phase)
+    except Exception:
+        pass
+    return None
 
 # 3D configurations (SURVEY.md §8f f3; the reference is 2D only, DESIGN.md §11)
 CONFIGS3 = {
@@ -236,7 +293,7 @@ def cpu_reference_run(cfg, steps, budget_s=None, warmup=0):
     from oracle import ref as R
     from paper_2510_25906_b200 import _abi as A
     from paper_2510_25906_b200.solver import make_bcs
-    c = CONFIGS[cfg]
+    c, _ = cpu_sample_case(cfg)
     nq = (c["order"] + 2) // 2
     per = {"both": 3, "y": 2, "x": 1, "none": 0}[c["periodic"]]
     t0 = time.perf_counter()
@@ -267,25 +324,26 @@ def run_reference_arm(args):
         return
     from oracle import ref as R
     cfg = args.config
-    c = CONFIGS[cfg]
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libucfv_ref.so was not built "
                                                               "(reference sources absent at build time)"}))
         return
-    # warm-up steps are untimed; each timed step is one full RK3 step of the config,
-    # bounded by a wall budget so the run ends within minutes
+    # warm-up steps are untimed; each timed step is one full RK3 step of the
+    # bounded sample, the timed steps bounded by a wall budget
     budget = float(os.environ.get("UCFVB_REF_BUDGET_S", "60"))
     rate, done, setup, n = cpu_reference_run(cfg, max(1, args.steps), budget_s=budget, warmup=args.warmup)
+    _, sample = cpu_sample_case(cfg)
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
-        "warmup": args.warmup, "ms_per_step": 1e3 * n * 3 / rate, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * n * 3 / rate, "higher_is_better": True,
+        "scaling": "strong" if args.scaling == "strong" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c["desc"], "cells": n, "order": c["order"], "integrator": "SSP-RK3",
-                   "timed_steps": done, "requested_steps": args.steps, "setup_s": round(setup, 3)},
+        "config": workload_config(cfg, world, args.scaling == "strong"),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": f"{done} RK3 steps of config {cfg} ({n} cells) through the unmodified reference "
-                                   f"Solver::compute_residual (single-threaded; host has {cores} cores)"},
+                         "sample": f"{done} timed RK3 steps (after {args.warmup} untimed) of {sample} through the "
+                                   f"unmodified reference Solver::compute_residual (single-threaded: the reference "
+                                   f"has no parallel regions; host has {cores} cores); setup {setup:.1f}s excluded"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -335,9 +393,9 @@ def run_b200_arm(args):
     def sum_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
+        t = torch.tensor(np.asarray(x, dtype=np.float64), device="cuda")
         dist.all_reduce(t)
-        return float(t.item())
+        return t.cpu().numpy() if t.dim() else float(t.item())
 
     def max_over_ranks(x):
         if world == 1:
@@ -363,14 +421,17 @@ def run_b200_arm(args):
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     launches = solver.launch_count()
-    owned_total = int(round(sum_over_ranks(n)))
+    owned_total = int(round(sum_over_ranks(float(n))))
     total_units = owned_total * 3 * args.steps
     value = total_units / (ms * 1e-3)
 
-    # census of the timed run (class mix feeds the roofline bytes)
+    # census of the same K steps from u0 (outside the timed region): per-step
+    # NAD class fractions (run.cpp:110-116 step labels) and threshold ties
     solver.state = u0
-    _, census = solver.run_steps(min(args.steps, 20), A.RK3, census=True)
+    _, census = solver.run_steps(args.steps, A.RK3, census=True)
+    ties = int(round(sum_over_ranks(float(solver.nad_ties()))))
     mix = census.sum(0) / census.sum()
+    per_step = [[round(float(x), 4) for x in row / max(1, row.sum())] for row in census]
 
     # ---- per-kernel durations (events between kernel groups, un-graphed stages)
     solver.state = u0
@@ -418,7 +479,6 @@ def run_b200_arm(args):
     e2e_value = owned_total * 3 * e2e_steps / (e2e_ms * 1e-3)
 
     # ---- roofline of the dominant kernel
-    H = solver
     K, NQ = st.view.K, st.view.n_qp
     NF = 3
     sd = st.numpy()
@@ -433,13 +493,7 @@ def run_b200_arm(args):
     achieved = phase_bytes[dom] / phases[dom] / 1e9
     stage_bytes = sum(phase_bytes)
     stage_achieved = stage_bytes / phases.sum() / 1e9
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        try:
-            traffic = json.loads(tf.read_text()).get(names[dom].split()[0])
-        except Exception:
-            traffic = None
+    traffic = traffic_for(cfg, solver.n_cells, names[dom].split()[0]) if world == 1 else None
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -447,10 +501,11 @@ def run_b200_arm(args):
             from oracle import ref as R
             if R.available():
                 rate, done, rsetup, _ = cpu_reference_run(cfg, 50, budget_s=float(os.environ.get("UCFVB_CPU_S", "12")))
+                _, sample = cpu_sample_case(cfg)
                 cpu_baseline = {"value": rate, "unit": UNIT, "cores": 1, "kind": "reference",
-                                "sample": f"{done} RK3 steps of config {cfg} ({n} cells), unmodified reference "
-                                          f"sources (oracle/_ref), 1 thread (the reference has no parallel regions);"
-                                          f" setup {rsetup:.1f}s excluded; host has {os.cpu_count()} cores"}
+                                "sample": f"{done} RK3 steps of {sample}, unmodified reference sources "
+                                          f"(oracle/_ref), 1 thread (the reference has no parallel regions); setup "
+                                          f"{rsetup:.1f}s excluded; host has {os.cpu_count()} cores"}
         except Exception as e:  # pragma: no cover
             cpu_baseline = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -460,19 +515,16 @@ def run_b200_arm(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": c["desc"] + ((f"; strong scaling: the config's mesh RCB-partitioned into {world} "
-                                                  f"subdomains ({n} owned cells on rank 0)" if strong else
-                                                  f"; weak scaling: domain repeated {world}x in y, RCB-partitioned, "
-                                                  f"one {n}-cell block per GPU") if world > 1 else ""),
-                       "cells": owned_total, "cells_per_gpu": n, "order": c["order"], "K": K, "M": MM,
-                       "integrator": "SSP-RK3 (3 stages/step)", "mode": "hybrid", "class_lists": lists_used,
-                       "parallelism": f"domain decomposition x{world}, NCCL halo exchange per stage" if world > 1
-                       else "single",
-                       "l2": "inputs larger than L2 (per-cell operator data %.0f MB)" % (
-                           (kb["central"] + kb["cwenoz"] + kb["flux"]) * n / 1e6),
-                       "class_mix_first_stage": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
-                                                 "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
-                       "setup_s": round(setup_s, 3)},
+            "config": workload_config(cfg, world, strong),
+            "census": {"class_lists": lists_used,
+                       "class_mix": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
+                                     "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
+                       "class_mix_per_step_LCMF": per_step, "nad_ties": ties,
+                       "note": "step labels after the first stage of each step (run.cpp:110-116), the K timed "
+                               "steps re-run from the initial state; nad_ties summed over every detecting stage"},
+            "setup_s": round(setup_s, 3),
+            "cells_per_gpu": n,
+            "env_overrides": env_overrides(),
             "clocks": clk.summary(),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(solver.n_cells * 32 * world),
                     "d2h_bytes_per_step": int(solver.n_cells * 32 * world)},
@@ -499,6 +551,20 @@ def build_case3(cfg, n_threads=0, n=None):
     deg = 1 if c["ic"] == 1 else max(2 * c["order"], 2)
     u0 = mesh.project_initial(c["ic"], c["params"], seed=SEED, degree=deg, n_threads=n_threads)
     return mesh, st, u0, time.perf_counter() - t0
+
+
+def workload_config3(cfg, world=1):
+    """The static `config` dict of a 3D bench line -- identical in both arms."""
+    c = CONFIGS3[cfg]
+    nper = 6 if c["kind"] == 1 else 1
+    K = {2: 9, 3: 19}.get(c["order"], None)
+    wl = c["desc"] + (f"; strong scaling: the config's mesh RCB-split into {world} subdomains, NCCL halo exchange "
+                      f"every stage" if world > 1 else "")
+    return {"workload": wl, "config": cfg, "cells": nper * c["n"] ** 3, "order": c["order"], "K": K,
+            "M": 2 * K if K else None, "nf": 4 if c["kind"] == 1 else 6, "integrator": "SSP-RK3 (3 stages/step)",
+            "mode": c["mode"], "operator_rows": "lattice classes (6 shared rows)" if c["classes"] else "per cell",
+            "parallelism": f"domain decomposition x{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (face values alone > 0.5 GB)"}
 
 
 def port3_rate(cfg, budget_s, warmup=0):
@@ -538,10 +604,10 @@ def run_arm_3d(args):
         rate, done, ncell = port3_rate(cfg, float(os.environ.get("UCFVB_CPU_S", "20")), warmup=args.warmup)
         sample = (f"{done} RK3 steps of config {cfg} on a 12^3-cube mesh ({ncell} cells), 3D oracle restatement "
                   f"oracle/ucfv3_port.c (the reference is 2D only), 1 thread; host has {os.cpu_count()} cores")
-        print(json.dumps({"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": 1, "steps": done, "warmup": args.warmup,
-                          "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-                          "dtype": "f64", "data": "synthetic", "impl": "reference",
-                          "config": {"workload": c["desc"]},
+        print(json.dumps({"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": done,
+                          "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+                          "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+                          "config": workload_config3(cfg, world),
                           "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
                           "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
@@ -683,17 +749,12 @@ def run_arm_3d(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": c["desc"] + (f"; strong scaling: RCB-split into {world} subdomains, NCCL halo "
-                                            f"exchange every stage ({n} local cells on rank 0)" if world > 1 else ""),
-                   "cells": n_global, "order": c["order"], "K": st.K, "M": st.M, "nf": mesh.nf,
-                   "nq": mesh.nq, "integrator": "SSP-RK3 (3 stages/step)", "mode": c["mode"],
-                   "operator_rows": "lattice classes (6 shared rows)" if c["classes"] else "per cell",
-                   "parallelism": f"domain decomposition x{world}" if world > 1 else "single",
-                   "l2": "inputs larger than L2 (face values alone %.0f MB)" % (mesh.n_faces * mesh.nq * 80 / 1e6),
-                   "class_mix_last_step": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
+        "config": workload_config3(cfg, world),
+        "census": {"class_mix_last_step": {"linear": round(float(mix[0]), 4), "cwenoz": round(float(mix[1]), 4),
                                            "muscl": round(float(mix[2]), 4), "first": round(float(mix[3]), 4)},
-                   "class_mix_per_step_LCMF": per_step,
-                   "nad_ties": int(ties), "setup_s": round(setup_s, 2)},
+                   "class_mix_per_step_LCMF": per_step, "nad_ties": int(ties)},
+        "setup_s": round(setup_s, 2), "cells_local": n,
+        "env_overrides": env_overrides(),
         "clocks": clk.summary(),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 40)},
         "gpu_launches": int(launches),
@@ -715,10 +776,10 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="2", choices=sorted(CONFIGS) + sorted(CONFIGS3))
+    ap.add_argument("--config", default="3", choices=sorted(CONFIGS) + sorted(CONFIGS3))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak (config domain repeated per GPU, default) or strong (the config's mesh split N ways)")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong (the config's mesh split N ways, default) or weak (config domain repeated per GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -278,8 +278,10 @@ int32_t ucfvb_get_census(ucfvb_solver* h, int64_t counts[4]);
  * No reference counterpart. */
 int32_t ucfvb_set_list_policy(ucfvb_solver* h, int32_t policy);
 int32_t ucfvb_get_list_stats(ucfvb_solver* h, int64_t stats[5]);
-/* cells whose NAD detector value lies within 1e-12 (relative) of a threshold
- * on the last detecting stage (north_star tie band) */
+/* NAD threshold ties (north_star tie band): cells whose detector value lies
+ * within 1e-12 (relative) of a threshold, summed over every detecting stage
+ * of the last advance / compute_residual / run call (a cell counts once per
+ * stage it ties in) */
 int32_t ucfvb_get_nad_ties(ucfvb_solver* h, int64_t* ties);
 
 /* parity taps: val_left_/val_right_ in [face*n_qp+q][4] order (solver.hpp:91),

@@ -79,6 +79,11 @@ struct Layout {
   const double* eps2;       // [n] (venkat_kappa*h)^3
   const double* h;          // [n]
   const double* inv_vol;    // [n] 1/area
+  // per-cell records of the troubled-cell operator rows (kernels_cells.cuh, CellRec)
+  const unsigned char* rec_ca;  // CWENOZ group A [n][CA]
+  const unsigned char* rec_cb;  // CWENOZ group B [n][CB]
+  const unsigned char* rec_ma;  // MUSCL group A  [n][MA]
+  const unsigned char* rec_mb;  // MUSCL group B  [n][MB]
 };
 
 struct Physics {
@@ -254,7 +259,6 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
   pdl_wait();
   if (g == 0) {  // this stage's class-list counters and tie count (read only by later kernels)
     for (int i = 0; i < 4; ++i) S.counts[i] = 0;
-    if (flags & FL_NAD) *S.ties = 0;
   }
   if (*(volatile int*)S.err) return;
   const bool live = c0 < L.n;
@@ -414,29 +418,39 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
     if (pm >= 0) S.chunks_m[s_bm + pm] = make_int2(c >> 5, static_cast<int>(mm));
     return;
   }
-  // chunk totals (counts[2]/[3], list statistics only): one atomic per block
-  __shared__ int s_kc, s_km;
-  if (threadIdx.x == 0) s_kc = s_km = 0;
-  __syncthreads();
-  if (lane == 0 && mc) atomicAdd(&s_kc, 1);
-  if (lane == 0 && mm) atomicAdd(&s_km, 1);
+  // dense per-cell lists, block-aggregated: one global atomic per block and
+  // class; entries keep warp order inside the block (the lists are unordered
+  // across blocks; per-cell results do not depend on the order). The chunk
+  // totals (counts[2]/[3]) are list statistics only.
+  __shared__ int s_wc[kBlock / 32], s_wm[kBlock / 32], s_bc, s_bm;
+  const int w = threadIdx.x >> 5;
+  if (lane == 0) {
+    s_wc[w] = __popc(mc);
+    s_wm[w] = __popc(mm);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (s_kc) atomicAdd(&S.counts[2], s_kc);
-    if (s_km) atomicAdd(&S.counts[3], s_km);
+    int tc = 0, tm = 0, kc = 0, km = 0;
+#pragma unroll
+    for (int i = 0; i < kBlock / 32; ++i) {
+      tc += s_wc[i];
+      tm += s_wm[i];
+      kc += s_wc[i] ? 1 : 0;
+      km += s_wm[i] ? 1 : 0;
+    }
+    s_bc = tc ? atomicAdd(&S.counts[0], tc) : 0;
+    s_bm = tm ? atomicAdd(&S.counts[1], tm) : 0;
+    if (kc) atomicAdd(&S.counts[2], kc);
+    if (km) atomicAdd(&S.counts[3], km);
   }
-  if (mc) {
-    int base = 0;
-    if (lane == __ffs(mc) - 1) base = atomicAdd(&S.counts[0], __popc(mc));
-    base = __shfl_sync(kFull, base, __ffs(mc) - 1);
-    if (lab == 1) S.list_c[base + __popc(mc & lt)] = c;
+  __syncthreads();
+  int oc = s_bc, om = s_bm;
+  for (int i = 0; i < w; ++i) {
+    oc += s_wc[i];
+    om += s_wm[i];
   }
-  if (mm) {
-    int base = 0;
-    if (lane == __ffs(mm) - 1) base = atomicAdd(&S.counts[1], __popc(mm));
-    base = __shfl_sync(kFull, base, __ffs(mm) - 1);
-    if (lab == 2) S.list_m[base + __popc(mm & lt)] = c;
-  }
+  if (lab == 1) S.list_c[oc + __popc(mc & lt)] = c;
+  if (lab == 2) S.list_m[om + __popc(mm & lt)] = c;
 }
 
 // ---------------------------------------------------------------------------

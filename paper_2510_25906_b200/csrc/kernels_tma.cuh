@@ -100,7 +100,6 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
     s_err = *(volatile int*)S.err;
     if (blockIdx.x == 0) {  // this stage's class-list counters and tie count
       for (int i = 0; i < 4; ++i) S.counts[i] = 0;
-      if (flags & FL_NAD) *S.ties = 0;
     }
   }
   __syncthreads();
@@ -288,253 +287,16 @@ struct TroubledStage {
   static constexpr uint32_t SPLIT_BYTES = A_BYTES + B_BYTES;
 };
 
-// k_troubled_tma: the CWENOZ and MUSCL reconstructions of one stage in one
-// persistent launch. Work items are the chunk lists built by k_spread
-// (FL_CHUNKS): items [0, nC) are CWENOZ chunks, [nC, nC + nM) MUSCL chunks;
-// the scheme is uniform per block iteration, lanes of cells outside the
-// chunk's mask idle through the (shuffle-synchronous) math and store nothing.
-// Arithmetic is identical to k_cwenoz / k_muscl (kernels.cuh).
-template <int K, int NQ, int NF, int MM, int MD, int NS>
-__global__ void __launch_bounds__(kBlock) k_troubled_tma(Layout L, Physics ph, Scratch S,
-                                                         const double4* __restrict__ U, int flags) {
-  using St = TroubledStage<K, NQ, NF, MM, MD>;
-  constexpr int Q = St::Q;
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + NS * St::BYTES);
-  const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
-  const int tid = threadIdx.x;
-  const int slot = tid >> 2;
-  const int v = tid & 3;
-  __shared__ int s_err, s_nc, s_nm;
-  pdl_wait();
-  if (tid == 0) {
-    s_err = *(volatile int*)S.err;
-    s_nc = S.counts[2];
-    s_nm = S.counts[3];
-    for (int i = 0; i < NS; ++i) mbar_init(&bar[i], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  if (s_err) return;
-  const int nc = s_nc, nitems = s_nc + s_nm;
-  if (nc > 0 && !(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
-    if (blockIdx.x == 0 && tid == 0) atomicOr(&S.err[0], 4);
-    return;
-  }
-  auto item_chunk = [&](int i) { return i < nc ? S.chunks_c[i] : S.chunks_m[i - nc]; };
-  auto issue = [&](int i, int st) {
-    unsigned char* b = smem + st * St::BYTES;
-    const size_t ch = static_cast<size_t>(item_chunk(i).x);
-    if (i < nc) {
-      mbar_arrive_expect_tx(&bar[st], St::C_BYTES);
-      unsigned char* p = b;
-      bulk_g2s(p, L.dir_idx + ch * NF * MD * 32, St::C_DIDX, &bar[st]);
-      p += St::C_DIDX;
-      bulk_g2s(p, L.pinv_dir + ch * NF * MD * 2 * 32, St::C_PDIR, &bar[st]);
-      p += St::C_PDIR;
-      bulk_g2s(p, L.oi + ch * K * K * 32, St::C_OI, &bar[st]);
-      p += St::C_OI;
-      bulk_g2s(p, L.phi + ch * Q * K * 32, St::C_PHI, &bar[st]);
-      p += St::C_PHI;
-      bulk_g2s(p, L.nbr + ch * NF * 32, St::C_NBR, &bar[st]);
-      p += St::C_NBR;
-      bulk_g2s(p, S.dofs + ch * K * 32, St::C_DOFS, &bar[st]);
-    } else {
-      mbar_arrive_expect_tx(&bar[st], St::M_BYTES);
-      unsigned char* p = b;
-      bulk_g2s(p, L.st_idx + ch * MM * 32, St::M_IDX, &bar[st]);
-      p += St::M_IDX;
-      bulk_g2s(p, L.pinv_lin + ch * MM * 2 * 32, St::M_PLIN, &bar[st]);
-      p += St::M_PLIN;
-      bulk_g2s(p, L.phi01 + ch * Q * 2 * 32, St::M_PHI, &bar[st]);
-      p += St::M_PHI;
-      bulk_g2s(p, L.nbr + ch * NF * 32, St::M_NBR, &bar[st]);
-    }
-  };
-  if (tid == 0)
-    for (int p = 0; p < NS - 1; ++p)
-      if (static_cast<int>(blockIdx.x + p * gridDim.x) < nitems) issue(blockIdx.x + p * gridDim.x, p);
-  double* dofs = reinterpret_cast<double*>(S.dofs);
-  double* fv = reinterpret_cast<double*>(S.fp);
-  const bool venkat = ph.limiter == 1;
-  int it = 0;
-  for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
-    const int st = it % NS;
-    const int ahead = i + (NS - 1) * gridDim.x;
-    if (tid == 0 && ahead < nitems) {
-      fence_proxy_async_smem();
-      issue(ahead, (it + NS - 1) % NS);
-    }
-    const int2 e = item_chunk(i);
-    const bool mine = (static_cast<unsigned>(e.y) >> slot) & 1u;
-    const int c = e.x * 32 + slot;  // chunks are full-size in the padded layout; cells past n are never in a mask
-    const int cc = c < L.n ? c : L.n - 1;
-    mbar_wait(&bar[st], (it / NS) & 1);
-    const unsigned char* b = smem + st * St::BYTES;
-    const double u0 = __ldg(Ud + 4 * static_cast<size_t>(cc) + v);
-    double vals[Q];
-    double lo = u0, hi = u0;
-    double kd[K];  // dofs to keep for the tap
-    if (i < nc) {
-      // ---- CWENOZ (solver.cpp:167-188, reconstruct.cpp:43-150)
-      const int* sdi = reinterpret_cast<const int*>(b);
-      const double* spd = reinterpret_cast<const double*>(b + St::C_DIDX);
-      const double* soi = reinterpret_cast<const double*>(b + St::C_DIDX + St::C_PDIR);
-      const double* sph = reinterpret_cast<const double*>(b + St::C_DIDX + St::C_PDIR + St::C_OI);
-      const int* snb = reinterpret_cast<const int*>(b + St::C_DIDX + St::C_PDIR + St::C_OI + St::C_PHI);
-      const double* sdo =
-          reinterpret_cast<const double*>(b + St::C_DIDX + St::C_PDIR + St::C_OI + St::C_PHI + St::C_NBR);
-      double um[NF][MD];
-#pragma unroll
-      for (int s = 0; s < NF; ++s)
-#pragma unroll
-        for (int m = 0; m < MD; ++m) um[s][m] = __ldg(Ud + 4 * static_cast<size_t>(sdi[(s * MD + m) * 32 + slot]) + v);
-      double dir[NF][2];
-#pragma unroll
-      for (int s = 0; s < NF; ++s) {
-        dir[s][0] = 0.0;
-        dir[s][1] = 0.0;
-#pragma unroll
-        for (int m = 0; m < MD; ++m) {
-          const double d = um[s][m] - u0;
-          dir[s][0] += spd[((s * MD + m) * 2 + 0) * 32 + slot] * d;
-          dir[s][1] += spd[((s * MD + m) * 2 + 1) * 32 + slot] * d;
-        }
-      }
-      constexpr int st1 = NF + 1;
-      const double lam0 = 1.0 - 1.0 / ph.lambda1p;
-      const double lams = (1.0 - lam0) / (st1 - 1);
-      double p1[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = sdo[(k * 32 + slot) * 4 + v];
-#pragma unroll
-      for (int s = 0; s < NF; ++s) {
-        p1[0] -= lams * dir[s][0];
-        p1[1] -= lams * dir[s][1];
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] /= lam0;
-      double si0 = 0.0;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        double t = 0.0;
-#pragma unroll
-        for (int q = 0; q < K; ++q) t += soi[(k * K + q) * 32 + slot] * p1[q];
-        si0 += p1[k] * t;
-      }
-      const double o00 = soi[slot], o01 = soi[32 + slot], o10 = soi[K * 32 + slot], o11 = soi[(K + 1) * 32 + slot];
-      double sis[NF];
-      double tau = 0.0;
-#pragma unroll
-      for (int s = 0; s < NF; ++s) {
-        const double a0 = dir[s][0], a1 = dir[s][1];
-        sis[s] = o00 * a0 * a0 + (o01 + o10) * a0 * a1 + o11 * a1 * a1;
-        tau += fabs(sis[s] - si0);
-      }
-      tau /= (st1 - 1);
-      tau = tau_pow(tau, ph.weno_b);
-      double om0 = lam0 * (1.0 + tau / (ph.weno_eps + si0));
-      double oms[NF];
-      double wsum = om0;
-#pragma unroll
-      for (int s = 0; s < NF; ++s) {
-        oms[s] = lams * (1.0 + tau / (ph.weno_eps + sis[s]));
-        wsum += oms[s];
-      }
-      om0 /= wsum;
-#pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
-#pragma unroll
-      for (int s = 0; s < NF; ++s) {
-        const double w = oms[s] / wsum;
-        p1[0] += w * dir[s][0];
-        p1[1] += w * dir[s][1];
-      }
-#pragma unroll
-      for (int lq = 0; lq < Q; ++lq) {
-        vals[lq] = u0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) vals[lq] += p1[k] * sph[(lq * K + k) * 32 + slot];
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) kd[k] = p1[k];
-      if (flags & FL_FALLBACK) {
-#pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          const int nb = snb[j * 32 + slot];
-          if (nb >= 0) {
-            const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
-            lo = smin(lo, x);
-            hi = smax(hi, x);
-          }
-        }
-      }
-    } else {
-      // ---- MUSCL (solver.cpp:189-221, reconstruct.cpp:30-86)
-      const int* sid = reinterpret_cast<const int*>(b);
-      const double* spl = reinterpret_cast<const double*>(b + St::M_IDX);
-      const double* sp01 = reinterpret_cast<const double*>(b + St::M_IDX + St::M_PLIN);
-      const int* snb = reinterpret_cast<const int*>(b + St::M_IDX + St::M_PLIN + St::M_PHI);
-      double um[MM];
-#pragma unroll
-      for (int m = 0; m < MM; ++m) um[m] = __ldg(Ud + 4 * static_cast<size_t>(sid[m * 32 + slot]) + v);
-      double l0 = 0.0, l1 = 0.0;
-#pragma unroll
-      for (int m = 0; m < MM; ++m) {
-        const double d = um[m] - u0;
-        l0 += spl[(m * 2 + 0) * 32 + slot] * d;
-        l1 += spl[(m * 2 + 1) * 32 + slot] * d;
-      }
-#pragma unroll
-      for (int j = 0; j < NF; ++j) {
-        const int nb = snb[j * 32 + slot];
-        if (nb >= 0) {
-          const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
-          lo = smin(lo, x);
-          hi = smax(hi, x);
-        }
-      }
-      double theta = 1.0;
-      const double eps2 = venkat ? L.eps2[cc] : 0.0;
-#pragma unroll
-      for (int lq = 0; lq < Q; ++lq) {
-        const double p0 = sp01[(lq * 2 + 0) * 32 + slot], pq1 = sp01[(lq * 2 + 1) * 32 + slot];
-        const double qv = u0 + l0 * p0 + l1 * pq1;
-        theta = venkat ? venkat_update(theta, u0, lo, hi, qv, eps2) : bj_update(theta, u0, lo, hi, qv);
-      }
-      if (!venkat) theta = smax(theta, 0.0);
-      const double d0 = theta * l0, d1 = theta * l1;
-#pragma unroll
-      for (int lq = 0; lq < Q; ++lq) {
-        double o = u0;
-        o += d0 * sp01[(lq * 2 + 0) * 32 + slot];
-        o += d1 * sp01[(lq * 2 + 1) * 32 + slot];
-        vals[lq] = o;  // dofs k >= 2 are zero: adding 0*phi leaves o unchanged
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) kd[k] = k == 0 ? d0 : (k == 1 ? d1 : 0.0);
-    }
-    bool demote = false;
-    if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);
-    if (mine) {
-#pragma unroll
-      for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(__ldg(L.dest + aos(c, lq, Q))) + v] = demote ? u0 : vals[lq];
-      if (demote && v == 0) S.labels[c] = 3;
-      if (flags & FL_TAPS) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = demote ? 0.0 : kd[k];
-      }
-    }
-    __syncthreads();  // stage `st` fully consumed before it is refilled
-  }
-}
-
-// k_troubled_split: k_troubled_tma with split-phase refill (one stage, two
-// mbarriers). Group A of the next work item is requested as soon as the
+// k_troubled_split: the CWENOZ and MUSCL reconstructions of one stage in one
+// persistent launch over the chunk lists built by k_spread (FL_CHUNKS): items
+// [0, nC) are CWENOZ chunks, [nC, nC + nM) MUSCL chunks; the scheme is uniform
+// per block iteration, lanes of cells outside the chunk's mask idle through
+// the (shuffle-synchronous) math and store nothing. Split-phase refill (one
+// stage, two mbarriers). Group A of the next work item is requested as soon as the
 // directional (CWENOZ) or linear (MUSCL) solves of the current item have read
 // it, so its copy overlaps the blend / limiter / evaluation / fallback; group
 // B is requested once the evaluation and the fallback bounds are done.
-// Arithmetic is identical to k_troubled_tma.
+// Arithmetic is identical to k_cwenoz / k_muscl (kernels.cuh).
 template <int K, int NQ, int NF, int MM, int MD>
 __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph, Scratch S,
                                                            const double4* __restrict__ U, int flags) {

@@ -18,6 +18,7 @@
 
 #include "kernels.cuh"
 #include "kernels_tma.cuh"
+#include "kernels_cells.cuh"
 #include "layout.hpp"
 #include "decompose.hpp"
 #include "solver.hpp"
@@ -79,31 +80,28 @@ struct KernelSet {
   // TMA-staged persistent central kernel (fast path); grid filled in at create
   bool central_tma = false;
   using Launch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
-  void (*central_tma_setup)(int n_sm, int stages, int* grid, Launch* launch) = nullptr;
+  void (*central_tma_setup)(int n_sm, int* grid, Launch* launch) = nullptr;
   int central_tma_grid = 0;
   // TMA-staged persistent CWENOZ+MUSCL kernel over chunk lists (fast path)
   Launch troubled = nullptr;
-  void (*troubled_setup)(int n_sm, int stages, int* grid, Launch* launch) = nullptr;
+  void (*troubled_setup)(int n_sm, int* grid, Launch* launch) = nullptr;
   int troubled_grid = 0;
+  // per-cell-record CWENOZ+MUSCL kernel over dense cell lists (fast path)
+  Launch cells = nullptr;
+  void (*cells_setup)(int n_sm, int* grid, Launch* launch) = nullptr;
+  int cells_grid = 0;
+  void (*pack_records)(cudaStream_t, const Layout&, unsigned char*, unsigned char*, unsigned char*,
+                       unsigned char*) = nullptr;
+  uint32_t rec_bytes[4] = {0, 0, 0, 0};  // CA, CB, MA, MB per cell
 };
 
 using StageLaunch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
 
-template <typename St>
-constexpr uint32_t tma_smem(int stages) { return stages * St::BYTES + 16 * stages; }
-
-template <int K, int NQ, int NF, int MM, int NS>
+template <int K, int NQ, int NF, int MM>
 void central_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                           const double4* U, int f) {
-  launch_k(k_central_tma<K, NQ, NF, MM, NS>, g, dim3(kBlock), tma_smem<CentralStage<K, NQ, NF, MM>>(NS), st, L, p, S,
+  launch_k(k_central_tma<K, NQ, NF, MM, 1>, g, dim3(kBlock), CentralStage<K, NQ, NF, MM>::BYTES + 16, st, L, p, S,
            U, f);
-}
-
-template <int K, int NQ, int NF, int MM, int MD, int NS>
-void troubled_tma_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
-                           const double4* U, int f) {
-  launch_k(k_troubled_tma<K, NQ, NF, MM, MD, NS>, g, dim3(kBlock), tma_smem<TroubledStage<K, NQ, NF, MM, MD>>(NS), st,
-           L, p, S, U, f);
 }
 
 template <int K, int NQ, int NF, int MM, int MD>
@@ -113,18 +111,20 @@ void troubled_split_launcher(dim3 g, cudaStream_t st, const Layout& L, const Phy
            TroubledStage<K, NQ, NF, MM, MD>::SPLIT_BYTES + 16, st, L, p, S, U, f);
 }
 
-// pick the stage count (1..3), raise the dynamic smem limit, size the persistent grid
-template <typename St, typename Kfn>
-void tma_setup(int n_sm, int stages, int* grid, StageLaunch* launch, StageLaunch l1, StageLaunch l2, StageLaunch l3,
-               Kfn k1, Kfn k2, Kfn k3) {
-  stages = std::max(1, std::min(3, stages));
-  const uint32_t smem = tma_smem<St>(stages);
-  Kfn k = stages == 1 ? k1 : stages == 2 ? k2 : k3;
-  *launch = stages == 1 ? l1 : stages == 2 ? l2 : l3;
+template <int K, int NQ, int NF, int MM, int MD>
+void troubled_cells_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
+                             const double4* U, int f) {
+  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(kBlock), CellRec<K, NQ, NF, MM, MD>::BYTES + 16, st, L, p,
+           S, U, f);
+}
+
+// raise the dynamic smem limit and size the persistent grid (resident blocks x SMs)
+template <typename Kfn>
+int persistent_grid(Kfn k, uint32_t smem, int n_sm) {
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, smem));
-  *grid = std::max(1, per_sm) * n_sm;
+  return std::max(1, per_sm) * n_sm;
 }
 
 template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
@@ -155,33 +155,28 @@ KernelSet make_set() {
   s.faces_per_flux_block = (kBlock / 32) * (32 / NQ);
   if constexpr (MMT > 0 && UNI) {
     s.central_tma = true;
-    s.central_tma_setup = [](int n_sm, int stages, int* grid, void (**launch)(dim3, cudaStream_t, const Layout&,
-                                                                              const Physics&, const Scratch&,
-                                                                              const double4*, int)) {
-      tma_setup<CentralStage<K, NQ, NF, MMT>>(n_sm, stages, grid, launch, central_tma_launcher<K, NQ, NF, MMT, 1>,
-                                             central_tma_launcher<K, NQ, NF, MMT, 2>,
-                                             central_tma_launcher<K, NQ, NF, MMT, 3>, k_central_tma<K, NQ, NF, MMT, 1>,
-                                             k_central_tma<K, NQ, NF, MMT, 2>, k_central_tma<K, NQ, NF, MMT, 3>);
+    s.central_tma_setup = [](int n_sm, int* grid, KernelSet::Launch* launch) {
+      *grid = persistent_grid(k_central_tma<K, NQ, NF, MMT, 1>, CentralStage<K, NQ, NF, MMT>::BYTES + 16, n_sm);
+      *launch = central_tma_launcher<K, NQ, NF, MMT>;
     };
-    s.troubled_setup = [](int n_sm, int stages, int* grid, void (**launch)(dim3, cudaStream_t, const Layout&,
-                                                                           const Physics&, const Scratch&,
-                                                                           const double4*, int)) {
-      if (stages == 0) {  // split-phase single stage
-        using St = TroubledStage<K, NQ, NF, MMT, MDT>;
-        auto k = k_troubled_split<K, NQ, NF, MMT, MDT>;
-        CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, St::SPLIT_BYTES + 16));
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, St::SPLIT_BYTES + 16));
-        *grid = std::max(1, per_sm) * n_sm;
-        *launch = troubled_split_launcher<K, NQ, NF, MMT, MDT>;
-        return;
-      }
-      tma_setup<TroubledStage<K, NQ, NF, MMT, MDT>>(
-          n_sm, stages, grid, launch, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 1>,
-          troubled_tma_launcher<K, NQ, NF, MMT, MDT, 2>, troubled_tma_launcher<K, NQ, NF, MMT, MDT, 3>,
-          k_troubled_tma<K, NQ, NF, MMT, MDT, 1>, k_troubled_tma<K, NQ, NF, MMT, MDT, 2>,
-          k_troubled_tma<K, NQ, NF, MMT, MDT, 3>);
+    s.troubled_setup = [](int n_sm, int* grid, KernelSet::Launch* launch) {
+      *grid = persistent_grid(k_troubled_split<K, NQ, NF, MMT, MDT>,
+                              TroubledStage<K, NQ, NF, MMT, MDT>::SPLIT_BYTES + 16, n_sm);
+      *launch = troubled_split_launcher<K, NQ, NF, MMT, MDT>;
     };
+    using R = CellRec<K, NQ, NF, MMT, MDT>;
+    s.cells_setup = [](int n_sm, int* grid, KernelSet::Launch* launch) {
+      *grid = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT>, R::BYTES + 16, n_sm);
+      *launch = troubled_cells_launcher<K, NQ, NF, MMT, MDT>;
+    };
+    s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* ca, unsigned char* cb, unsigned char* ma,
+                        unsigned char* mb) {
+      k_pack_records<K, NQ, NF, MMT, MDT><<<(L.n + 255) / 256, 256, 0, st>>>(L, ca, cb, ma, mb);
+    };
+    s.rec_bytes[0] = R::CA;
+    s.rec_bytes[1] = R::CB;
+    s.rec_bytes[2] = R::MA;
+    s.rec_bytes[3] = R::MB;
   }
   return s;
 }
@@ -362,6 +357,11 @@ struct GpuSolver::Impl {
         ks.troubled(dim3(std::min(ks.troubled_grid, (L.n + 31) / 32)), stream, L, ph, S, U,
                     FL_NAD | FL_FALLBACK | taps);
         nl += 3;
+      } else if (ks.cells) {
+        ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
+        record(2);
+        ks.cells(dim3(std::min(ks.cells_grid, (L.n + 31) / 32 + 2)), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+        nl += 3;
       } else {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
         record(2);
@@ -498,6 +498,10 @@ struct GpuSolver::Impl {
       nl += launch_stage(ud, false, e, census, with_dt);
       nl += exchange(dst);
     }
+    // inside the step (graph): a failure on any rank stops every rank's later
+    // kernels (they exit on a set error word), so no rank writes past the
+    // failing step and all can return to its input state
+    nl += allreduce_error();
     return nl;
   }
 
@@ -527,6 +531,9 @@ struct GpuSolver::Impl {
     return e[0];
   }
 
+  // the tie count covers one public call (include/ucfvb.h: ucfvb_get_nad_ties)
+  void reset_ties() { CK(cudaMemsetAsync(S.ties, 0, sizeof(unsigned long long), stream)); }
+
   void reset_error() {
     const int e[4] = {0, INT_MAX, INT_MAX, INT_MAX};
     CK(cudaMemcpyAsync(S.err, e, sizeof e, cudaMemcpyHostToDevice, stream));
@@ -545,14 +552,44 @@ struct GpuSolver::Impl {
     }
   }
 
-  // every rank learns that some rank failed (the kinds are OR-ed via max of bits)
-  void allreduce_error() {
-    if (comm) NK(nccl().AllReduce(S.err, S.err, 1, ncclInt32, ncclMax, comm, stream));
+  // every rank learns the job's error word: the kind by max (the kind bits of
+  // one step are exclusive), the failing step / face / cell by min, so every
+  // rank rolls back to the same step (run_impl, advance_host)
+  int64_t allreduce_error() {
+    if (!comm) return 0;
+    NK(nccl().GroupStart());
+    NK(nccl().AllReduce(S.err, S.err, 1, ncclInt32, ncclMax, comm, stream));
+    NK(nccl().AllReduce(S.err + 1, S.err + 1, 3, ncclInt32, ncclMin, comm, stream));
+    NK(nccl().GroupEnd());
+    return 0;
   }
 
   void check_after() {
     int k, f, c;
     if (read_error(&k, &f, &c)) raise_device_error(k, f, c);
+  }
+
+  // Owns every resource, so a constructor that throws half-way (unsupported
+  // order, out of memory) releases what it had acquired through unique_ptr.
+  size_t l2_limit_before = 0;
+  bool l2_limit_set = false;
+  ~Impl() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (auto& a : graph)
+      for (auto& b : a)
+        for (auto& g : b)
+          if (g) cudaGraphExecDestroy(g);
+    if (comm) nccl().CommDestroy(comm);
+    for (void* p : owned) cudaFree(p);
+    if (census_dev) cudaFree(census_dev);
+    if (dtlog_dev) cudaFree(dtlog_dev);
+    if (host_stage) cudaFreeHost(host_stage);
+    if (hcounts) cudaFreeHost(hcounts);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    // the persisting-L2 carve-out is device-wide: give back what we raised
+    if (l2_limit_set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, l2_limit_before);
   }
 };
 
@@ -617,10 +654,9 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   CK(cudaMallocHost(&I.hcounts, 4 * sizeof(int)));
   std::memset(I.hcounts, 0, 4 * sizeof(int));
   if (I.ks.central_tma) {
-    const char* e1 = std::getenv("UCFVB_TMA_STAGES_CENTRAL");
-    const char* e2 = std::getenv("UCFVB_TMA_STAGES_TROUBLED");
-    I.ks.central_tma_setup(I.n_sm, e1 ? std::atoi(e1) : 1, &I.ks.central_tma_grid, &I.ks.central);
-    I.ks.troubled_setup(I.n_sm, e2 ? std::atoi(e2) : 0, &I.ks.troubled_grid, &I.ks.troubled);
+    I.ks.central_tma_setup(I.n_sm, &I.ks.central_tma_grid, &I.ks.central);
+    I.ks.troubled_setup(I.n_sm, &I.ks.troubled_grid, &I.ks.troubled);
+    I.ks.cells_setup(I.n_sm, &I.ks.cells_grid, &I.ks.cells);
   }
   auto& own = I.owned;
   Layout& L = I.L;
@@ -651,6 +687,16 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   L.eps2 = dupload(H.eps2, own);
   L.h = dupload(H.h, own);
   L.inv_vol = dupload(H.inv_vol, own);
+  if (I.ks.pack_records) {  // per-cell records of the troubled-cell rows (kernels_cells.cuh)
+    unsigned char* rec[4];
+    for (int i = 0; i < 4; ++i) rec[i] = dalloc<unsigned char>(static_cast<size_t>(H.n) * I.ks.rec_bytes[i], own);
+    L.rec_ca = rec[0];
+    L.rec_cb = rec[1];
+    L.rec_ma = rec[2];
+    L.rec_mb = rec[3];
+    I.ks.pack_records(I.stream, L, rec[0], rec[1], rec[2], rec[3]);
+    CK(cudaGetLastError());
+  }
 
   // the operator data now lives on the device: keep only what the taps need
   {
@@ -697,6 +743,8 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
       size_t limit = 0;
       CK(cudaDeviceGetLimit(&limit, cudaLimitPersistingL2CacheSize));
       const size_t persist = std::min<size_t>(max_persist, std::max(limit, bytes));
+      I.l2_limit_before = limit;
+      I.l2_limit_set = true;
       CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, persist));
       cudaStreamAttrValue attr{};
       attr.accessPolicyWindow.base_ptr = stage_buf;
@@ -747,24 +795,7 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   CK(cudaStreamSynchronize(I.stream));
 }
 
-GpuSolver::~GpuSolver() {
-  if (!p_) return;
-  Impl& I = *p_;
-  cudaStreamSynchronize(I.stream);
-  for (auto& a : I.graph)
-    for (auto& b : a)
-      for (auto& g : b)
-        if (g) cudaGraphExecDestroy(g);
-  if (I.comm) nccl().CommDestroy(I.comm);
-  for (void* p : I.owned) cudaFree(p);
-  if (I.census_dev) cudaFree(I.census_dev);
-  if (I.dtlog_dev) cudaFree(I.dtlog_dev);
-  if (I.host_stage) cudaFreeHost(I.host_stage);
-  if (I.hcounts) cudaFreeHost(I.hcounts);
-  for (auto& e : I.ev)
-    if (e) cudaEventDestroy(e);
-  if (I.stream) cudaStreamDestroy(I.stream);
-}
+GpuSolver::~GpuSolver() = default;  // Impl::~Impl releases everything
 
 int GpuSolver::n_cells() const { return p_->L.n; }
 int GpuSolver::n_faces() const { return p_->host.n_faces; }
@@ -815,6 +846,7 @@ void GpuSolver::advance(double dt, double t, int rk) {
   h.t_end = INFINITY;
   h.cfl = I.opt.cfl;
   CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
+  I.reset_ties();
   I.S.step = I.step_zero;
   I.stage_is_first = true;  // Solver::advance (solver.cpp:382)
   if (I.opt.use_graphs && !I.timing) {
@@ -840,6 +872,7 @@ void GpuSolver::compute_residual(const double* u, double t, double* out) {
   RkEpilogue e{};
   e.rhs_out = I.rhs;
   e.dt = &I.ds->dt;
+  I.reset_ties();
   I.launches = I.launch_stage(in, I.stage_is_first, e, false);
   I.stage_is_first = false;
   int k, f, c;
@@ -889,6 +922,7 @@ double GpuSolver::run_impl(int n_steps, int rk, double t0, double t_end, bool un
   h.dt_log = dt_out ? I.dtlog_dev : nullptr;
   h.until = until ? 1 : 0;
   CK(cudaMemcpyAsync(I.ds, &h, sizeof h, cudaMemcpyHostToDevice, I.stream));
+  I.reset_ties();
   // census rows are indexed by the device step counter
   I.S.census = census ? I.census_dev : nullptr;
   I.S.step = &I.ds->step;
@@ -983,6 +1017,7 @@ double GpuSolver::advance_host(const double* u_in, double* u_out, int n_steps, i
   hs->t_end = INFINITY;
   hs->cfl = I.opt.cfl;
   CK(cudaMemcpyAsync(I.ds, hs, sizeof(DtState), cudaMemcpyHostToDevice, I.stream));
+  I.reset_ties();
   I.S.step = &I.ds->step;
   const int cur0 = I.cur;
   int64_t nl = I.launch_dt_reduce(I.ubuf[I.cur]);

@@ -46,6 +46,11 @@ namespace {
 constexpr int V5 = 5;
 constexpr int MD3 = 6;
 constexpr int kCwList = 0, kMuList = 1, kBadFace = 2, kBadCell = 3, kCnt0 = 4;
+// counters[kHalt] != 0 once a recorded failure has been seen by a later
+// kernel: every state-writing kernel and every error-recording kernel after
+// that exits, so the failing kernel's min face / cell stays deterministic and
+// U stays at the failing step's input (the reference throws before touching state_)
+constexpr int kHalt = 0;
 
 #define CK3(x)                                                                                      \
   do {                                                                                              \
@@ -163,7 +168,7 @@ struct Work3 {
   uint8_t* raw;      // raw label | prefail << 2
   uint8_t* labels;
   int32_t* lists;    // [2][ntl][cap] class lists (ntl = 1, or one per lattice type when staged)
-  int32_t* counters; // [0..1] unused, bad face, bad cell, then [4 + L*ntl + t] list lengths
+  int32_t* counters; // [0] halt, [1] unused, bad face, bad cell, then [4 + L*ntl + t] list lengths
   int ntl, cap;
   unsigned long long* dtmin;
   double* dt;        // device dt of the current step
@@ -171,6 +176,16 @@ struct Work3 {
   unsigned long long* ties;
 };
 __device__ __forceinline__ int cnt_idx(const Work3& W, int L, int t) { return kCnt0 + L * W.ntl + t; }
+__device__ __forceinline__ bool halted(const Work3& W) { return *(volatile int32_t*)&W.counters[kHalt] != 0; }
+// a failure recorded by an earlier kernel: raise the halt flag (idempotent)
+__device__ __forceinline__ bool failed_before(const Work3& W) {
+  const volatile int32_t* c = W.counters;
+  if (c[kBadFace] != 0x7fffffff || c[kBadCell] != 0x7fffffff) {
+    if (threadIdx.x == 0) W.counters[kHalt] = 1;
+    return true;
+  }
+  return c[kHalt] != 0;
+}
 __device__ __forceinline__ int32_t* list_of(const Work3& W, int L, int t) {
   return W.lists + (static_cast<size_t>(L) * W.ntl + t) * W.cap;
 }
@@ -1034,7 +1049,7 @@ __global__ void k3_constant(Dev3 D, Work3 W, const double* __restrict__ U) {
 template <int NQ>
 __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
-  if (f >= D.nF) return;
+  if (f >= D.nF || halted(W)) return;
   double tot[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
   bool ok = true;
   if (D.fown && D.fown[f] == 2) {  // subdomain boundary face of a halo cell: no flux, never owned
@@ -1067,6 +1082,7 @@ template <int NQ>
 __global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3 W) {
   constexpr int LP = NQ <= 1 ? 1 : (NQ <= 2 ? 2 : (NQ <= 4 ? 4 : 8));  // lanes per face (NQ <= 8)
   static_assert(NQ <= 8, "at most 8 points per face");
+  if (halted(W)) return;  // block-uniform
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   const int f0 = g / LP, q0 = g % LP;
   const bool in = f0 < D.nF;
@@ -1107,6 +1123,7 @@ __global__ void __launch_bounds__(256) k3_gather_rk(Dev3 D, Work3 W, const doubl
                                                     const double* __restrict__ ub, double* __restrict__ out,
                                                     double* __restrict__ res_out, double wa, double wb, double wr,
                                                     int combine) {
+  if (failed_before(W)) return;  // block-uniform
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= D.n) return;
   double acc[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
@@ -1137,8 +1154,9 @@ __global__ void __launch_bounds__(256) k3_gather_rk(Dev3 D, Work3 W, const doubl
 }
 
 // SSPRK(5,4) final combination (time_integrator.cpp:66-73)
-__global__ void k3_rk54_final(int64_t N, double* u, const double* ub, const double* uc, const double* rhs3,
+__global__ void k3_rk54_final(Work3 W, int64_t N, double* u, const double* ub, const double* uc, const double* rhs3,
                               const double* ud, const double* rhs, const double* dtp) {
+  if (failed_before(W)) return;  // block-uniform: U keeps the failing step's input
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= N) return;
   const double dt = dtp[0];
@@ -1147,8 +1165,16 @@ __global__ void k3_rk54_final(int64_t N, double* u, const double* ub, const doub
   u[i] = c52 * ub[i] + c53 * uc[i] + a53 * dt * rhs3[i] + c54 * ud[i] + a54 * dt * rhs[i];
 }
 
+// SSP-RK3 final stage result (written out of place) -> U, owned cells, when no failure was recorded
+__global__ void k3_commit(Work3 W, int64_t N, double* __restrict__ u, const double* __restrict__ src) {
+  if (failed_before(W)) return;  // block-uniform
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < N) u[i] = src[i];
+}
+
 // ---- max_stable_dt (solver.cpp:103-111) ----------------------------------------------------
 __global__ void __launch_bounds__(256) k3_dt(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+  if (halted(W)) return;  // block-uniform
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   double dt = 1e300;
   if (c < D.n_owned) {
@@ -1178,9 +1204,15 @@ __global__ void k3_halo_pack(const double* __restrict__ U, const int32_t* __rest
 
 __global__ void k3_dt_init(Work3 W) { *W.dtmin = static_cast<unsigned long long>(__double_as_longlong(1e300)); }
 
-__global__ void k3_dt_finalize(Work3 W, double cfl) { W.dt[0] = cfl * __longlong_as_double(static_cast<long long>(*W.dtmin)); }
+__global__ void k3_dt_finalize(Work3 W, double cfl) {
+  if (failed_before(W)) return;
+  W.dt[0] = cfl * __longlong_as_double(static_cast<long long>(*W.dtmin));
+}
 
-__global__ void k3_time_add(Work3 W) { *W.t += W.dt[0]; }
+__global__ void k3_time_add(Work3 W) {
+  if (failed_before(W)) return;
+  *W.t += W.dt[0];
+}
 
 // ---- dispatch ----------------------------------------------------------------------------------
 struct Kern3 {
@@ -1336,7 +1368,7 @@ struct GpuSolver3::Impl {
   }
 
   void launch_stage(const double* Us, bool first, double* out, const double* wa_src, const double* wb_src,
-                    double wa, double wb, double wr, double* res, int combine) {
+                    double wa, double wb, double wr, double* res, int combine, bool xchg = true) {
     const int mode = o.mode;
     const bool nad = mode == UCFVB_HYBRID;
     const int nblk = (n + 255) / 256;
@@ -1383,17 +1415,25 @@ struct GpuSolver3::Impl {
     mark(4);
     kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine);
     launches += 2;
-    if (combine && out) exchange(out);
+    if (combine && out && xchg) exchange(out);
     mark(5);
     collect();
   }
 
   // one RK step on the device state U with the device dt W.dt
+  // The step's result reaches U only through a final kernel gated on the
+  // (all-reduced) error counters: k3_commit (RK3, last stage written out of
+  // place into uc) or k3_rk54_final.
   void step(int rk) {
+    const int64_t NO = static_cast<int64_t>(n_owned) * V5;
     if (rk == UCFVB_RK3) {
       launch_stage(U, true, ua, U, U, 1.0, 0.0, 1.0, nullptr, 1);
       launch_stage(ua, false, ub, U, ua, 0.75, 0.25, 0.25, nullptr, 1);
-      launch_stage(ub, false, U, U, ub, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, nullptr, 1);
+      launch_stage(ub, false, uc, U, ub, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, nullptr, 1, false);
+      allreduce_errors();
+      k3_commit<<<static_cast<unsigned>((NO + 255) / 256), 256, 0, st>>>(W, NO, U, uc);
+      ++launches;
+      exchange(U);
       return;
     }
     const double a10 = 0.391752226571890;
@@ -1405,10 +1445,16 @@ struct GpuSolver3::Impl {
     launch_stage(ub, false, uc, U, ub, b30, b32, a32, nullptr, 1);
     launch_stage(uc, false, ud, U, uc, b40, b43, a43, rhs3, 1);
     launch_stage(ud, false, nullptr, nullptr, nullptr, 0, 0, 0, rhs, 0);
-    const int64_t N = static_cast<int64_t>(n) * V5;
-    k3_rk54_final<<<static_cast<unsigned>((N + 255) / 256), 256, 0, st>>>(N, U, ub, uc, rhs3, ud, rhs, W.dt);
+    allreduce_errors();
+    k3_rk54_final<<<static_cast<unsigned>((NO + 255) / 256), 256, 0, st>>>(W, NO, U, ub, uc, rhs3, ud, rhs, W.dt);
     ++launches;
     exchange(U);
+  }
+
+  // every rank learns the job's failures (min face / cell) before any rank
+  // commits the step, so all ranks keep the failing step's input
+  void allreduce_errors() {
+    if (comm) NK(nccl().AllReduce(W.counters + kBadFace, W.counters + kBadFace, 2, ncclInt32, ncclMin, comm, st));
   }
 
   void dt_kernels() {
@@ -1439,8 +1485,9 @@ struct GpuSolver3::Impl {
   }
 
   void reset_errors() {
-    const int32_t init[2] = {0x7fffffff, 0x7fffffff};
-    CK3(cudaMemcpyAsync(W.counters + 2, init, sizeof init, cudaMemcpyHostToDevice, st));
+    const int32_t init[4] = {0, 0, 0x7fffffff, 0x7fffffff};  // halt, -, bad face, bad cell
+    std::memcpy(h_counters, init, sizeof init);
+    CK3(cudaMemcpyAsync(W.counters, h_counters, sizeof init, cudaMemcpyHostToDevice, st));
   }
 
   void check_errors() {
@@ -1720,10 +1767,8 @@ double GpuSolver3::advance_host(const double* u_in, double* u_out, int n_steps, 
   CK3(cudaSetDevice(I.device));
   const size_t bytes = sizeof(double) * static_cast<size_t>(I.n) * V5;
   CK3(cudaMemcpyAsync(I.U, u_in, bytes, cudaMemcpyHostToDevice, I.st));
-  const int32_t init[2] = {0x7fffffff, 0x7fffffff};
-  std::memcpy(I.h_counters + 2, init, sizeof init);
+  I.reset_errors();
   I.h_dt[1] = t0;
-  CK3(cudaMemcpyAsync(I.W.counters + 2, I.h_counters + 2, sizeof init, cudaMemcpyHostToDevice, I.st));
   CK3(cudaMemcpyAsync(I.W.t, &I.h_dt[1], sizeof(double), cudaMemcpyHostToDevice, I.st));
   if (!I.timing && (!I.step_graph || I.graph_rk != rk)) I.capture(rk);
   for (int i = 0; i < n_steps; ++i) {

@@ -17,7 +17,8 @@ INT_FIELDS = {"order", "mode", "limiter", "riemann", "si_exponent", "detect_ever
 
 
 def names():
-    return sorted(p.stem for p in GOLDEN.glob("*.npz"))
+    # fullsize_*.npz are digests of full-length reference runs (tests/golden/make_fullsize_refs.py), not stage fixtures
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if not p.stem.startswith("fullsize_"))
 
 
 class Fixture:

@@ -144,6 +144,25 @@ def test_forced_cwenoz_blast_fails_at_same_face():
     assert f"face {face}" in str(ec.value)
 
 
+@pytest.mark.parametrize("rk", [A.RK3, A.RK54], ids=["rk3", "rk54"])
+def test_failure_keeps_failing_step_input3(rk):
+    """A non-physical failure inside a graph-replayed run leaves U at the
+    failing step's input (the reference throws before touching state_): the
+    step's result reaches U only through a commit gated on the error word,
+    and every later kernel of the run exits."""
+    m, st, o, u0, gpu, cpu = build(HEX, 2, 0.05, IC_BLAST, mode="cwenoz")
+    gpu.state = u0
+    with pytest.raises(A.NonPhysicalError, match="face"):
+        gpu.run_steps(4, rk=rk)
+    np.testing.assert_array_equal(gpu.state, u0)
+    bad = u0.copy()
+    bad[11, 0] = -1.0
+    gpu.state = bad
+    with pytest.raises(A.NonPhysicalError, match="cell 11"):
+        gpu.run_steps(3, rk=rk)
+    np.testing.assert_array_equal(gpu.state, bad)
+
+
 def test_nonphysical_reports_face():
     m, st, o, u0, gpu, cpu = build(HEX, 2, 0.0, IC_BLAST, mode="first")
     u = u0.copy()

@@ -3,6 +3,8 @@
 * Config 2 (262,144 cells): against the compiled reference (oracle/_ref) on the
   same mesh/seed -- one stage (labels identical, residual within 1e-10) and
   two SSP-RK3 steps (census identical, L1 within 1e-8).
+* Configs 2 and 3 for their configured step counts (200 / 50) against the
+  committed record of the reference's own full-length run.
 * Config 3 (8,388,608 cells, p=3): size-independent properties -- discrete
   conservation on the fully periodic domain, run-to-run bit-determinism, and
   (at quarter scale) a 4-subdomain decomposition reproducing the single-domain
@@ -51,6 +53,53 @@ def test_config2_full_size_against_reference():
     np.testing.assert_array_equal(cen_gpu, cen_ref)
     ug, ur = g.state, rs.get_state()
     assert np.sum(np.abs(ug - ur)) / np.sum(np.abs(ur)) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["config2", "config3"])
+def test_full_length_against_reference_run(name):
+    """The configured step count at full size against the committed record of
+    the compiled reference's own run (tests/golden/make_fullsize_refs.py;
+    reference loop run.cpp:97-132 over solver.cpp:316-379): identical input
+    state, the census of step labels identical on EVERY step, dt equal every
+    step, and the final conserved variables within L1 1e-8 (relative, per
+    variable, on the stored 65,536-cell sample; per-variable L1 norms and
+    1024 block sums likewise)."""
+    import json
+    from pathlib import Path
+
+    from tests.fullsize_digest import sha256, summarise
+
+    gold = Path(__file__).resolve().parent / "golden"
+    if not (gold / f"fullsize_{name}.npz").exists():
+        pytest.skip(f"no committed reference run for {name}")
+    meta = json.loads((gold / f"fullsize_{name}.json").read_text())
+    ref = np.load(gold / f"fullsize_{name}.npz")
+    mk, order, ic, prm, opts, bcs, mesh, st, u0 = product_case(name)
+    assert mesh.n_cells == meta["cells"]
+    assert sha256(u0) == meta["u0_sha256"]  # the product setup reproduces the reference's initial state
+    o = A.options_from_dict(order=order, **opts)
+    g = Solver(mesh, o, make_bcs(bcs), stencils=st)
+    del st
+    g.state = u0
+    n = meta["steps"]
+    t, cen, dts = g.run_log(n, A.RK3)
+    ties = g.nad_ties()
+    np.testing.assert_array_equal(cen, ref["census"])
+    # dt is a min over cells of the state: bit-equal while the states are; the
+    # tau^b ulp differences of CWENOZ cells may move it in the last bits
+    assert np.max(np.abs(dts - ref["dt"]) / ref["dt"]) <= 1e-12
+    assert abs(t - float(ref["t"])) <= 1e-12 * float(ref["t"])
+    u = g.state
+    idx = ref["sample_idx"]
+    us, ur = u[idx], ref["sample_state"]
+    l1 = np.abs(us - ur).sum(0) / np.abs(ur).sum(0)
+    assert np.all(l1 <= 1e-8), l1
+    dg = summarise(u)
+    assert np.all(np.abs(dg["l1"] - ref["l1"]) <= 1e-8 * ref["l1"])
+    assert np.all(np.abs(dg["block_sum"] - ref["block_sum"]) <= 1e-8 * ref["block_abs"])
+    print(f"{name}: {n} steps, census identical, max dt rel diff "
+          f"{np.max(np.abs(dts - ref['dt']) / ref['dt']):.2e}, sample L1 rel {l1.max():.2e}, "
+          f"final state bit-identical: {dg['sha256'] == meta['final_sha256']}, NAD ties {ties}")
 
 
 def test_config3_full_size_conservation_and_determinism():

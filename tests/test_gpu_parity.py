@@ -106,11 +106,17 @@ def test_stage_matches_oracle(c, kernel_path):
     assert rel_err(gpu.dofs(), cpu.dofs()) <= 1e-10 or np.allclose(gpu.dofs(), cpu.dofs(), rtol=1e-10, atol=1e-14)
 
 
-@pytest.fixture(params=["fast", "generic"])
+@pytest.fixture(params=["fast", "cells", "generic"])
 def kernel_path(request, monkeypatch):
-    """fast: compile-time stencil sizes (uniform meshes); generic: runtime sizes."""
+    """fast: compile-time stencil sizes (uniform meshes), troubled cells over
+    chunk lists; cells: the same over dense per-cell lists with per-cell
+    operator records (k_troubled_cells); generic: runtime sizes."""
     if request.param == "generic":
         monkeypatch.setenv("UCFVB_FORCE_GENERIC", "1")
+    if request.param == "cells":
+        monkeypatch.setenv("UCFVB_TROUBLED", "lists")
+    if request.param == "fast":
+        monkeypatch.setenv("UCFVB_TROUBLED", "chunks")
     return request.param
 
 

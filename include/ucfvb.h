@@ -304,8 +304,10 @@ int32_t ucfvb_n_qp(const ucfvb_solver* h);
  * the stencil-depth halo every owned residual depends on (face neighbours to
  * depth 2 for spread + NAD, then central stencils and face neighbours of those),
  * as a self-contained local mesh + stencil set. Local cells are ordered
- * [owned (global order) | halo grouped by owner rank (global order)], so each
- * peer's halo block is one contiguous receive range. Halo cells beyond the
+ * [owned interior | owned cells some peer holds | halo grouped by owner rank],
+ * each group in global order: each peer's halo block is one contiguous receive
+ * range, and the owned cells that are sent come last, so a stage updates them
+ * first and exchanges the halo while it updates the interior. Halo cells beyond the
  * classification layers carry inert (zero-weight) stencils; faces leaving the
  * local set belong to the local patch "__halo__" and are never integrated. */
 /* recursive coordinate bisection of cell centroids into n_parts balanced parts */
@@ -316,6 +318,8 @@ int32_t ucfvb_subdomain_build(const ucfvb_mesh_view* mesh, const ucfvb_stencil_v
 int32_t ucfvb_subdomain_views(const ucfvb_subdomain* s, ucfvb_mesh_view* mesh, ucfvb_stencil_view* stencils);
 /* n_owned, n_local, n_peers */
 int32_t ucfvb_subdomain_info(const ucfvb_subdomain* s, int32_t* n_owned, int32_t* n_local, int32_t* n_peers);
+/* owned cells [0, n_interior) that no peer holds (never sent) */
+int32_t ucfvb_subdomain_interior(const ucfvb_subdomain* s, int32_t* n_interior);
 /* global cell id of every local cell [n_local] */
 int32_t ucfvb_subdomain_global_ids(const ucfvb_subdomain* s, int32_t* gid);
 /* peer i: its rank, how many owned cells go to it, and the local range
@@ -336,6 +340,23 @@ int32_t ucfvb_create_sub(const ucfvb_subdomain* sub, const ucfvb_options* opt, c
  * min all-reduce, and run_steps' census a sum all-reduce. */
 int32_t ucfvb_nccl_unique_id(uint8_t id[128]);
 int32_t ucfvb_attach_nccl(ucfvb_solver* h, const uint8_t id[128], int32_t rank, int32_t world);
+
+/* In-process loopback group: the n subdomain solvers of one n-part partition
+ * (parts[i] created with ucfvb_create_sub on rank i's subdomain, all on one
+ * device), stepped together with the same schedule a rank runs -- sent cells
+ * first, the halo exchange forked onto an exchange stream while the interior
+ * is updated -- with device-to-device copies (one cudaMemcpyAsync per peer
+ * block) as the transport and the dt min / error word reduced by kernels
+ * across the group; one CUDA graph captures a step of all parts. For testing
+ * the multi-GPU exchange schedule on a single device. The parts must outlive
+ * the group and are not stepped on their own while it exists. */
+typedef struct ucfvb_group ucfvb_group;
+int32_t ucfvb_group_create(ucfvb_solver* const* parts, int32_t n, ucfvb_group** out);
+/* n_steps RK steps of every part with device dt (run_steps); on a failure
+ * every part keeps the failing step's input and the call returns its status */
+int32_t ucfvb_group_run_steps(ucfvb_group* g, int32_t n_steps, int32_t rk, double t0, double* t_out);
+int64_t ucfvb_group_launch_count(const ucfvb_group* g);
+void ucfvb_group_free(ucfvb_group* g);
 
 /* ---- device-resident entry points (benchmark "value" leg) ---------------- */
 /* device pointer to the [n_cells][4] state; valid until the next call */

@@ -349,6 +349,11 @@ def _declare(lib):
         "ucfvb_create_sub": (C.c_int32, [H, P(Options), P(BC), C.c_int32, C.c_int32, P(H)]),
         "ucfvb_nccl_unique_id": (C.c_int32, [P(C.c_uint8)]),
         "ucfvb_attach_nccl": (C.c_int32, [H, P(C.c_uint8), C.c_int32, C.c_int32]),
+        "ucfvb_subdomain_interior": (C.c_int32, [H, c_i32p]),
+        "ucfvb_group_create": (C.c_int32, [P(H), C.c_int32, P(H)]),
+        "ucfvb_group_run_steps": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, c_dp]),
+        "ucfvb_group_launch_count": (C.c_int64, [H]),
+        "ucfvb_group_free": (None, [H]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -370,7 +375,8 @@ ABI_SYMBOLS = [
     "ucfvb_state_device_ptr", "ucfvb_stream", "ucfvb_launch_count",
     "ucfvb_partition_rcb", "ucfvb_subdomain_build", "ucfvb_subdomain_views", "ucfvb_subdomain_info",
     "ucfvb_subdomain_global_ids", "ucfvb_subdomain_peer", "ucfvb_subdomain_send_list", "ucfvb_subdomain_free",
-    "ucfvb_create_sub", "ucfvb_nccl_unique_id", "ucfvb_attach_nccl",
+    "ucfvb_create_sub", "ucfvb_nccl_unique_id", "ucfvb_attach_nccl", "ucfvb_subdomain_interior",
+    "ucfvb_group_create", "ucfvb_group_run_steps", "ucfvb_group_launch_count", "ucfvb_group_free",
 ]
 
 

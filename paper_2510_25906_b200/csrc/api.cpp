@@ -6,6 +6,7 @@
 #include <exception>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "decompose.hpp"
 #include "layout.hpp"
@@ -261,6 +262,11 @@ int32_t ucfvb_subdomain_info(const ucfvb_subdomain* s, int32_t* n_owned, int32_t
   return UCFVB_OK;
 }
 
+int32_t ucfvb_subdomain_interior(const ucfvb_subdomain* s, int32_t* n_interior) {
+  *n_interior = s->n_interior;
+  return UCFVB_OK;
+}
+
 int32_t ucfvb_subdomain_global_ids(const ucfvb_subdomain* s, int32_t* gid) {
   std::memcpy(gid, s->gid.data(), s->gid.size() * sizeof(int32_t));
   return UCFVB_OK;
@@ -309,5 +315,43 @@ int32_t ucfvb_attach_nccl(ucfvb_solver* h, const uint8_t id[128], int32_t rank, 
   return guard(h, [&] { h->s->attach_nccl(id, rank, world, h->sub); });
 }
 
+struct ucfvb_group {
+  ucfvb::GpuGroup* g = nullptr;
+};
+
+int32_t ucfvb_group_create(ucfvb_solver* const* parts, int32_t n, ucfvb_group** out) {
+  *out = nullptr;
+  return guard(nullptr, [&] {
+    std::vector<ucfvb::GpuSolver*> s(n > 0 ? n : 0);
+    std::vector<const ucfvb_subdomain*> sub(s.size());
+    for (int32_t i = 0; i < n; ++i) {
+      s[i] = parts[i]->s;
+      sub[i] = parts[i]->sub;
+    }
+    auto* h = new ucfvb_group;
+    try {
+      h->g = new ucfvb::GpuGroup(s.data(), sub.data(), n);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int32_t ucfvb_group_run_steps(ucfvb_group* g, int32_t n_steps, int32_t rk, double t0, double* t_out) {
+  return guard(nullptr, [&] {
+    const double t = g->g->run_steps(n_steps, rk, t0);
+    if (t_out) *t_out = t;
+  });
+}
+
+int64_t ucfvb_group_launch_count(const ucfvb_group* g) { return g->g->launch_count(); }
+
+void ucfvb_group_free(ucfvb_group* g) {
+  if (!g) return;
+  delete g->g;
+  delete g;
+}
 
 }  // extern "C"

@@ -131,9 +131,28 @@ ucfvb_subdomain* build_subdomain(const ucfvb_mesh_view& m, const ucfvb_stencil_v
     Sets S = rank_sets(m, s, part, r);
     std::vector<int8_t> is_classify(n, 0);
     for (int c : S.classify) is_classify[c] = 1;
-    // local order: owned (global order) | halo by (owner, global id)
-    std::vector<int> owned = S.owned, halo;
+    // the owned cells some peer holds in its local set (they are sent every stage)
+    std::vector<std::vector<int>> send_g(n_parts);
+    std::vector<int8_t> sent(n, 0);
+    for (int q = 0; q < n_parts; ++q) {
+      if (q == r) continue;
+      Sets Sq = rank_sets(m, s, part, q);
+      for (int c : Sq.local)
+        if (part[c] == r) {
+          send_g[q].push_back(c);
+          sent[c] = 1;
+        }
+      std::sort(send_g[q].begin(), send_g[q].end());
+    }
+    // local order: owned interior (global order) | owned sent cells (global
+    // order) | halo by (owner, global id). The solver updates the sent cells
+    // first each stage, so the halo exchange overlaps the interior's update.
+    std::vector<int> owned, owned_sent, halo;
+    for (int c : S.owned) (sent[c] ? owned_sent : owned).push_back(c);
     std::sort(owned.begin(), owned.end());
+    std::sort(owned_sent.begin(), owned_sent.end());
+    D->n_interior = static_cast<int>(owned.size());
+    owned.insert(owned.end(), owned_sent.begin(), owned_sent.end());
     {
       std::vector<int8_t> own(n, 0);
       for (int c : owned) own[c] = 1;
@@ -284,15 +303,8 @@ ucfvb_subdomain* build_subdomain(const ucfvb_mesh_view& m, const ucfvb_stencil_v
       ++recv_count[q];
     }
     std::vector<std::vector<int32_t>> send(n_parts);
-    for (int q = 0; q < n_parts; ++q) {
-      if (q == r) continue;
-      Sets Sq = rank_sets(m, s, part, q);
-      std::vector<int> mine;
-      for (int c : Sq.local)
-        if (part[c] == r) mine.push_back(c);
-      std::sort(mine.begin(), mine.end());
-      for (int c : mine) send[q].push_back(lid[c]);
-    }
+    for (int q = 0; q < n_parts; ++q)
+      for (int c : send_g[q]) send[q].push_back(lid[c]);
     for (int q = 0; q < n_parts; ++q) {
       if (q == r || (recv_count[q] == 0 && send[q].empty())) continue;
       ucfvb_subdomain::Peer p;

@@ -9,6 +9,7 @@
 
 struct ucfvb_subdomain {
   int rank = 0, n_parts = 1, n_owned = 0, n_local = 0;
+  int n_interior = 0;  // owned cells [0, n_interior) that no peer holds (never sent)
   std::vector<int32_t> gid, part_of_local;
   // local mesh (vertices borrowed from the global view)
   std::vector<int32_t> cvp, cv, cfp, cf, fvtx, fl, fr, patch, partner, shift, pqp;

@@ -129,6 +129,7 @@ struct RkEpilogue {
   double4* out;            // nullable
   double4* rhs_out;        // nullable: store the residual itself
   const double* dt;        // device dt
+  int c_begin, c_end;      // owned cells [c_begin, c_end) of this launch (c_end 0: all owned cells)
 };
 
 __device__ __forceinline__ size_t aos(int c, int e, int E) {
@@ -855,10 +856,11 @@ __global__ void __launch_bounds__(kBlock) k_face_flux(Layout L, Physics ph, Scra
 template <int NF, bool UNI, int NT>  // NT >= rk.nterms: registers for the prefetched RK terms
 __global__ void __launch_bounds__(kBlock) k_gather_rk(Layout L, Scratch S, RkEpilogue rk, int flags, DtState* ds,
                                                       double gamma) {
-  const int c0 = blockIdx.x * kBlock + threadIdx.x;
+  const int cend = rk.c_end ? rk.c_end : L.n_owned;
+  const int c0 = rk.c_begin + blockIdx.x * kBlock + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool live = c0 < L.n_owned;
-  const int c = live ? c0 : L.n_owned - 1;
+  const bool live = c0 < cend;
+  const int c = live ? c0 : cend - 1;
   // RK terms were written by earlier stages and 1/area is static: fetched while the face kernel drains
   d4 term[NT];
 #pragma unroll

@@ -91,8 +91,14 @@ __global__ void k_pack_records(Layout L, unsigned char* ca, unsigned char* cb, u
 // Work items: tiles of 32 list entries, CWENOZ tiles [0, tc) then MUSCL tiles.
 // Four lanes per cell (lane v = conserved variable v); arithmetic identical
 // to k_troubled_split / k_cwenoz / k_muscl.
+#ifndef UCFVB_CELLS_MINB
+#define UCFVB_CELLS_MINB 1
+#endif
+#ifndef UCFVB_CELLS_PF
+#define UCFVB_CELLS_PF 0
+#endif
 template <int K, int NQ, int NF, int MM, int MD>
-__global__ void __launch_bounds__(kBlock) k_troubled_cells(Layout L, Physics ph, Scratch S,
+__global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Layout L, Physics ph, Scratch S,
                                                            const double4* __restrict__ U, int flags) {
   using R = CellRec<K, NQ, NF, MM, MD>;
   constexpr int Q = R::Q;
@@ -340,6 +346,19 @@ __global__ void __launch_bounds__(kBlock) k_troubled_cells(Layout L, Physics ph,
     if (tid < 32 && next < nitems) {
       fence_proxy_async_smem();
       issue_b(next);
+    }
+    if (UCFVB_CELLS_PF && next < nitems && v == 0) {
+      // the next tile's member rows of U into L2 while this tile finishes
+      mbar_wait(&bar[0], par ^ 1u);
+      if (next < tc) {
+        const int* nid = reinterpret_cast<const int*>(ga + slot * R::SCA + R::CA_ID);
+#pragma unroll
+        for (int m = 0; m < NF * MD; ++m) prefetch_l2(U + nid[m]);
+      } else {
+        const int* nid = reinterpret_cast<const int*>(ga + slot * R::SMA + R::MA_ID);
+#pragma unroll
+        for (int m = 0; m < MM; ++m) prefetch_l2(U + nid[m]);
+      }
     }
     bool demote = false;
     if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);

@@ -287,24 +287,56 @@ struct GpuSolver::Impl {
   }
   dim3 grid_owned() const { return dim3((L.n_owned + kBlock - 1) / kBlock); }
 
-  // halo exchange of a stage state: pack per peer, then one grouped send/recv
-  int64_t exchange(double4* buf) {
-    if (!comm || peers.empty()) return 0;
+  // ---- halo exchange of a stage state (subdomains) ------------------------
+  // Owned cells are ordered [interior | sent] (ucfvb_subdomain_build): the
+  // stage's gather updates the sent cells [n_int, n_owned) first, the exchange
+  // (pack per peer + transport) then runs on comm_stream -- forked from and
+  // joined back into the solver stream with events, inside the step graph --
+  // while the gather updates the interior [0, n_int). Transports: NCCL
+  // (attach_nccl: grouped ncclSend/ncclRecv) or an in-process loopback group
+  // (ucfvb_group_*: one cudaMemcpyAsync per peer block, single device).
+  int n_int = -1;  // < 0: no exchange attached
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool in_group = false;
+  double4* pending_xout = nullptr;  // loopback: this stage's output, awaiting the group's copies
+  bool exchanging() const { return n_int >= 0 && !peers.empty(); }
+
+  void ensure_comm_stream() {
+    if (comm_stream) return;
+    CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+
+  // on comm_stream: pack the owned cells each peer needs, then (NCCL) one
+  // grouped send/recv into buf's halo blocks
+  int64_t exchange_start(double4* buf) {
     int64_t nl = 0;
     for (const DevPeer& p : peers)
       if (p.n_send) {
-        launch_k(k_halo_pack, dim3((p.n_send + 255) / 256), 256, 0, stream, buf, p.send_idx, p.n_send, sendbuf + p.send_off);
+        launch_k(k_halo_pack, dim3((p.n_send + 255) / 256), 256, 0, comm_stream, buf, p.send_idx, p.n_send,
+                 sendbuf + p.send_off);
         ++nl;
       }
-    NK(nccl().GroupStart());
-    for (const DevPeer& p : peers) {
-      if (p.n_send) NK(nccl().Send(sendbuf + p.send_off, 4 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm,
-                                   stream));
-      if (p.n_recv) NK(nccl().Recv(buf + p.recv_begin, 4 * static_cast<size_t>(p.n_recv), ncclDouble, p.rank, comm,
-                                   stream));
+    if (comm) {
+      NK(nccl().GroupStart());
+      for (const DevPeer& p : peers) {
+        if (p.n_send)
+          NK(nccl().Send(sendbuf + p.send_off, 4 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm,
+                         comm_stream));
+        if (p.n_recv)
+          NK(nccl().Recv(buf + p.recv_begin, 4 * static_cast<size_t>(p.n_recv), ncclDouble, p.rank, comm,
+                         comm_stream));
+      }
+      NK(nccl().GroupEnd());
     }
-    NK(nccl().GroupEnd());
     return nl;
+  }
+  // the next kernel on the solver stream waits for the exchange
+  void exchange_join() {
+    CK(cudaEventRecord(ev_join, comm_stream));
+    CK(cudaStreamWaitEvent(stream, ev_join, 0));
   }
 
   // min(h/speed) over the owned cells of `src` into ds->dmin_bits
@@ -342,7 +374,9 @@ struct GpuSolver::Impl {
 
   // one compute_residual stage on the stream (solver.cpp:316-379)
   // dt_next: this stage's output starts the next step; reduce its max_stable_dt term
-  int64_t launch_stage(const double4* U, bool first, const RkEpilogue& rk, bool census, bool dt_next = false) {
+  // xout: this stage's output state, whose halo is exchanged (subdomains)
+  int64_t launch_stage(const double4* U, bool first, const RkEpilogue& rk, bool census, bool dt_next = false,
+                       double4* xout = nullptr) {
     int64_t nl = 0;
     const int taps = opt.keep_taps ? FL_TAPS : 0;
     const int mode = opt.mode;
@@ -395,12 +429,37 @@ struct GpuSolver::Impl {
     int ff = 0;
     if (first) ff |= FL_STEP_LABELS | (census ? FL_CENSUS : 0);
     ks.face_flux(dim3((L.n_faces + ks.faces_per_flux_block - 1) / ks.faces_per_flux_block), stream, L, ph, S);
-    ks.gather(grid_owned(), stream, L, S, rk, ff | (dt_next ? FL_DT : 0), ds, opt.gamma);
-    ++nl;
+    ff |= dt_next ? FL_DT : 0;
+    if (xout && exchanging()) {
+      RkEpilogue sent = rk, interior = rk;
+      sent.c_begin = n_int;
+      sent.c_end = L.n_owned;
+      interior.c_begin = 0;
+      interior.c_end = n_int;
+      nl += launch_gather(sent, ff);
+      CK(cudaEventRecord(ev_fork, stream));
+      CK(cudaStreamWaitEvent(comm_stream, ev_fork, 0));
+      nl += exchange_start(xout);
+      nl += launch_gather(interior, ff);
+      if (in_group)
+        pending_xout = xout;  // the group pushes the peer blocks, then joins
+      else
+        exchange_join();
+    } else {
+      nl += launch_gather(rk, ff);
+    }
     record(4);
     CK(cudaGetLastError());
     accumulate_phases();
     return nl + 1;
+  }
+
+  // the gather + RK update of owned cells [rk.c_begin, rk.c_end) (all owned when c_end == 0)
+  int64_t launch_gather(const RkEpilogue& rk, int flags) {
+    const int n = (rk.c_end ? rk.c_end : L.n_owned) - rk.c_begin;
+    if (n <= 0) return 0;
+    ks.gather(dim3((n + kBlock - 1) / kBlock), stream, L, S, rk, flags, ds, opt.gamma);
+    return 1;
   }
 
   void accumulate_phases() {
@@ -418,86 +477,56 @@ struct GpuSolver::Impl {
     ++e.nterms;
   }
 
-  // All launches of one time step (the body a graph captures). `src` is the
-  // state at t, `dst` receives the state at t+dt. With `with_dt` the step
-  // starts with k_dt (device dt, run_steps); otherwise ds->dt was set by the host.
-  int64_t launch_step(int rk, bool with_dt, const double4* src, double4* dst, bool census) {
-    int64_t nl = 0;
+  struct StagePlan {
+    const double4* U;
+    bool first;
+    RkEpilogue rk;
+    bool dt_next;
+  };
+
+  // The stages of one time step: `src` is the state at t, `dst` receives the
+  // state at t+dt (combine2 orders, time_integrator.cpp:31-38, 42-74; SSP-RK3
+  // Shu-Osher). Each stage's output (rk.out) is what its halo exchange sends.
+  std::vector<StagePlan> step_plan(int rk, bool with_dt, const double4* src, double4* dst) {
     const double* dt = &ds->dt;
-    if (with_dt) nl += launch_dt_finalize();  // dmin of src: k_dt (first step) or the previous final gather
+    std::vector<StagePlan> plan;
+    auto stage = [&](const double4* U, bool first, double4* out, std::initializer_list<std::pair<const double4*, double>> t,
+                     std::initializer_list<int> scaled, double4* rhs_out, bool dt_next) {
+      RkEpilogue e{};
+      e.dt = dt;
+      e.out = out;
+      e.rhs_out = rhs_out;
+      auto sc = scaled.begin();
+      for (const auto& [term, coef] : t) add_term(e, term, coef, *sc++ != 0);
+      plan.push_back(StagePlan{U, first, e, dt_next});
+    };
     if (rk == UCFVB_RK3) {
       double4 *u1 = work[0], *u2 = work[1];
-      RkEpilogue e1{};
-      e1.dt = dt;
-      e1.out = u1;
-      add_term(e1, src, 1.0, false);
-      add_term(e1, src, 0.0, false);
-      add_term(e1, nullptr, 1.0, true);
-      nl += launch_stage(src, true, e1, census);
-      nl += exchange(u1);
-      RkEpilogue e2{};
-      e2.dt = dt;
-      e2.out = u2;
-      add_term(e2, src, 0.75, false);
-      add_term(e2, u1, 0.25, false);
-      add_term(e2, nullptr, 0.25, true);
-      nl += launch_stage(u1, false, e2, census);
-      nl += exchange(u2);
-      RkEpilogue e3{};
-      e3.dt = dt;
-      e3.out = dst;
-      add_term(e3, src, 1.0 / 3.0, false);
-      add_term(e3, u2, 2.0 / 3.0, false);
-      add_term(e3, nullptr, 2.0 / 3.0, true);
-      nl += launch_stage(u2, false, e3, census, with_dt);
-      nl += exchange(dst);
+      stage(src, true, u1, {{src, 1.0}, {src, 0.0}, {nullptr, 1.0}}, {0, 0, 1}, nullptr, false);
+      stage(u1, false, u2, {{src, 0.75}, {u1, 0.25}, {nullptr, 0.25}}, {0, 0, 1}, nullptr, false);
+      stage(u2, false, dst, {{src, 1.0 / 3.0}, {u2, 2.0 / 3.0}, {nullptr, 2.0 / 3.0}}, {0, 0, 1}, nullptr, with_dt);
     } else {
       using namespace rk54;
       double4 *ua = work[0], *ub = work[1], *uc = work[2], *ud = work[3], *r3 = work[4];
-      RkEpilogue e{};
-      e.dt = dt;
-      e.out = ua;
-      add_term(e, src, 1.0, false);
-      add_term(e, src, 0.0, false);
-      add_term(e, nullptr, a10, true);
-      nl += launch_stage(src, true, e, census);
-      nl += exchange(ua);
-      e = RkEpilogue{};
-      e.dt = dt;
-      e.out = ub;
-      add_term(e, src, b20, false);
-      add_term(e, ua, b21, false);
-      add_term(e, nullptr, a21, true);
-      nl += launch_stage(ua, false, e, census);
-      nl += exchange(ub);
-      e = RkEpilogue{};
-      e.dt = dt;
-      e.out = uc;
-      add_term(e, src, b30, false);
-      add_term(e, ub, b32, false);
-      add_term(e, nullptr, a32, true);
-      nl += launch_stage(ub, false, e, census);
-      nl += exchange(uc);
-      e = RkEpilogue{};
-      e.dt = dt;
-      e.out = ud;
-      e.rhs_out = r3;
-      add_term(e, src, b40, false);
-      add_term(e, uc, b43, false);
-      add_term(e, nullptr, a43, true);
-      nl += launch_stage(uc, false, e, census);
-      nl += exchange(ud);
-      e = RkEpilogue{};
-      e.dt = dt;
-      e.out = dst;
-      add_term(e, ub, c52, false);
-      add_term(e, uc, c53, false);
-      add_term(e, r3, a53, true);
-      add_term(e, ud, c54, false);
-      add_term(e, nullptr, a54, true);
-      nl += launch_stage(ud, false, e, census, with_dt);
-      nl += exchange(dst);
+      stage(src, true, ua, {{src, 1.0}, {src, 0.0}, {nullptr, a10}}, {0, 0, 1}, nullptr, false);
+      stage(ua, false, ub, {{src, b20}, {ua, b21}, {nullptr, a21}}, {0, 0, 1}, nullptr, false);
+      stage(ub, false, uc, {{src, b30}, {ub, b32}, {nullptr, a32}}, {0, 0, 1}, nullptr, false);
+      stage(uc, false, ud, {{src, b40}, {uc, b43}, {nullptr, a43}}, {0, 0, 1}, r3, false);
+      stage(ud, false, dst, {{ub, c52}, {uc, c53}, {r3, a53}, {ud, c54}, {nullptr, a54}}, {0, 0, 1, 0, 1}, nullptr,
+            with_dt);
     }
+    return plan;
+  }
+
+  // All launches of one time step (the body a graph captures). With `with_dt`
+  // the step starts from the reduced max_stable_dt of `src` (k_dt for a run's
+  // first step, else the previous step's final gather); otherwise ds->dt was
+  // set by the host.
+  int64_t launch_step(int rk, bool with_dt, const double4* src, double4* dst, bool census) {
+    int64_t nl = 0;
+    if (with_dt) nl += launch_dt_finalize();
+    for (const StagePlan& sp : step_plan(rk, with_dt, src, dst))
+      nl += launch_stage(sp.U, sp.first, sp.rk, census, sp.dt_next, sp.rk.out);
     // inside the step (graph): a failure on any rank stops every rank's later
     // kernels (they exit on a set error word), so no rank writes past the
     // failing step and all can return to its input state
@@ -588,6 +617,9 @@ struct GpuSolver::Impl {
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     // the persisting-L2 carve-out is device-wide: give back what we raised
     if (l2_limit_set) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, l2_limit_before);
   }
@@ -1116,19 +1148,13 @@ void GpuSolver::get_phase_times(double t[4]) {
   for (int i = 0; i < 4; ++i) t[i] = p_->phase[i];
 }
 
-void GpuSolver::attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub) {
-  Impl& I = *p_;
-  if (!sub) throw ApiError(UCFVB_INVALID, "attach_nccl: the solver was not created on a subdomain");
-  if (I.comm) throw ApiError(UCFVB_INVALID, "attach_nccl: a communicator is already attached");
-  ncclUniqueId u;
-  std::memcpy(&u, id, 128);
-  CK(cudaSetDevice(I.device));
-  NK(nccl().CommInitRank(&I.comm, world, u, rank));
-  I.world = world;
-  I.rank = rank;
+// the subdomain's exchange plan on the device: send lists per peer, one
+// contiguous send buffer, the interior / sent split and the exchange stream
+static void setup_exchange(GpuSolver::Impl& I, const ucfvb_subdomain* sub) {
+  if (!I.peers.empty()) throw ApiError(UCFVB_INVALID, "solver: an exchange is already attached");
   size_t off = 0;
   for (const auto& p : sub->peers) {
-    Impl::DevPeer d;
+    GpuSolver::Impl::DevPeer d;
     d.rank = p.rank;
     d.n_send = static_cast<int>(p.send.size());
     d.recv_begin = p.recv_begin;
@@ -1142,9 +1168,256 @@ void GpuSolver::attach_nccl(const uint8_t id[128], int rank, int world, const uc
     I.peers.push_back(d);
   }
   I.sendbuf = dalloc<double4>(std::max<size_t>(1, off), I.owned);
+  I.n_int = sub->n_interior;
+  I.ensure_comm_stream();
   // graphs captured before the exchange existed are stale
   I.drop_graphs();
 }
+
+void GpuSolver::attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub) {
+  Impl& I = *p_;
+  if (!sub) throw ApiError(UCFVB_INVALID, "attach_nccl: the solver was not created on a subdomain");
+  if (I.comm) throw ApiError(UCFVB_INVALID, "attach_nccl: a communicator is already attached");
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  CK(cudaSetDevice(I.device));
+  NK(nccl().CommInitRank(&I.comm, world, u, rank));
+  I.world = world;
+  I.rank = rank;
+  setup_exchange(I, sub);
+}
+
+// ---- in-process loopback group ---------------------------------------------
+// min of the parts' collected dt terms, written back to every part
+__global__ void k_group_dt_min(DtState* const* ds, int n) {
+  double m = ds[0]->dmin;
+  for (int i = 1; i < n; ++i) m = smin(m, ds[i]->dmin);
+  for (int i = 0; i < n; ++i) ds[i]->dmin = m;
+}
+// the job's error word (as allreduce_error): kind by max, step / face / cell by min
+__global__ void k_group_err(int* const* err, int n) {
+  int e[4] = {err[0][0], err[0][1], err[0][2], err[0][3]};
+  for (int i = 1; i < n; ++i) {
+    e[0] = max(e[0], err[i][0]);
+    for (int j = 1; j < 4; ++j) e[j] = min(e[j], err[i][j]);
+  }
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < 4; ++j) err[i][j] = e[j];
+}
+
+struct GpuGroup::Impl {
+  std::vector<GpuSolver::Impl*> P;
+  std::vector<cudaEvent_t> ev_part, ev_sent;
+  cudaEvent_t ev_lead = nullptr;
+  DtState** d_ds = nullptr;
+  int** d_err = nullptr;
+  // push plan: part p sends its peer block e to part `to`, into `to`'s receive range
+  struct Push {
+    int to;
+    size_t src_off;
+    int dst_begin, n;
+  };
+  std::vector<std::vector<Push>> push;
+  std::vector<std::vector<int>> senders;  // parts whose copies part q waits for
+  cudaGraphExec_t graph[2][2] = {};
+  int64_t graph_launches[2][2] = {};
+  int64_t launches = 0;
+  cudaStream_t lead() const { return P[0]->stream; }
+
+  void all_to_lead() {
+    for (size_t p = 1; p < P.size(); ++p) {
+      CK(cudaEventRecord(ev_part[p], P[p]->stream));
+      CK(cudaStreamWaitEvent(lead(), ev_part[p], 0));
+    }
+  }
+  void lead_to_all() {
+    CK(cudaEventRecord(ev_lead, lead()));
+    for (size_t p = 1; p < P.size(); ++p) CK(cudaStreamWaitEvent(P[p]->stream, ev_lead, 0));
+  }
+
+  // one RK step of every part (device dt): the same kernels and exchange
+  // schedule as a rank's step, with the group's copies as the transport
+  int64_t launch_step(int rk, int parity) {
+    int64_t nl = 0;
+    const int n = static_cast<int>(P.size());
+    for (auto* q : P) {
+      launch_k(k_dt_collect, 1, 1, 0, q->stream, q->ds);
+      ++nl;
+    }
+    all_to_lead();
+    k_group_dt_min<<<1, 1, 0, lead()>>>(d_ds, n);
+    ++nl;
+    lead_to_all();
+    std::vector<std::vector<GpuSolver::Impl::StagePlan>> plan(n);
+    for (int p = 0; p < n; ++p) {
+      GpuSolver::Impl* q = P[p];
+      launch_k(k_dt_finalize, 1, 1, 0, q->stream, q->ds, q->S.err, 0);
+      ++nl;
+      plan[p] = q->step_plan(rk, true, q->ubuf[parity], q->ubuf[parity ^ 1]);
+    }
+    for (size_t i = 0; i < plan[0].size(); ++i) {
+      for (int p = 0; p < n; ++p) {
+        const auto& sp = plan[p][i];
+        nl += P[p]->launch_stage(sp.U, sp.first, sp.rk, false, sp.dt_next, sp.rk.out);
+      }
+      // every part pushes its packed peer blocks into the receivers' halo ranges
+      for (int p = 0; p < n; ++p) {
+        GpuSolver::Impl* q = P[p];
+        for (const Push& x : push[p])
+          CK(cudaMemcpyAsync(P[x.to]->pending_xout + x.dst_begin, q->sendbuf + x.src_off,
+                             sizeof(double4) * static_cast<size_t>(x.n), cudaMemcpyDeviceToDevice, q->comm_stream));
+        CK(cudaEventRecord(ev_sent[p], q->comm_stream));
+      }
+      for (int p = 0; p < n; ++p)
+        for (int from : senders[p]) CK(cudaStreamWaitEvent(P[p]->stream, ev_sent[from], 0));
+    }
+    for (int p = 0; p < n; ++p) CK(cudaStreamWaitEvent(P[p]->stream, ev_sent[p], 0));  // own exchange stream joined
+    all_to_lead();
+    k_group_err<<<1, 1, 0, lead()>>>(d_err, n);
+    ++nl;
+    lead_to_all();
+    return nl;
+  }
+
+  cudaGraphExec_t get_graph(int rk, int parity) {
+    cudaGraphExec_t& g = graph[rk][parity];
+    if (g) return g;
+    cudaGraph_t gr;
+    CK(cudaStreamBeginCapture(lead(), cudaStreamCaptureModeThreadLocal));
+    lead_to_all();
+    const int64_t nl = launch_step(rk, parity);
+    all_to_lead();
+    CK(cudaStreamEndCapture(lead(), &gr));
+    CK(cudaGraphInstantiate(&g, gr, 0));
+    CK(cudaGraphDestroy(gr));
+    graph_launches[rk][parity] = nl;
+    return g;
+  }
+
+  ~Impl() {
+    for (auto& a : graph)
+      for (auto& g : a)
+        if (g) cudaGraphExecDestroy(g);
+    for (auto e : ev_part)
+      if (e) cudaEventDestroy(e);
+    for (auto e : ev_sent)
+      if (e) cudaEventDestroy(e);
+    if (ev_lead) cudaEventDestroy(ev_lead);
+    if (d_ds) cudaFree(d_ds);
+    if (d_err) cudaFree(d_err);
+  }
+};
+
+GpuGroup::GpuGroup(GpuSolver* const* parts, const ucfvb_subdomain* const* subs, int n) : p_(new Impl) {
+  Impl& G = *p_;
+  if (n < 1) throw ApiError(UCFVB_INVALID, "group: needs at least one part");
+  for (int p = 0; p < n; ++p) {
+    if (!subs[p]) throw ApiError(UCFVB_INVALID, "group: every part must be created on a subdomain");
+    if (subs[p]->rank != p || subs[p]->n_parts != n)
+      throw ApiError(UCFVB_INVALID, "group: part i must be rank i of an n-part partition");
+    GpuSolver::Impl& I = *parts[p]->p_;
+    if (I.comm || I.in_group) throw ApiError(UCFVB_INVALID, "group: a part already has an exchange attached");
+    if (I.device != parts[0]->p_->device) throw ApiError(UCFVB_INVALID, "group: all parts must share one device");
+    G.P.push_back(&I);
+  }
+  CK(cudaSetDevice(G.P[0]->device));
+  for (int p = 0; p < n; ++p) {
+    setup_exchange(*G.P[p], subs[p]);
+    G.P[p]->in_group = true;
+  }
+  G.push.resize(n);
+  G.senders.resize(n);
+  for (int p = 0; p < n; ++p)
+    for (const auto& d : G.P[p]->peers) {
+      if (!d.n_send) continue;
+      const GpuSolver::Impl::DevPeer* back = nullptr;
+      for (const auto& e : G.P[d.rank]->peers)
+        if (e.rank == p) back = &e;
+      if (!back || back->n_recv != d.n_send) throw ApiError(UCFVB_INVALID, "group: inconsistent exchange plans");
+      G.push[p].push_back(Impl::Push{d.rank, d.send_off, back->recv_begin, d.n_send});
+      G.senders[d.rank].push_back(p);
+    }
+  G.ev_part.resize(n);
+  G.ev_sent.resize(n);
+  for (int p = 0; p < n; ++p) {
+    CK(cudaEventCreateWithFlags(&G.ev_part[p], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&G.ev_sent[p], cudaEventDisableTiming));
+  }
+  CK(cudaEventCreateWithFlags(&G.ev_lead, cudaEventDisableTiming));
+  std::vector<DtState*> hds(n);
+  std::vector<int*> herr(n);
+  for (int p = 0; p < n; ++p) {
+    hds[p] = G.P[p]->ds;
+    herr[p] = G.P[p]->S.err;
+  }
+  CK(cudaMalloc(&G.d_ds, n * sizeof(DtState*)));
+  CK(cudaMalloc(&G.d_err, n * sizeof(int*)));
+  CK(cudaMemcpy(G.d_ds, hds.data(), n * sizeof(DtState*), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(G.d_err, herr.data(), n * sizeof(int*), cudaMemcpyHostToDevice));
+}
+
+GpuGroup::~GpuGroup() = default;
+
+// run_steps over the group (device dt, graph-replayed): every part advances
+// n_steps; on a failure every part returns to the failing step's input
+double GpuGroup::run_steps(int n_steps, int rk, double t0) {
+  Impl& G = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "group: unknown integrator");
+  if (n_steps <= 0) return t0;
+  CK(cudaSetDevice(G.P[0]->device));
+  const int cur0 = G.P[0]->cur;
+  for (auto* q : G.P) {
+    if (q->cur != cur0) throw ApiError(UCFVB_INVALID, "group: parts out of step");
+    DtState h{};
+    h.dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);  // bits of 1e300
+    h.t = t0;
+    h.step = -1;
+    h.t_end = INFINITY;
+    h.cfl = q->opt.cfl;
+    CK(cudaMemcpyAsync(q->ds, &h, sizeof h, cudaMemcpyHostToDevice, q->stream));
+    q->reset_ties();
+    q->S.step = &q->ds->step;
+    G.launches += q->launch_dt_reduce(q->ubuf[q->cur]);
+    CK(cudaStreamSynchronize(q->stream));
+  }
+  for (int s = 0; s < n_steps; ++s) {
+    const int par = (cur0 + s) & 1;
+    if (G.P[0]->opt.use_graphs) {
+      CK(cudaGraphLaunch(G.get_graph(rk, par), G.lead()));
+      G.launches += G.graph_launches[rk][par];
+    } else {
+      G.lead_to_all();
+      G.launches += G.launch_step(rk, par);
+      G.all_to_lead();
+    }
+  }
+  CK(cudaStreamSynchronize(G.lead()));
+  CK(cudaGetLastError());
+  DtState h{};
+  CK(cudaMemcpy(&h, G.P[0]->ds, sizeof h, cudaMemcpyDeviceToHost));
+  int e[4];
+  CK(cudaMemcpy(e, G.P[0]->S.err, sizeof e, cudaMemcpyDeviceToHost));
+  for (auto* q : G.P) {
+    q->S.step = q->step_zero;
+    q->fetch_counts();
+    q->stage_is_first = false;
+    q->cur = (cur0 + n_steps) & 1;
+  }
+  if (e[0]) {
+    const int failed = std::min(std::max(0, e[3]), n_steps - 1);
+    for (auto* q : G.P) q->cur = (cur0 + failed) & 1;
+    try {
+      G.P[0]->raise_device_error(e[0], e[1], e[2]);
+    } catch (ApiError& err) {
+      for (auto* q : G.P) q->reset_error();
+      for (auto* q : G.P) CK(cudaStreamSynchronize(q->stream));
+      throw ApiError(err.code, "group run failed at step " + std::to_string(failed) + ": " + err.what());
+    }
+  }
+  return h.t + h.dt;
+}
+
+int64_t GpuGroup::launch_count() const { return p_->launches; }
 
 void GpuSolver::set_list_policy(int policy) {
   Impl& I = *p_;

@@ -54,9 +54,32 @@ class GpuSolver {
   // NCCL communicator + the subdomain's exchange plan (halo exchange after every stage)
   void attach_nccl(const uint8_t id[128], int rank, int world, const ucfvb_subdomain* sub);
 
+  struct Impl;
+
  private:
+  friend class GpuGroup;
   double run_impl(int n_steps, int rk, double t0, double t_end, bool until, int64_t* census, double* dt_out,
                   int* n_done);
+  std::unique_ptr<Impl> p_;
+};
+
+// In-process loopback group: the subdomain solvers of one partition (part i
+// = rank i) on ONE device, stepped together with the multi-GPU schedule of a
+// rank -- sent cells first, the halo exchange forked onto each part's exchange
+// stream while its interior is updated -- and device-to-device copies (one
+// cudaMemcpyAsync per peer block) as the transport, the dt min and the error
+// word reduced by kernels across the group; one CUDA graph captures a step of
+// all parts. It tests the exchange schedule and plans on a single GPU.
+class GpuGroup {
+ public:
+  GpuGroup(GpuSolver* const* parts, const ucfvb_subdomain* const* subs, int n);
+  ~GpuGroup();
+  GpuGroup(const GpuGroup&) = delete;
+  GpuGroup& operator=(const GpuGroup&) = delete;
+  double run_steps(int n_steps, int rk, double t0);
+  int64_t launch_count() const;
+
+ private:
   struct Impl;
   std::unique_ptr<Impl> p_;
 };

@@ -33,7 +33,8 @@ class Peer:
 class Subdomain:
     """Rank `rank`'s owned cells + stencil-depth halo as a local mesh/stencil pair.
 
-    Local cells are [owned | halo grouped by owner]; `gid` maps local -> global.
+    Local cells are [owned interior | owned sent cells | halo grouped by owner];
+    `gid` maps local -> global.
     Keep the global mesh alive (the local view borrows its vertex array)."""
 
     def __init__(self, mesh, stencils, part: np.ndarray, n_parts: int, rank: int):
@@ -50,6 +51,9 @@ class Subdomain:
         no, nl, npr = C.c_int32(), C.c_int32(), C.c_int32()
         _ck(_lib().ucfvb_subdomain_info(h, C.byref(no), C.byref(nl), C.byref(npr)))
         self.n_owned, self.n_local = no.value, nl.value
+        ni = C.c_int32()
+        _ck(_lib().ucfvb_subdomain_interior(h, C.byref(ni)))
+        self.n_interior = ni.value  # owned cells [0, n_interior) are never sent
         self.gid = np.zeros(self.n_local, dtype=np.int32)
         _ck(_lib().ucfvb_subdomain_global_ids(h, self.gid.ctypes.data_as(A.c_i32p)))
         self.peers = []

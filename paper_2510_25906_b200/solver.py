@@ -246,6 +246,37 @@ class Solver:
             pass
 
 
+class Group:
+    """In-process loopback group (ucfvb_group_*): the subdomain solvers of one
+    n-part partition on one device, stepped together with a rank's multi-GPU
+    schedule and device-to-device copies as the halo transport."""
+
+    def __init__(self, parts):
+        self._lib = A.load_library()
+        self.parts = list(parts)  # keep the solvers alive
+        arr = (C.c_void_p * len(self.parts))(*[p._h.value if hasattr(p._h, "value") else p._h for p in self.parts])
+        h = C.c_void_p()
+        rc = self._lib.ucfvb_group_create(arr, len(self.parts), C.byref(h))
+        if rc != A.OK:
+            raise A.error_for(rc, self._lib.ucfvb_last_error(None).decode())
+        self._h = h
+
+    def run_steps(self, n_steps: int, rk: int = A.RK3, t0: float = 0.0) -> float:
+        t = C.c_double()
+        rc = self._lib.ucfvb_group_run_steps(self._h, int(n_steps), int(rk), float(t0), C.byref(t))
+        if rc != A.OK:
+            raise A.error_for(rc, self._lib.ucfvb_last_error(None).decode())
+        return t.value
+
+    def launch_count(self) -> int:
+        return int(self._lib.ucfvb_group_launch_count(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and A._LIB is not None:
+            A._LIB.ucfvb_group_free(self._h)
+            self._h = None
+
+
 def nccl_unique_id() -> bytes:
     """ncclGetUniqueId through the native library (rank 0 creates, all ranks attach)."""
     lib = A.load_library()

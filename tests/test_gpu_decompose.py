@@ -1,13 +1,15 @@
 """Subdomain solvers on the GPU (ucfvb_create_sub): N subdomains driven stage
 by stage with a host halo refresh reproduce the single-domain GPU run
-bit-for-bit on owned cells; the NCCL path (dt/census/error all-reduces inside
-the captured step) runs with a 1-rank communicator."""
+bit-for-bit on owned cells; the in-graph exchange schedule (sent cells first,
+the halo exchange forked onto an exchange stream while the interior is
+updated) over the loopback transport likewise; the NCCL path (dt/census/error
+all-reduces inside the captured step) runs with a 1-rank communicator."""
 import numpy as np
 import pytest
 
 from paper_2510_25906_b200 import _abi as A
 from paper_2510_25906_b200.decompose import Subdomain, partition_rcb
-from paper_2510_25906_b200.solver import Solver, make_bcs, nccl_unique_id
+from paper_2510_25906_b200.solver import Group, Solver, make_bcs, nccl_unique_id
 from tests.decomp_driver import local_exchange, run_rk3
 from tests.test_decompose import CASES, setup
 
@@ -78,3 +80,53 @@ def test_nccl_single_rank_path_matches_plain_solver():
     t3, _ = g.run_steps(3, A.RK3)  # graph-replayed steps with the in-graph all-reduce
     t4, _ = plain.run_steps(3, A.RK3)
     np.testing.assert_array_equal(g.state[np.argsort(sub.gid)], plain.state)
+
+
+@pytest.mark.parametrize("rk", [A.RK3, A.RK54], ids=["rk3", "rk54"])
+@pytest.mark.parametrize("name", sorted(CASES))
+@pytest.mark.parametrize("n", [2, 3])
+def test_loopback_group_schedule_matches_single_domain(name, n, rk):
+    """The multi-GPU step schedule on one device: n subdomain solvers in one
+    captured graph, each stage's sent cells updated first, the pack + one
+    cudaMemcpyAsync per peer block on the forked exchange stream while the
+    interior is updated, dt and error word reduced across the parts. Owned
+    states and times are bit-identical to the single domain."""
+    c, mesh, st, o, u0 = setup(name)
+    steps = 4
+    single = Solver(mesh, o, make_bcs(c["bcs"]), stencils=st)
+    single.state = u0
+    t_ref, _ = single.run_steps(steps, rk)
+    ref = single.state
+    part = partition_rcb(mesh, n)
+    subs = [Subdomain(mesh, st, part, n, r) for r in range(n)]
+    assert all(0 <= s.n_interior < s.n_owned for s in subs)
+    parts = [Solver.on_subdomain(s, o, make_bcs(c["bcs"])) for s in subs]
+    for p, s in zip(parts, subs):
+        p.state = s.local_state(u0)
+    g = Group(parts)
+    t = g.run_steps(2, rk)
+    t = g.run_steps(steps - 2, rk, t0=t)  # second call replays the other graph parity too
+    assert t == t_ref
+    out = np.zeros_like(u0)
+    for p, s in zip(parts, subs):
+        out[s.gid[: s.n_owned]] = p.state[: s.n_owned]
+    np.testing.assert_array_equal(out, ref)
+
+
+def test_loopback_group_failure_rolls_back_every_part():
+    """A non-physical state on one part: every part returns to the failing
+    step's input (the error word is reduced across the group each step)."""
+    c, mesh, st, o, u0 = setup("shock-p2")
+    part = partition_rcb(mesh, 2)
+    subs = [Subdomain(mesh, st, part, 2, r) for r in range(2)]
+    parts = [Solver.on_subdomain(s, o, make_bcs(c["bcs"])) for s in subs]
+    bad = u0.copy()
+    bad[subs[1].gid[0], 0] = -1.0  # an owned cell of part 1
+    for p, s in zip(parts, subs):
+        p.state = s.local_state(bad)
+    before = [p.state for p in parts]
+    g = Group(parts)
+    with pytest.raises(A.NonPhysicalError):
+        g.run_steps(3)
+    for p, b in zip(parts, before):
+        np.testing.assert_array_equal(p.state, b)

@@ -192,15 +192,21 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- roofline model
-def kernel_bytes(K, NQ, NF, MM, MD):
+def kernel_bytes(K, NQ, NF, MM, MD, mix=None):
     """Algorithmic HBM bytes per cell of each kernel: every
     array the kernel must read or write, once; stencil-neighbour gathers of U
     counted as L2 hits (only the cell's own U is counted). Face points are
-    double4 (32 B), indices int32, labels uint8."""
+    double4 (32 B), indices int32, labels uint8. `mix` = class fractions
+    (L, C, M, F) of the run: the central kernel stores candidate face points
+    only for raw-Linear cells and dofs only for cells that are not raw-MUSCL;
+    final Linear cells were raw-Linear and final MUSCL cells include every
+    raw-MUSCL one, so f_L and 1 - f_M are lower bounds of those fractions
+    (bytes never overcounted)."""
     Q = NF * NQ
+    fl, fm = (1.0, 0.0) if mix is None else (float(mix[0]), float(mix[2]))
     central = (32 + 4 * MM + 8 * MM * K      # U, stencil ids, pinv        (TMA group A)
                + 8 * Q * K + 8 + 4 * NF + 4 * Q  # phi, threshold, nbrs, slots (TMA group B)
-               + 32 * Q + 32 * K + 1)         # candidate face points, dofs, raw label
+               + 32 * Q * fl + 32 * K * (1.0 - fm) + 1)  # candidate face points, dofs, raw label
     cwenoz = (32 + 4 * NF * MD + 16 * NF * MD + 8 * K * K + 8 * Q * K + 4 * NF + 32 * K  # U, dir ids/pinv, OI, phi, nbrs, dofs
               + 4 * Q + 32 * Q + 8)           # slots, face points, chunk entry/label
     muscl = 32 + 4 * MM + 16 * MM + 16 * Q + 4 * NF + 4 * Q + 32 * Q + 8
@@ -484,7 +490,7 @@ def run_b200_arm(args):
     sd = st.numpy()
     MM = int(np.max(np.diff(sd["central_ptr"]))) - 1
     MD = int(np.max(np.diff(sd["dir_member_ptr"]))) - 1
-    kb = kernel_bytes(K, NQ, NF, MM, MD)
+    kb = kernel_bytes(K, NQ, NF, MM, MD, mix)
     names = ["central (reconstruct)", "spread+compaction (detect)", "cwenoz+muscl (weights)", "flux+RK"]
     phase_bytes = [kb["central"] * n, kb["spread"] * n,
                    (kb["cwenoz"] * mix[1] + kb["muscl"] * mix[2]) * n, kb["flux"] * n]

@@ -271,7 +271,11 @@ int32_t ucfvb_get_labels(ucfvb_solver* h, uint8_t* labels);
 /* label counts of step_labels: Linear, CWENOZ, MUSCL, FirstOrder */
 int32_t ucfvb_get_census(ucfvb_solver* h, int64_t counts[4]);
 /* Troubled-cell class lists (an implementation choice; results are identical):
- * policy 0 = 32-cell chunk lists (default), 1 = dense per-cell lists. Stats of
+ * policy 0 = 32-cell chunk lists (k_troubled_split), 1 = dense per-cell lists
+ * (k_troubled_cells), 2 = adaptive (default): after every synchronising call
+ * the lists of the next ones follow the last stage's chunk fill -- chunks when
+ * the troubled cells fill >= 3/4 of the chunks that hold them, else per-cell
+ * lists (the first call of a solver uses chunks). Stats of
  * the last synchronised stage's lists: CWENOZ cells, MUSCL cells, CWENOZ
  * chunks, MUSCL chunks, 1 if per-cell lists are in use (cells whose
  * reconstruction fell back to first order stay counted in their list).

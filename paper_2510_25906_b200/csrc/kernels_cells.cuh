@@ -29,7 +29,7 @@ namespace ucfvb {
 // cell) into 8 distinct bank pairs
 __host__ __device__ constexpr uint32_t odd16(uint32_t x) { return ((x >> 4) & 1u) ? x : x + 16u; }
 
-template <int K, int NQ, int NF, int MM, int MD>
+template <int K, int NQ, int NF, int MM, int MD, int TC = 32>
 struct CellRec {
   static constexpr int Q = NF * NQ;
   static constexpr uint32_t CA_PD = 0, CA_ID = NF * MD * 2 * 8;
@@ -41,8 +41,8 @@ struct CellRec {
   static constexpr uint32_t MB_PHI = 0, MB_NBR = Q * 2 * 8, MB_DST = MB_NBR + NF * 4;
   static constexpr uint32_t MB = round16(MB_DST + Q * 4);
   static constexpr uint32_t SCA = odd16(CA), SCB = odd16(CB), SMA = odd16(MA), SMB = odd16(MB);
-  static constexpr uint32_t TILE_A = 32 * (SCA > SMA ? SCA : SMA);
-  static constexpr uint32_t TILE_B = 32 * (SCB > SMB ? SCB : SMB);
+  static constexpr uint32_t TILE_A = TC * (SCA > SMA ? SCA : SMA);  // TC cells per tile
+  static constexpr uint32_t TILE_B = TC * (SCB > SMB ? SCB : SMB);
   static constexpr uint32_t BYTES = TILE_A + TILE_B;
 };
 
@@ -92,15 +92,21 @@ __global__ void k_pack_records(Layout L, unsigned char* ca, unsigned char* cb, u
 // Four lanes per cell (lane v = conserved variable v); arithmetic identical
 // to k_troubled_split / k_cwenoz / k_muscl.
 #ifndef UCFVB_CELLS_MINB
-#define UCFVB_CELLS_MINB 1
+#define UCFVB_CELLS_MINB 16
 #endif
 #ifndef UCFVB_CELLS_PF
 #define UCFVB_CELLS_PF 0
 #endif
+#ifndef UCFVB_CELLS_TILE
+#define UCFVB_CELLS_TILE 8
+#endif
+// cells per tile; a block is 4 * kCellTile threads
+constexpr int kCellTile = UCFVB_CELLS_TILE;
 template <int K, int NQ, int NF, int MM, int MD>
-__global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Layout L, Physics ph, Scratch S,
+__global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_cells(Layout L, Physics ph, Scratch S,
                                                            const double4* __restrict__ U, int flags) {
-  using R = CellRec<K, NQ, NF, MM, MD>;
+  constexpr int TC = kCellTile;
+  using R = CellRec<K, NQ, NF, MM, MD, TC>;
   constexpr int Q = R::Q;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B
@@ -123,8 +129,8 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
   __syncthreads();
   if (s_err) return;
   const int nc = s_nc, nm = s_nm;
-  const int tc = (nc + 31) >> 5;
-  const int nitems = tc + ((nm + 31) >> 5);
+  const int tc = (nc + TC - 1) / TC;
+  const int nitems = tc + (nm + TC - 1) / TC;
   if (nc > 0 && !(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
     if (blockIdx.x == 0 && tid == 0) atomicOr(&S.err[0], 4);
     return;
@@ -132,13 +138,13 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
   // list entry j of tile i; lanes past the list's end repeat its last cell
   // (their records are staged and computed but never stored)
   auto tile_cell = [&](int i, int j) {
-    return i < tc ? __ldg(S.list_c + min(i * 32 + j, nc - 1)) : __ldg(S.list_m + min((i - tc) * 32 + j, nm - 1));
+    return i < tc ? __ldg(S.list_c + min(i * TC + j, nc - 1)) : __ldg(S.list_m + min((i - tc) * TC + j, nm - 1));
   };
-  // warp 0 only: lane j fetches slot j's record
+  // lanes j < TC of warp 0 only: lane j fetches slot j's record
   auto issue_a = [&](int i) {
     const int c = tile_cell(i, tid);
-    if (tid == 0) mbar_arrive_expect_tx(&bar[0], 32 * (i < tc ? R::CA : R::MA));
-    __syncwarp();
+    if (tid == 0) mbar_arrive_expect_tx(&bar[0], TC * (i < tc ? R::CA : R::MA));
+    __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
       bulk_g2s(ga + tid * R::SCA, L.rec_ca + static_cast<size_t>(c) * R::CA, R::CA, &bar[0]);
     else
@@ -146,14 +152,14 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
   };
   auto issue_b = [&](int i) {
     const int c = tile_cell(i, tid);
-    if (tid == 0) mbar_arrive_expect_tx(&bar[1], 32 * (i < tc ? R::CB : R::MB));
-    __syncwarp();
+    if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * (i < tc ? R::CB : R::MB));
+    __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
       bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::CB, R::CB, &bar[1]);
     else
       bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::MB, R::MB, &bar[1]);
   };
-  if (tid < 32 && static_cast<int>(blockIdx.x) < nitems) {
+  if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);
     issue_b(blockIdx.x);
   }
@@ -165,7 +171,7 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
     const uint32_t par = it & 1;
     const int next = i + gridDim.x;
     const bool cw = i < tc;
-    const bool mine = cw ? i * 32 + slot < nc : (i - tc) * 32 + slot < nm;
+    const bool mine = cw ? i * TC + slot < nc : (i - tc) * TC + slot < nm;
     const int c = tile_cell(i, slot);
     const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
     double vals[Q];
@@ -199,7 +205,7 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
         }
       }
       __syncthreads();  // group A consumed: request the next tile's
-      if (tid < 32 && next < nitems) {
+      if (tid < TC && next < nitems) {
         fence_proxy_async_smem();
         issue_a(next);
       }
@@ -302,7 +308,7 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
         l1 += spl[m * 2 + 1] * d;
       }
       __syncthreads();  // group A consumed: request the next tile's
-      if (tid < 32 && next < nitems) {
+      if (tid < TC && next < nitems) {
         fence_proxy_async_smem();
         issue_a(next);
       }
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(kBlock, UCFVB_CELLS_MINB) k_troubled_cells(Lay
       for (int lq = 0; lq < Q; ++lq) dst[lq] = sdst[lq];
     }
     __syncthreads();  // group B consumed: request the next tile's
-    if (tid < 32 && next < nitems) {
+    if (tid < TC && next < nitems) {
       fence_proxy_async_smem();
       issue_b(next);
     }

@@ -173,9 +173,13 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
       fence_proxy_async_smem();
       issue_a(refill, st);
     }
-    if ((flags & FL_DOFS) && live) {
+    // dofs feed the CWENOZ kernel; a raw MUSCL label survives the spread (it
+    // only raises labels), so on detecting stages those cells' dofs are dead
+    bool keep_dofs = (flags & FL_DOFS) && live;
+    if (keep_dofs && !((flags & FL_NAD) && (flags & FL_EVAL))) {
 #pragma unroll
       for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = acc[k];
+      keep_dofs = false;
     }
     mbar_wait(&bar[2 * st + 1], par);
     if (flags & FL_EVAL) {
@@ -232,6 +236,9 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
           if (tm && (tid & 31) == __ffs(tm) - 1) atomicAdd(S.ties, static_cast<unsigned long long>(__popc(tm)));
         }
         if (v == 0 && live) S.raw[c] = static_cast<uint8_t>(sev | (bad ? 4 : 0));
+#ifndef UCFVB_NO_DOFS_SKIP
+        if (keep_dofs && (flags & FL_NAD) && sev == 2 && !(flags & FL_TAPS)) keep_dofs = false;
+#endif
         // a raw label >= CWENOZ survives the spread (it only raises labels): the
         // troubled kernel rewrites this cell's face points, so the candidates are dead
         store = !((flags & FL_NAD) && sev >= 1);
@@ -240,6 +247,10 @@ __global__ void __launch_bounds__(kBlock, smem_min_blocks(NS * CentralStage<K, N
 #pragma unroll
         for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(sdst[lq * 32 + slot]) + v] = vals[lq];
       }
+    }
+    if (keep_dofs) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) dofs[4 * aos(c, k, K) + v] = acc[k];
     }
     __syncthreads();  // group B consumed
     if (tid == 0 && refill < nchunks) {

@@ -114,16 +114,16 @@ void troubled_split_launcher(dim3 g, cudaStream_t st, const Layout& L, const Phy
 template <int K, int NQ, int NF, int MM, int MD>
 void troubled_cells_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                              const double4* U, int f) {
-  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(kBlock), CellRec<K, NQ, NF, MM, MD>::BYTES + 16, st, L, p,
-           S, U, f);
+  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(4 * kCellTile), CellRec<K, NQ, NF, MM, MD, kCellTile>::BYTES + 16,
+           st, L, p, S, U, f);
 }
 
 // raise the dynamic smem limit and size the persistent grid (resident blocks x SMs)
 template <typename Kfn>
-int persistent_grid(Kfn k, uint32_t smem, int n_sm) {
+int persistent_grid(Kfn k, uint32_t smem, int n_sm, int threads = kBlock) {
   CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kBlock, smem));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem));
   return std::max(1, per_sm) * n_sm;
 }
 
@@ -166,7 +166,8 @@ KernelSet make_set() {
     };
     using R = CellRec<K, NQ, NF, MMT, MDT>;
     s.cells_setup = [](int n_sm, int* grid, KernelSet::Launch* launch) {
-      *grid = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT>, R::BYTES + 16, n_sm);
+      *grid = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT>,
+                              CellRec<K, NQ, NF, MMT, MDT, kCellTile>::BYTES + 16, n_sm, 4 * kCellTile);
       *launch = troubled_cells_launcher<K, NQ, NF, MMT, MDT>;
     };
     s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* ca, unsigned char* cb, unsigned char* ma,
@@ -270,11 +271,26 @@ struct GpuSolver::Impl {
 
   size_t l2_window_bytes = 0, l2_persist_bytes = 0;
   // Class lists for the troubled cells: 32-cell chunk lists (TMA-staged
-  // k_troubled_split, the default) or dense per-cell lists (k_cwenoz /
-  // k_muscl; UCFVB_TROUBLED=lists or set_list_policy). Chunks measured faster
-  // on configs 1-3, including config 3's half-full chunks (profiles/round1.md).
+  // k_troubled_split) or dense per-cell lists (k_troubled_cells over per-cell
+  // records; generic k_cwenoz / k_muscl off the fast path). Adaptive by
+  // default: chunks stage whole 32-cell chunks of rows, so they win only when
+  // the troubled cells fill the chunks they occupy (config 2: 84 %, chunks
+  // 62.6 vs 74 us/stage; config 3: 50 %, per-cell lists 4.0 vs 6.0 ms/stage;
+  // profiles/round2.md). UCFVB_TROUBLED=chunks|lists or set_list_policy pins it.
   bool per_cell_lists = false;
+  bool lists_auto = true;
   int* hcounts = nullptr;  // pinned copy of S.counts after the last synchronising call
+  // after a synchronising call: the adaptive policy follows the last stage's chunk fill
+  void adapt_lists() {
+    if (!lists_auto || !ks.troubled || !ks.cells) return;
+    const int64_t cells = int64_t(hcounts[0]) + hcounts[1], chunks = int64_t(hcounts[2]) + hcounts[3];
+    if (chunks <= 0) return;
+    const bool want = 4 * cells < 3 * 32 * chunks;
+    if (want != per_cell_lists) {
+      per_cell_lists = want;
+      drop_graphs();
+    }
+  }
   void fetch_counts() { CK(cudaMemcpyAsync(hcounts, S.counts, 4 * sizeof(int), cudaMemcpyDeviceToHost, stream)); }
   void drop_graphs() {
     for (auto& a : graph)
@@ -394,7 +410,8 @@ struct GpuSolver::Impl {
       } else if (ks.cells) {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
         record(2);
-        ks.cells(dim3(std::min(ks.cells_grid, (L.n + 31) / 32 + 2)), stream, L, ph, S, U, FL_NAD | FL_FALLBACK | taps);
+        ks.cells(dim3(std::min(ks.cells_grid, (L.n + kCellTile - 1) / kCellTile + 2)), stream, L, ph, S, U,
+                 FL_NAD | FL_FALLBACK | taps);
         nl += 3;
       } else {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
@@ -682,7 +699,10 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   bool uniform = true;
   for (int c = 0; c < H.n; ++c) uniform &= H.nfc[c] == H.NF;
   I.ks = pick_kernels(H.K, H.NQ, H.NF, H.MM, H.MD, uniform);
-  if (const char* tl = std::getenv("UCFVB_TROUBLED")) I.per_cell_lists = std::strcmp(tl, "lists") == 0;
+  if (const char* tl = std::getenv("UCFVB_TROUBLED")) {  // diagnostics: pin the list policy
+    I.per_cell_lists = std::strcmp(tl, "lists") == 0;
+    I.lists_auto = false;
+  }
   CK(cudaMallocHost(&I.hcounts, 4 * sizeof(int)));
   std::memset(I.hcounts, 0, 4 * sizeof(int));
   if (I.ks.central_tma) {
@@ -766,7 +786,10 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   S.dofs = stage_buf + n_fp + n_ff;
   {
     const char* e = std::getenv("UCFVB_L2_PERSIST");
-    const bool want = !(e && e[0] == '0');
+    // the persisting carve-out pays only while the stage buffers are L2-sized
+    // (config 2: 117 MB, +21 %); for config 3 (4.8 GB) it evicts the stencil
+    // gathers' lines and costs 17 % (measured, profiles/round2.md)
+    const bool want = !(e && e[0] == '0') && (n_fp + n_ff + n_dofs) * sizeof(double4) <= (size_t(256) << 20);
     int max_persist = 0, max_window = 0;
     CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
     CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
@@ -894,6 +917,7 @@ void GpuSolver::advance(double dt, double t, int rk) {
   if (I.read_error(&k, &f, &c)) I.raise_device_error(k, f, c);  // state stays at t (reference semantics)
   I.cur ^= 1;
   I.stage_is_first = false;
+  I.adapt_lists();
 }
 
 void GpuSolver::compute_residual(const double* u, double t, double* out) {
@@ -1026,6 +1050,7 @@ double GpuSolver::run_impl(int n_steps, int rk, double t0, double t_end, bool un
   if (dt_out && ran > 0) CK(cudaMemcpy(dt_out, I.dtlog_dev, sizeof(double) * ran, cudaMemcpyDeviceToHost));
   I.stage_is_first = false;
   CK(cudaStreamSynchronize(I.stream));
+  I.adapt_lists();
   return h.t + h.dt;
 }
 
@@ -1073,6 +1098,7 @@ double GpuSolver::advance_host(const double* u_in, double* u_out, int n_steps, i
   CK(cudaStreamSynchronize(I.stream));
   CK(cudaGetLastError());
   I.stage_is_first = false;
+  I.adapt_lists();
   if (he[0]) {
     const int failed = std::min(std::max(0, he[3]), n_steps - 1);
     I.cur = (cur0 + failed) & 1;
@@ -1421,8 +1447,9 @@ int64_t GpuGroup::launch_count() const { return p_->launches; }
 
 void GpuSolver::set_list_policy(int policy) {
   Impl& I = *p_;
-  if (policy < 0 || policy > 1) throw ApiError(UCFVB_INVALID, "set_list_policy: policy must be 0 or 1");
-  if ((policy == 1) != I.per_cell_lists) {
+  if (policy < 0 || policy > 2) throw ApiError(UCFVB_INVALID, "set_list_policy: policy must be 0, 1 or 2");
+  I.lists_auto = policy == 2;
+  if (policy != 2 && (policy == 1) != I.per_cell_lists) {
     I.per_cell_lists = policy == 1;
     I.drop_graphs();
   }

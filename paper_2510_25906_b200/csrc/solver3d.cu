@@ -296,10 +296,18 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // type): the grid is a multiple of the type count, so block b only ever sees
 // chunks of type b % 6 and stages that type's pinv and phi rows in shared
 // memory once, read as broadcast 16-byte loads
+// nad bit 0: NAD classification (hybrid); bit 1: this stage detects (first
+// stage or detect_every_stage), so the raw label decides the final one
 template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
+  // staged path on a detecting stage: the candidate face values are stored
+  // after the NAD vote, only for cells that stay Linear (a raw label >=
+  // CWENOZ survives the spread and a failed pre-check demotes the cell: the
+  // troubled kernels / the spread rewrite those cells' face points)
+  const bool detect = STAGED && K >= 8 && eval && (nad & 2);
+  nad &= 1;
   constexpr int G = M + NF;  // stencil members + face neighbours
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
@@ -489,7 +497,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
               const int q = 8 * i + fr, cl = 8 * t + 2 * fc + j;
               if (q < Q) {
                 sval[q][v][cl] = f[i][t][j];
-                if (cb + cl < D.n) W.fp[static_cast<size_t>(D.slot[ao(cb + cl, q, Q)]) * V5 + v] = f[i][t][j];
+                if (!detect && cb + cl < D.n) W.fp[static_cast<size_t>(D.slot[ao(cb + cl, q, Q)]) * V5 + v] = f[i][t][j];
               }
             }
         __syncthreads();  // every face value of the block in sval
@@ -542,6 +550,15 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       const int sev = max(s_sev[0][lane], s_sev[1][lane]);
       const int fail = s_pos[lane] | s_bf[0][lane] | s_bf[1][lane];
       W.raw[c] = static_cast<uint8_t>(sev | (fail << 2));
+    }
+    if (detect) {  // the surviving candidates, five contiguous variables per face point
+      if (v == 0) s_pos[lane] = !(max(s_sev[0][lane], s_sev[1][lane]) | s_pos[lane] | s_bf[0][lane] | s_bf[1][lane]);
+      __syncthreads();
+      const int cb = ch << 5;
+      for (int p = threadIdx.x; p < Q * 32 * V5; p += 160) {
+        const int w = p % V5, q = (p / V5) % Q, l = p / (V5 * Q);
+        if (s_pos[l] && cb + l < D.n) W.fp[static_cast<size_t>(D.slot[ao(cb + l, q, Q)]) * V5 + w] = sval[q][w][l];
+      }
     }
     __syncthreads();
   }
@@ -1375,7 +1392,8 @@ struct GpuSolver3::Impl {
     mark(0);
     if (mode == UCFVB_LINEAR || mode == UCFVB_HYBRID) {  // forced CWENOZ solves inside k3_cwenoz
       if (staged)
-        kern.central_staged<<<central_grid, 160, kern.smem_central_staged, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
+        kern.central_staged<<<central_grid, 160, kern.smem_central_staged, st>>>(
+            D, P, W, Us, 1, nad ? (1 | ((first || o.detect_every_stage) ? 2 : 0)) : 0);
       else
         kern.central<<<central_grid, 160, kern.smem_central, st>>>(D, P, W, Us, 1, nad ? 1 : 0);
       ++launches;

@@ -189,10 +189,10 @@ class Solver:
         self._ck(self._lib.ucfvb_get_nad_ties(self._h, C.byref(t)))
         return t.value
 
-    LIST_POLICIES = {"chunks": 0, "lists": 1}
+    LIST_POLICIES = {"chunks": 0, "lists": 1, "auto": 2}
 
     def set_list_policy(self, policy: str):
-        """Troubled-cell class lists: "chunks" (default) or "lists" (per cell)."""
+        """Troubled-cell class lists: "chunks", "lists" (per cell) or "auto" (default: by chunk fill)."""
         self._ck(self._lib.ucfvb_set_list_policy(self._h, self.LIST_POLICIES[policy]))
 
     def list_stats(self) -> dict:

@@ -1,8 +1,9 @@
 """Summarise an `ncu --set full` report (read here with `ncu -i --page raw --csv`)
 into profiles/<name>_ncu_full_summary.json and, with --traffic, the per-phase
-DRAM bytes bench.py reads as roofline.traffic (profiles/traffic.json).
+DRAM bytes per launch bench.py reads as roofline.traffic (profiles/traffic.json,
+keyed by config and cell count; one launch per kernel in the report).
 
-    python scripts/ncu_summary.py gpurun_out/prof_r1f.ncu-rep profiles/r01f_ncu_full_summary.json --traffic
+    python scripts/ncu_summary.py gpurun_out/x.ncu-rep profiles/r02_x_ncu_full_summary.json --traffic 3 8388608
 """
 import argparse
 import csv
@@ -20,7 +21,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("report")
     ap.add_argument("out")
-    ap.add_argument("--traffic", action="store_true")
+    ap.add_argument("--traffic", nargs=2, metavar=("CONFIG", "CELLS"))
     a = ap.parse_args()
     raw = subprocess.run(["ncu", "-i", a.report, "--page", "raw", "--csv"], capture_output=True, text=True,
                          check=True).stdout
@@ -69,8 +70,15 @@ def main():
     print(json.dumps(out, indent=1))
     if a.traffic:
         tf = Path(__file__).resolve().parents[1] / "profiles" / "traffic.json"
-        tf.write_text(json.dumps(traffic, indent=1) + "\n")
-        print("traffic:", traffic, file=sys.stderr)
+        try:
+            allt = json.loads(tf.read_text())
+            if not all(k.startswith("config") for k in allt):
+                allt = {}
+        except Exception:
+            allt = {}
+        allt[f"config{a.traffic[0]}"] = {"cells": int(a.traffic[1]), "source": a.report, **traffic}
+        tf.write_text(json.dumps(allt, indent=1) + "\n")
+        print("traffic:", allt, file=sys.stderr)
 
 
 if __name__ == "__main__":

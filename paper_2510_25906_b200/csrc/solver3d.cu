@@ -212,7 +212,9 @@ __host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
 // values for the positivity check, and report the bounds failure (fallback_check)
 // KE: number of leading dofs evaluated (MUSCL's limited r = 1 polynomial: 3, the
 // rest are zero; oracle evaluate_cell_n)
-template <int K, int NQ, int NF, int KE = K>
+// STORE = false: only the staged values (the troubled kernels store the final
+// face values cooperatively in troubled_fallback)
+template <int K, int NQ, int NF, int KE = K, bool STORE = true>
 __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
                                            double u0, const double* a, double (*sval)[V5][33], bool chk,
                                            double blo, double bhi, double& viol, const int* sl,
@@ -222,7 +224,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
   auto group = [&](int q0) {
     int gs[QG];  // this group's slots (issued before the fma chains)
 #pragma unroll
-    for (int j = 0; j < QG; ++j) gs[j] = sl ? sl[q0 + j] : D.slot[ao(c, q0 + j, Q)];
+    for (int j = 0; j < QG; ++j) gs[j] = !STORE ? 0 : (sl ? sl[q0 + j] : D.slot[ao(c, q0 + j, Q)]);
     double val[QG];
 #pragma unroll
     for (int j = 0; j < QG; ++j) val[j] = u0;
@@ -244,7 +246,7 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
     }
 #pragma unroll
     for (int j = 0; j < QG; ++j) {
-      if (act) W.fp[static_cast<size_t>(gs[j]) * V5 + v] = val[j];
+      if (STORE && act) W.fp[static_cast<size_t>(gs[j]) * V5 + v] = val[j];
       sval[q0 + j][v][lane] = val[j];
       if (chk) viol = smax(viol, smax(blo - val[j], val[j] - bhi));
     }
@@ -261,13 +263,22 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
 }
 
 // fallback (solver.cpp:229-264) after a troubled reconstruction; demoted cells
-// get first-order values
+// get first-order values. Then the block stores the chunk's final face values
+// from shared memory, five consecutive threads per face point (one contiguous
+// 40-byte record; the reconstruction's per-variable stores were scattered
+// 8-byte writes, and demoted cells' values were written twice)
 template <int NF, int NQ>
 __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
                                                   int lane, bool act, double u0, bool chk, double blo, double bhi,
                                                   double viol, double (*sval)[V5][33], int* s_fail) {
   constexpr int Q = NF * NQ;
-  if (v == 0) s_fail[lane] = 0;
+  __shared__ int s_cell[32];
+  __shared__ double s_u0[V5][32];
+  if (v == 0) {
+    s_fail[lane] = 0;
+    s_cell[lane] = act ? c : -1;
+  }
+  s_u0[v][lane] = u0;
   __syncthreads();
   if (P.mode == UCFVB_HYBRID) {
     if (chk) {
@@ -284,9 +295,12 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
     }
   }
   __syncthreads();
-  if (act && s_fail[lane]) {
-    if (v == 0) W.labels[c] = UCFVB_SCHEME_FIRST;
-    for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = u0;
+  if (act && v == 0 && s_fail[lane]) W.labels[c] = UCFVB_SCHEME_FIRST;
+  for (int p = threadIdx.x; p < Q * 32 * V5; p += 160) {
+    const int w = p % V5, q = (p / V5) % Q, l = p / (V5 * Q);
+    const int cell = s_cell[l];
+    if (cell >= 0)
+      W.fp[static_cast<size_t>(D.slot[ao(cell, q, Q)]) * V5 + w] = s_fail[l] ? s_u0[w][l] : sval[q][w][l];
   }
   __syncthreads();
 }
@@ -626,8 +640,11 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
 }
 
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
+#ifndef UCFVB_CW3_MINB
+#define UCFVB_CW3_MINB 1
+#endif
 template <int K, int M, int NF, int NQ, bool STAGED>
-__global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+__global__ void __launch_bounds__(160, UCFVB_CW3_MINB) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
   constexpr int EP = M * K, ED = NF * 3 * MD3, EO = (K * K + 1) & ~1;  // region sizes (even: phi is read as double2)
@@ -919,9 +936,7 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
           for (int j = 0; j < 2; ++j) {
             const int q = 8 * i + fr, cl = 8 * tt + 2 * fc + j;
             if (q < Q) {
-              sval[q][v][cl] = f[i][tt][j];
-              const int cc2 = scell[cl];
-              if (cc2 >= 0) W.fp[static_cast<size_t>(D.slot[ao(cc2, q, Q)]) * V5 + v] = f[i][tt][j];
+              sval[q][v][cl] = f[i][tt][j];  // stored by troubled_fallback
             }
           }
       __syncthreads();  // every face value of the chunk in sval
@@ -932,8 +947,8 @@ __global__ void __launch_bounds__(160) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const
         }
     } else {
       __syncthreads();  // the gather buffer becomes the face-value buffer
-      eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
-                            STAGED ? sp + EP + ED + EO : nullptr);
+      eval_store<K, NQ, NF, K, false>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
+                                      STAGED ? sp + EP + ED + EO : nullptr);
     }
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
@@ -1044,8 +1059,8 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    eval_store<K, NQ, NF, 3>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
-                             STAGED ? sp + 3 * M : nullptr);
+    eval_store<K, NQ, NF, 3, false>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
+                                    STAGED ? sp + 3 * M : nullptr);
     troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
@@ -1135,14 +1150,16 @@ __global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3
 
 // ---- gather + RK combination (solver.cpp:296-311, time_integrator.cpp:31-38) --------------
 // out = wa*ua + wb*ub + (wr*dt)*res, res = -acc*(1/vol); store_res keeps res (compute_residual tap / RK54)
+// cells: nullable list of the cells to update (n_cells of them); else cells [0, D.n)
 template <int NF>
 __global__ void __launch_bounds__(256) k3_gather_rk(Dev3 D, Work3 W, const double* __restrict__ ua,
                                                     const double* __restrict__ ub, double* __restrict__ out,
                                                     double* __restrict__ res_out, double wa, double wb, double wr,
-                                                    int combine) {
+                                                    int combine, const int32_t* __restrict__ cells, int n_cells) {
   if (failed_before(W)) return;  // block-uniform
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= D.n) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (cells ? n_cells : D.n)) return;
+  const int c = cells ? cells[i] : i;
   double acc[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int i = 0; i < NF; ++i) {
@@ -1245,7 +1262,8 @@ struct Kern3 {
   void (*constant)(Dev3, Work3, const double*);
   void (*flux)(Dev3, Phys3, Work3);
   int flux_lanes = 1;
-  void (*gather)(Dev3, Work3, const double*, const double*, double*, double*, double, double, double, int);
+  void (*gather)(Dev3, Work3, const double*, const double*, double*, double*, double, double, double, int,
+                 const int32_t*, int);
 };
 
 template <int K, int M, int NF, int NQ>
@@ -1347,19 +1365,25 @@ struct GpuSolver3::Impl {
   double* sendbuf = nullptr;
   ncclComm_t comm = nullptr;
   int world = 1, rank = 0;
-  void exchange(double* buf) {
+  // owned cells some peer holds (updated first each stage) and the rest
+  int32_t *sent_cells = nullptr, *interior_cells = nullptr;
+  int n_sent = 0, n_interior = 0;
+  cudaStream_t comm_st = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void exchange(double* buf, cudaStream_t s = nullptr) {
     if (!comm || peers.empty()) return;
+    if (!s) s = st;
     for (const DevPeer& p : peers)
       if (p.n_send) {
-        k3_halo_pack<<<(p.n_send * V5 + 255) / 256, 256, 0, st>>>(buf, p.send_idx, p.n_send, sendbuf + p.send_off);
+        k3_halo_pack<<<(p.n_send * V5 + 255) / 256, 256, 0, s>>>(buf, p.send_idx, p.n_send, sendbuf + p.send_off);
         ++launches;
       }
     NK(nccl().GroupStart());
     for (const DevPeer& p : peers) {
-      if (p.n_send) NK(nccl().Send(sendbuf + p.send_off, V5 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm, st));
+      if (p.n_send) NK(nccl().Send(sendbuf + p.send_off, V5 * static_cast<size_t>(p.n_send), ncclDouble, p.rank, comm, s));
       if (p.n_recv)
         NK(nccl().Recv(buf + static_cast<size_t>(p.recv_begin) * V5, V5 * static_cast<size_t>(p.n_recv), ncclDouble,
-                       p.rank, comm, st));
+                       p.rank, comm, s));
     }
     NK(nccl().GroupEnd());
   }
@@ -1431,9 +1455,32 @@ struct GpuSolver3::Impl {
     if (first) CK3(cudaMemcpyAsync(step_labels, W.labels, n, cudaMemcpyDeviceToDevice, st));
     kern.flux<<<static_cast<unsigned>((static_cast<int64_t>(nF) * kern.flux_lanes + 127) / 128), 128, 0, st>>>(D, P, W);
     mark(4);
-    kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine);
-    launches += 2;
-    if (combine && out && xchg) exchange(out);
+    if (sent_cells) {
+      // subdomain: owned cells only, the cells peers hold first; with NCCL the
+      // halo exchange then runs on the exchange stream (forked / joined with
+      // events, inside the step graph) while the interior cells are updated
+      const bool fork = combine && out && xchg && comm && !peers.empty();
+      if (n_sent > 0)
+        kern.gather<<<(n_sent + 255) / 256, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine,
+                                                          sent_cells, n_sent);
+      if (fork) {
+        CK3(cudaEventRecord(ev_fork, st));
+        CK3(cudaStreamWaitEvent(comm_st, ev_fork, 0));
+        exchange(out, comm_st);
+      }
+      if (n_interior > 0)
+        kern.gather<<<(n_interior + 255) / 256, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine,
+                                                             interior_cells, n_interior);
+      if (fork) {
+        CK3(cudaEventRecord(ev_join, comm_st));
+        CK3(cudaStreamWaitEvent(st, ev_join, 0));
+      }
+      launches += 3;
+    } else {
+      kern.gather<<<nblk, 256, 0, st>>>(D, W, wa_src, wb_src, out, res, wa, wb, wr, combine, nullptr, 0);
+      launches += 2;
+      if (combine && out && xchg) exchange(out);
+    }
     mark(5);
     collect();
   }
@@ -1576,6 +1623,20 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
         I.peers.push_back(dp);
       }
       I.sendbuf = dalloc<double>(std::max<size_t>(off, 1), I.owned);
+      std::vector<uint8_t> is_sent(I.n_owned, 0);
+      for (const auto& pr : sub->peers)
+        for (int32_t c : pr.send) is_sent[c] = 1;
+      std::vector<int32_t> sent, interior;
+      for (int c = 0; c < I.n_owned; ++c) (is_sent[c] ? sent : interior).push_back(c);
+      I.n_sent = static_cast<int>(sent.size());
+      I.n_interior = static_cast<int>(interior.size());
+      I.sent_cells = dalloc<int32_t>(std::max<size_t>(sent.size(), 1), I.owned);
+      I.interior_cells = dalloc<int32_t>(std::max<size_t>(interior.size(), 1), I.owned);
+      if (!sent.empty()) up(I.sent_cells, sent);
+      if (!interior.empty()) up(I.interior_cells, interior);
+      CK3(cudaStreamCreateWithFlags(&I.comm_st, cudaStreamNonBlocking));
+      CK3(cudaEventCreateWithFlags(&I.ev_fork, cudaEventDisableTiming));
+      CK3(cudaEventCreateWithFlags(&I.ev_join, cudaEventDisableTiming));
     }
     D.central = upload_ao(s.central, n, M + 1);
     D.nbr = upload_ao(m.cell_nbr, n, NF);
@@ -1696,6 +1757,11 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     if (I.h_counters) cudaFreeHost(I.h_counters);
     if (I.h_dt) cudaFreeHost(I.h_dt);
     if (I.st) cudaStreamDestroy(I.st);
+    if (I.comm_st) cudaStreamDestroy(I.comm_st);
+    if (I.ev_fork) cudaEventDestroy(I.ev_fork);
+    if (I.ev_join) cudaEventDestroy(I.ev_join);
+    for (auto& e : I.ev)
+      if (e) cudaEventDestroy(e);
     delete p_;
     throw;
   }
@@ -1713,6 +1779,9 @@ GpuSolver3::~GpuSolver3() {
   if (I.h_counters) cudaFreeHost(I.h_counters);
   if (I.h_dt) cudaFreeHost(I.h_dt);
   if (I.st) cudaStreamDestroy(I.st);
+  if (I.comm_st) cudaStreamDestroy(I.comm_st);
+  if (I.ev_fork) cudaEventDestroy(I.ev_fork);
+  if (I.ev_join) cudaEventDestroy(I.ev_join);
   delete p_;
 }
 

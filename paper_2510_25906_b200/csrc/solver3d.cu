@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -214,11 +215,12 @@ __host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
 // rest are zero; oracle evaluate_cell_n)
 // STORE = false: only the staged values (the troubled kernels store the final
 // face values cooperatively in troubled_fallback)
+// phc: the chunk's per-cell phi rows staged in shared memory ([Q*K][32], lane = cell)
 template <int K, int NQ, int NF, int KE = K, bool STORE = true>
 __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c, int op, int v, int lane, bool act,
                                            double u0, const double* a, double (*sval)[V5][33], bool chk,
                                            double blo, double bhi, double& viol, const int* sl,
-                                           const double* phs = nullptr) {
+                                           const double* phs = nullptr, const double* phc = nullptr) {
   constexpr int Q = NF * NQ;
   constexpr int QG = (Q % 4 == 0) ? 4 : ((Q % 3 == 0) ? 3 : 1);  // independent fma chains in flight
   auto group = [&](int q0) {
@@ -238,6 +240,11 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
           if ((e & 1) == 0 || k == 0) w[j] = reinterpret_cast<const double2*>(phs)[e >> 1];
           val[j] = __fma_rn(a[k], (e & 1) ? w[j].y : w[j].x, val[j]);
         }
+    } else if (phc) {
+#pragma unroll
+      for (int k = 0; k < KE; ++k)
+#pragma unroll
+        for (int j = 0; j < QG; ++j) val[j] = __fma_rn(a[k], phc[((q0 + j) * K + k) * 32 + lane], val[j]);
     } else {
 #pragma unroll
       for (int k = 0; k < KE; ++k)
@@ -296,11 +303,17 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
   }
   __syncthreads();
   if (act && v == 0 && s_fail[lane]) W.labels[c] = UCFVB_SCHEME_FIRST;
-  for (int p = threadIdx.x; p < Q * 32 * V5; p += 160) {
-    const int w = p % V5, q = (p / V5) % Q, l = p / (V5 * Q);
+  {  // thread (cell l, variable w): all Q points of cell l, slots loaded up front
+    const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;
     const int cell = s_cell[l];
-    if (cell >= 0)
-      W.fp[static_cast<size_t>(D.slot[ao(cell, q, Q)]) * V5 + w] = s_fail[l] ? s_u0[w][l] : sval[q][w][l];
+    if (cell >= 0) {
+      int sl[Q];
+#pragma unroll
+      for (int q = 0; q < Q; ++q) sl[q] = __ldg(&D.slot[ao(cell, q, Q)]);
+      const bool fail = s_fail[l] != 0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(sl[q]) * V5 + w] = fail ? s_u0[w][l] : sval[q][w][l];
+    }
   }
   __syncthreads();
 }
@@ -312,7 +325,11 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // memory once, read as broadcast 16-byte loads
 // nad bit 0: NAD classification (hybrid); bit 1: this stage detects (first
 // stage or detect_every_stage), so the raw label decides the final one
-template <int K, int M, int NF, int NQ, bool STAGED>
+// TMA: per-cell operator rows (config 4): the chunk's pinv block (group A)
+// and phi block (group B) are bulk-copied into shared memory one chunk ahead,
+// each refilled as soon as the solve / the evaluation has consumed it
+// (split-phase, as the 2D k_central_tma)
+template <int K, int M, int NF, int NQ, bool STAGED, bool TMA = false>
 __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
@@ -334,24 +351,49 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
   double* sp = smem3 + kUnion;
   // per-cell operator rows (p <= 2): the chunk's pinv block is copied to shared
   // memory with 16-byte cp.async at the chunk start (all in flight at once)
-  constexpr bool PCS = !STAGED && K * M <= 200;
+  constexpr bool PCS = !STAGED && !TMA && K * M <= 200;
   double* spc = smem3 + kUnion;
+  double* sphc = spc + M * K * 32;  // TMA: the chunk's phi block
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sphc + Q * K * 32);  // TMA: [0] pinv, [1] phi
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
   const int nch = (D.n + 31) >> 5;
+  constexpr uint32_t kPinvBytes = M * K * 32 * 8, kPhiBytes = Q * K * 32 * 8;
+  auto issue_pinv = [&](int ch) {
+    mbar_arrive_expect_tx(&bar[0], kPinvBytes);
+    bulk_g2s(spc, D.pinv + static_cast<size_t>(ch) * M * K * 32, kPinvBytes, &bar[0]);
+  };
+  auto issue_phi = [&](int ch) {
+    mbar_arrive_expect_tx(&bar[1], kPhiBytes);
+    bulk_g2s(sphc, D.phi + static_cast<size_t>(ch) * Q * K * 32, kPhiBytes, &bar[1]);
+  };
+  if (TMA) {
+    if (threadIdx.x == 0) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      mbar_fence_init();
+      if (static_cast<int>(blockIdx.x) < nch) {
+        issue_pinv(blockIdx.x);
+        issue_phi(blockIdx.x);
+      }
+    }
+    __syncthreads();
+  }
+  int it = 0;
   if (STAGED) {
     const int t = blockIdx.x % D.n_ops;
     for (int e = threadIdx.x; e < M * K; e += 160) sp[e] = D.pinv[ao(t, e, M * K)];
     for (int e = threadIdx.x; e < Q * K; e += 160) sp[M * K + e] = D.phi[ao(t, e, Q * K)];
     __syncthreads();
   }
-  for (int ch = blockIdx.x; ch < nch; ch += gridDim.x) {
+  for (int ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
     const int c = (ch << 5) + lane;
     const bool act = c < D.n;
     const int cc = act ? c : (D.n - 1);
     const int op = D.opi[cc];
-    if (D.n_ops == D.n && threadIdx.x == 0 && ch + static_cast<int>(gridDim.x) < nch) {
+    const int nxt = ch + static_cast<int>(gridDim.x);
+    if (!TMA && D.n_ops == D.n && threadIdx.x == 0 && ch + static_cast<int>(gridDim.x) < nch) {
       // this block's next chunk's pinv rows and stencil ids -> L2 (TMA prefetch;
       // measured: prefetching phi as well thrashes L2 and is slower)
       const int nx = ch + gridDim.x;
@@ -387,6 +429,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
     const double u0 = U[static_cast<size_t>(cc) * V5 + v];
     cp_async_wait_all();  // this thread's own copies
     if (pcs) __syncthreads();  // the pinv block is copied by all threads
+    if (TMA) mbar_wait(&bar[0], it & 1);
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
@@ -455,10 +498,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
             if ((e & 1) == 0) w = reinterpret_cast<const double2*>(sp)[e >> 1];
             a[k] = __fma_rn((e & 1) ? w.y : w.x, x, a[k]);
           }
-        } else if (PCS) {
+        } else if (PCS || TMA) {
 #pragma unroll
           for (int k = 0; k < K; ++k)
-            a[k] = __fma_rn(pcs ? spc[(m * K + k) * 32 + lane] : D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
+            a[k] = __fma_rn((TMA || pcs) ? spc[(m * K + k) * 32 + lane] : D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
         } else {
 #pragma unroll
           for (int k = 0; k < K; ++k) a[k] = __fma_rn(D.pinv[ao(op, m * K + k, M * K)], x, a[k]);
@@ -466,6 +509,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       }
     }
     __syncthreads();  // the gather buffer becomes the face-value buffer
+    if (TMA && threadIdx.x == 0 && nxt < nch) {  // pinv consumed: the next chunk's
+      fence_proxy_async_smem();
+      issue_pinv(nxt);
+    }
     const bool chk = (v == 0 || v == 4);
     double viol = -1e300;
     if constexpr (STAGED && K >= 8) {
@@ -522,7 +569,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
           }
       }
     } else {
-      if (eval) eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl, STAGED ? sp + M * K : nullptr);
+      if (TMA) mbar_wait(&bar[1], it & 1);
+      if (eval)
+        eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
+                              STAGED ? sp + M * K : nullptr, TMA ? sphc : nullptr);
     }
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
@@ -569,12 +619,20 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       if (v == 0) s_pos[lane] = !(max(s_sev[0][lane], s_sev[1][lane]) | s_pos[lane] | s_bf[0][lane] | s_bf[1][lane]);
       __syncthreads();
       const int cb = ch << 5;
-      for (int p = threadIdx.x; p < Q * 32 * V5; p += 160) {
-        const int w = p % V5, q = (p / V5) % Q, l = p / (V5 * Q);
-        if (s_pos[l] && cb + l < D.n) W.fp[static_cast<size_t>(D.slot[ao(cb + l, q, Q)]) * V5 + w] = sval[q][w][l];
+      const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;  // thread (cell l, variable w)
+      if (s_pos[l] && cb + l < D.n) {
+        int sl[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) sl[q] = __ldg(&D.slot[ao(cb + l, q, Q)]);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(sl[q]) * V5 + w] = sval[q][w][l];
       }
     }
     __syncthreads();
+    if (TMA && threadIdx.x == 0 && nxt < nch) {  // phi consumed: the next chunk's
+      fence_proxy_async_smem();
+      issue_phi(nxt);
+    }
   }
 }
 
@@ -1253,6 +1311,8 @@ struct Kern3 {
   size_t smem_central, smem_cwenoz, smem_muscl, smem_central_staged;
   void (*central)(Dev3, Phys3, Work3, const double*, int, int);
   void (*central_staged)(Dev3, Phys3, Work3, const double*, int, int);
+  void (*central_tma)(Dev3, Phys3, Work3, const double*, int, int) = nullptr;  // per-cell rows, K*M <= 200
+  size_t smem_central_tma = 0;
   void (*spread)(Dev3, Work3, const double*, int);
   void (*cwenoz)(Dev3, Phys3, Work3, const double*);
   void (*muscl)(Dev3, Phys3, Work3, const double*);
@@ -1284,6 +1344,10 @@ Kern3 kern3() {
                          4 * static_cast<size_t>(NF * MD3 + 32);
   k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);
   k.central = k3_central<K, M, NF, NQ, false>;
+  if constexpr (K * M <= 200) {
+    k.central_tma = k3_central<K, M, NF, NQ, false, true>;
+    k.smem_central_tma = smem3_bytes(M + NF, Q) + 8 * static_cast<size_t>(M * K * 32 + Q * K * 32) + 16;
+  }
   k.central_staged = k3_central<K, M, NF, NQ, true>;
   k.spread = k3_spread<NF, NQ>;
   k.cwenoz = k3_cwenoz<K, M, NF, NQ, false>;
@@ -1737,6 +1801,12 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
       I.central_grid = grid_for(I.kern.central_staged, I.kern.smem_central_staged);
       I.central_grid = std::max(nops, I.central_grid - I.central_grid % nops);  // block b <-> type b % n_ops
     } else {
+      // per-cell rows: the TMA-staged central kernel (UCFVB_CENTRAL3_TMA=0: the cp.async one, diagnostics)
+      const char* e = std::getenv("UCFVB_CENTRAL3_TMA");
+      if (I.kern.central_tma && nops == n && !(e && e[0] == '0')) {
+        I.kern.central = I.kern.central_tma;
+        I.kern.smem_central = I.kern.smem_central_tma;
+      }
       I.central_grid = grid_for(I.kern.central, I.kern.smem_central);
     }
     if (I.staged) {

@@ -270,11 +270,13 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
 }
 
 // fallback (solver.cpp:229-264) after a troubled reconstruction; demoted cells
-// get first-order values. Then the block stores the chunk's final face values
-// from shared memory, five consecutive threads per face point (one contiguous
-// 40-byte record; the reconstruction's per-variable stores were scattered
-// 8-byte writes, and demoted cells' values were written twice)
-template <int NF, int NQ>
+// get first-order values. COOP (lattice-class kernels): the reconstruction
+// only staged its face values in shared memory, and the block now stores the
+// chunk's final values, five consecutive threads per face point (one
+// contiguous 40-byte record instead of scattered 8-byte stores per variable):
+// config 5 weights 26.4 -> 22.8 ms/stage; per-cell-row kernels (config 4c)
+// keep the per-thread stores (cooperative measured 4.76 vs 4.65 ms).
+template <int NF, int NQ, bool COOP>
 __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
                                                   int lane, bool act, double u0, bool chk, double blo, double bhi,
                                                   double viol, double (*sval)[V5][33], int* s_fail) {
@@ -283,9 +285,9 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
   __shared__ double s_u0[V5][32];
   if (v == 0) {
     s_fail[lane] = 0;
-    s_cell[lane] = act ? c : -1;
+    if (COOP) s_cell[lane] = act ? c : -1;
   }
-  s_u0[v][lane] = u0;
+  if (COOP) s_u0[v][lane] = u0;
   __syncthreads();
   if (P.mode == UCFVB_HYBRID) {
     if (chk) {
@@ -302,17 +304,27 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
     }
   }
   __syncthreads();
-  if (act && v == 0 && s_fail[lane]) W.labels[c] = UCFVB_SCHEME_FIRST;
-  {  // thread (cell l, variable w): all Q points of cell l, slots loaded up front
-    const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;
+  if constexpr (COOP) {
+    if (act && v == 0 && s_fail[lane]) W.labels[c] = UCFVB_SCHEME_FIRST;
+    const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;  // thread (cell l, variable w)
     const int cell = s_cell[l];
     if (cell >= 0) {
-      int sl[Q];
-#pragma unroll
-      for (int q = 0; q < Q; ++q) sl[q] = __ldg(&D.slot[ao(cell, q, Q)]);
       const bool fail = s_fail[l] != 0;
+      constexpr int G = 4;  // slot loads a group at a time (register pressure of the CWENOZ kernel)
+#pragma unroll 1
+      for (int q0 = 0; q0 < Q; q0 += G) {
+        int sl[G];
 #pragma unroll
-      for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(sl[q]) * V5 + w] = fail ? s_u0[w][l] : sval[q][w][l];
+        for (int j = 0; j < G; ++j) sl[j] = q0 + j < Q ? D.slot[ao(cell, q0 + j, Q)] : 0;
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+          if (q0 + j < Q) W.fp[static_cast<size_t>(sl[j]) * V5 + w] = fail ? s_u0[w][l] : sval[q0 + j][w][l];
+      }
+    }
+  } else {
+    if (act && s_fail[lane]) {
+      if (v == 0) W.labels[c] = UCFVB_SCHEME_FIRST;
+      for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5 + v] = u0;
     }
   }
   __syncthreads();
@@ -325,6 +337,12 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // memory once, read as broadcast 16-byte loads
 // nad bit 0: NAD classification (hybrid); bit 1: this stage detects (first
 // stage or detect_every_stage), so the raw label decides the final one
+// TMA staging of the phi block as well (pinv + phi: 1 block/SM, config 4
+// central 3.85 ms/stage; pinv only: 3 blocks/SM, 3.51 ms; cp.async pinv at the
+// chunk start: 3.61 ms). UCFVB_TMA3_PHI=1 builds the pinv + phi variant.
+#ifndef UCFVB_TMA3_PHI
+#define UCFVB_TMA3_PHI 0
+#endif
 // TMA: per-cell operator rows (config 4): the chunk's pinv block (group A)
 // and phi block (group B) are bulk-copied into shared memory one chunk ahead,
 // each refilled as soon as the solve / the evaluation has consumed it
@@ -354,11 +372,12 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
   constexpr bool PCS = !STAGED && !TMA && K * M <= 200;
   double* spc = smem3 + kUnion;
   double* sphc = spc + M * K * 32;  // TMA: the chunk's phi block
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sphc + Q * K * 32);  // TMA: [0] pinv, [1] phi
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sphc + (UCFVB_TMA3_PHI ? Q * K * 32 : 0));  // TMA: [0] pinv, [1] phi
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
   const int nch = (D.n + 31) >> 5;
+  constexpr bool kTmaPhi = TMA && UCFVB_TMA3_PHI;  // phi staged too (else read through L1)
   constexpr uint32_t kPinvBytes = M * K * 32 * 8, kPhiBytes = Q * K * 32 * 8;
   auto issue_pinv = [&](int ch) {
     mbar_arrive_expect_tx(&bar[0], kPinvBytes);
@@ -375,7 +394,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       mbar_fence_init();
       if (static_cast<int>(blockIdx.x) < nch) {
         issue_pinv(blockIdx.x);
-        issue_phi(blockIdx.x);
+        if (kTmaPhi) issue_phi(blockIdx.x);
       }
     }
     __syncthreads();
@@ -569,10 +588,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
           }
       }
     } else {
-      if (TMA) mbar_wait(&bar[1], it & 1);
+      if (kTmaPhi) mbar_wait(&bar[1], it & 1);
       if (eval)
         eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
-                              STAGED ? sp + M * K : nullptr, TMA ? sphc : nullptr);
+                              STAGED ? sp + M * K : nullptr, kTmaPhi ? sphc : nullptr);
     }
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
@@ -620,7 +639,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       __syncthreads();
       const int cb = ch << 5;
       const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;  // thread (cell l, variable w)
-      if (s_pos[l] && cb + l < D.n) {
+      if (s_pos[l] && cb + l < D.n) {  // every slot load in flight before the stores (end of the iteration: registers are free)
         int sl[Q];
 #pragma unroll
         for (int q = 0; q < Q; ++q) sl[q] = __ldg(&D.slot[ao(cb + l, q, Q)]);
@@ -629,7 +648,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       }
     }
     __syncthreads();
-    if (TMA && threadIdx.x == 0 && nxt < nch) {  // phi consumed: the next chunk's
+    if (kTmaPhi && threadIdx.x == 0 && nxt < nch) {  // phi consumed: the next chunk's
       fence_proxy_async_smem();
       issue_phi(nxt);
     }
@@ -698,11 +717,11 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
 }
 
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
-#ifndef UCFVB_CW3_MINB
-#define UCFVB_CW3_MINB 1
-#endif
+// lattice-class p = 3 (config 5): three resident blocks per SM (<= 136
+// registers; 168 unbounded) measured faster despite a few spills (22.3 vs
+// 25.2 ms/stage of weights); per-cell rows keep the unbounded allocation
 template <int K, int M, int NF, int NQ, bool STAGED>
-__global__ void __launch_bounds__(160, UCFVB_CW3_MINB) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+__global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
   constexpr int EP = M * K, ED = NF * 3 * MD3, EO = (K * K + 1) & ~1;  // region sizes (even: phi is read as double2)
@@ -994,7 +1013,9 @@ __global__ void __launch_bounds__(160, UCFVB_CW3_MINB) k3_cwenoz(Dev3 D, Phys3 P
           for (int j = 0; j < 2; ++j) {
             const int q = 8 * i + fr, cl = 8 * tt + 2 * fc + j;
             if (q < Q) {
-              sval[q][v][cl] = f[i][tt][j];  // stored by troubled_fallback
+              sval[q][v][cl] = f[i][tt][j];
+              const int cc2 = scell[cl];
+              if (!STAGED && cc2 >= 0) W.fp[static_cast<size_t>(D.slot[ao(cc2, q, Q)]) * V5 + v] = f[i][tt][j];
             }
           }
       __syncthreads();  // every face value of the chunk in sval
@@ -1005,10 +1026,10 @@ __global__ void __launch_bounds__(160, UCFVB_CW3_MINB) k3_cwenoz(Dev3 D, Phys3 P
         }
     } else {
       __syncthreads();  // the gather buffer becomes the face-value buffer
-      eval_store<K, NQ, NF, K, false>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
-                                      STAGED ? sp + EP + ED + EO : nullptr);
+      eval_store<K, NQ, NF, K, !STAGED>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
+                                             STAGED ? sp + EP + ED + EO : nullptr);
     }
-    troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
 
@@ -1117,9 +1138,9 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       blo = W.bounds[ao(c, v == 0 ? 0 : 2, 4)];
       bhi = W.bounds[ao(c, v == 0 ? 1 : 3, 4)];
     }
-    eval_store<K, NQ, NF, 3, false>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
-                                    STAGED ? sp + 3 * M : nullptr);
-    troubled_fallback<NF, NQ>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+    eval_store<K, NQ, NF, 3, !STAGED>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
+                                           STAGED ? sp + 3 * M : nullptr);
+    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
   }
 }
 
@@ -1346,7 +1367,7 @@ Kern3 kern3() {
   k.central = k3_central<K, M, NF, NQ, false>;
   if constexpr (K * M <= 200) {
     k.central_tma = k3_central<K, M, NF, NQ, false, true>;
-    k.smem_central_tma = smem3_bytes(M + NF, Q) + 8 * static_cast<size_t>(M * K * 32 + Q * K * 32) + 16;
+    k.smem_central_tma = smem3_bytes(M + NF, Q) + 8 * static_cast<size_t>(M * K * 32 + (UCFVB_TMA3_PHI ? Q * K * 32 : 0)) + 16;
   }
   k.central_staged = k3_central<K, M, NF, NQ, true>;
   k.spread = k3_spread<NF, NQ>;

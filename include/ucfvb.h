@@ -229,6 +229,17 @@ int32_t ucfvb_run_steps(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0,
  * device state is the failing step's input (as ucfvb_run_steps). */
 int32_t ucfvb_advance_host(ucfvb_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
                            double t0, double* t_out);
+/* ucfvb_advance_host over n_batch independent states of the same mesh (an
+ * ensemble of run_simulation loops, run.cpp:87-132, one per initial state):
+ * entry i is u_in[i] -> n_steps steps -> u_out[i], t_out[i] (nullable) its
+ * final time. The entries are pipelined: the upload of entry i+1 and the
+ * download of entry i-1 run on copy streams while entry i is stepped, so the
+ * PCIe transfers leave the critical path; results are bit-identical to
+ * n_batch ucfvb_advance_host calls. Buffers should be pinned; u_out[i] may
+ * alias u_in[i] but no other entry's input. One synchronisation, at the end.
+ * On failure (the message names the entry) later entries are not computed. */
+int32_t ucfvb_advance_host_batch(ucfvb_solver* h, int32_t n_batch, const double* const* u_in,
+                                 double* const* u_out, int32_t n_steps, int32_t rk, double t0, double* t_out);
 /* ucfvb_run_steps plus each step's dt (run.cpp:99-112 CensusRow::dt): dt_out
  * (nullable) receives [n_steps] doubles; step k's end time is t0 + dt_0 + ...
  * + dt_k summed in step order, exactly as run_simulation's `t += dt`. */

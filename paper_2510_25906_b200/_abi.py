@@ -315,6 +315,8 @@ def _declare(lib):
         "ucfvb_compute_residual": (C.c_int32, [H, c_dp, C.c_double, c_dp]),
         "ucfvb_run_steps": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i64p]),
         "ucfvb_advance_host": (C.c_int32, [H, c_dp, c_dp, C.c_int32, C.c_int32, C.c_double, c_dp]),
+        "ucfvb_advance_host_batch": (C.c_int32, [H, C.c_int32, P(c_dp), P(c_dp), C.c_int32, C.c_int32,
+                                                 C.c_double, c_dp]),
         "ucfvb_run_steps_log": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i64p,
                                             c_dp]),
         "ucfvb_run_until": (C.c_int32, [H, C.c_int32, C.c_int32, C.c_double, C.c_double, c_dp, c_i32p, c_i64p,
@@ -368,7 +370,7 @@ ABI_SYMBOLS = [
     "ucfvb_mesh_free", "ucfvb_build_stencils", "ucfvb_stencils_get_view", "ucfvb_stencils_free",
     "ucfvb_project_initial", "ucfvb_create", "ucfvb_destroy", "ucfvb_set_state",
     "ucfvb_get_state", "ucfvb_max_stable_dt", "ucfvb_advance", "ucfvb_compute_residual",
-    "ucfvb_run_steps", "ucfvb_run_steps_log", "ucfvb_run_until", "ucfvb_advance_host", "ucfvb_write_field_snapshot", "ucfvb_write_census_csv",
+    "ucfvb_run_steps", "ucfvb_run_steps_log", "ucfvb_run_until", "ucfvb_advance_host", "ucfvb_advance_host_batch", "ucfvb_write_field_snapshot", "ucfvb_write_census_csv",
     "ucfvb_write_timing_csv", "ucfvb_get_step_labels", "ucfvb_get_labels", "ucfvb_get_census",
     "ucfvb_get_nad_ties", "ucfvb_set_list_policy", "ucfvb_get_list_stats", "ucfvb_get_face_values", "ucfvb_get_dofs", "ucfvb_set_phase_timing",
     "ucfvb_get_phase_times", "ucfvb_n_cells", "ucfvb_n_faces", "ucfvb_n_qp",

@@ -169,6 +169,13 @@ int32_t ucfvb_advance_host(ucfvb_solver* h, const double* u_in, double* u_out, i
     if (t_out) *t_out = t;
   });
 }
+int32_t ucfvb_advance_host_batch(ucfvb_solver* h, int32_t n_batch, const double* const* u_in, double* const* u_out,
+                                 int32_t n_steps, int32_t rk, double t0, double* t_out) {
+  return guard(h, [&] {
+    if (!u_in || !u_out) throw ucfvb::ApiError(UCFVB_INVALID, "advance_host_batch: null pointer table");
+    h->s->advance_host_batch(n_batch, u_in, u_out, n_steps, rk, t0, t_out);
+  });
+}
 int32_t ucfvb_run_steps_log(ucfvb_solver* h, int32_t n_steps, int32_t rk, double t0, double t_end, double* t_out,
                             int64_t* census_out, double* dt_out) {
   return guard(h, [&] {

@@ -566,6 +566,13 @@ struct GpuSolver::Impl {
 
   int err_step = 0;
   char* host_stage = nullptr;  // pinned DtState + error word for advance_host
+  // advance_host_batch: device staging per direction, copy streams, events, pinned per-entry slots
+  double4* pipe_up[2] = {nullptr, nullptr};
+  double4* pipe_down[2] = {nullptr, nullptr};
+  cudaStream_t up_stream = nullptr, down_stream = nullptr;
+  cudaEvent_t pipe_ev[8] = {};
+  char* pipe_host = nullptr;
+  int pipe_slots = 0;
   int read_error(int* kind, int* face, int* cell) {
     int e[4];
     CK(cudaMemcpyAsync(e, S.err, sizeof e, cudaMemcpyDeviceToHost, stream));
@@ -630,6 +637,11 @@ struct GpuSolver::Impl {
     if (census_dev) cudaFree(census_dev);
     if (dtlog_dev) cudaFree(dtlog_dev);
     if (host_stage) cudaFreeHost(host_stage);
+    if (pipe_host) cudaFreeHost(pipe_host);
+    for (auto& e : pipe_ev)
+      if (e) cudaEventDestroy(e);
+    if (up_stream) cudaStreamDestroy(up_stream);
+    if (down_stream) cudaStreamDestroy(down_stream);
     if (hcounts) cudaFreeHost(hcounts);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
@@ -1105,6 +1117,108 @@ double GpuSolver::advance_host(const double* u_in, double* u_out, int n_steps, i
     I.raise_device_error(he[0], he[1], he[2]);
   }
   return hs->t + hs->dt;
+}
+
+// The pipelined form of advance_host over independent states of one mesh (an
+// ensemble): the upload of state i+1 and the download of result i-1 run on two
+// copy streams (both PCIe directions) while state i is stepped. Two device
+// staging buffers per direction; the compute stream copies staging -> state
+// buffer and state buffer -> staging device-to-device (2 x 32 B/cell at HBM
+// rate), so the captured step graphs and their buffers are untouched.
+void GpuSolver::advance_host_batch(int n_batch, const double* const* u_in, double* const* u_out, int n_steps, int rk,
+                                   double t0, double* t_out) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance_host_batch: unknown integrator");
+  if (n_steps <= 0) throw ApiError(UCFVB_INVALID, "advance_host_batch: n_steps must be >= 1");
+  if (n_batch <= 0) throw ApiError(UCFVB_INVALID, "advance_host_batch: n_batch must be >= 1");
+  for (int i = 0; i < n_batch; ++i)
+    if (!u_in[i] || !u_out[i]) throw ApiError(UCFVB_INVALID, "advance_host_batch: null state pointer");
+  const size_t bytes = sizeof(double4) * I.L.n;
+  if (!I.pipe_up[0]) {
+    for (int i = 0; i < 2; ++i) {
+      I.pipe_up[i] = dalloc<double4>(I.L.n, I.owned);
+      I.pipe_down[i] = dalloc<double4>(I.L.n, I.owned);
+    }
+    CK(cudaStreamCreateWithFlags(&I.up_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&I.down_stream, cudaStreamNonBlocking));
+    for (auto& e : I.pipe_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // pinned per-entry slots: the dt-state each entry starts from, and what it ended with
+  const size_t slot = 2 * sizeof(DtState) + 4 * sizeof(int);
+  if (I.pipe_slots < n_batch) {
+    if (I.pipe_host) CK(cudaFreeHost(I.pipe_host));
+    I.pipe_host = nullptr;
+    CK(cudaMallocHost(&I.pipe_host, slot * n_batch));
+    I.pipe_slots = n_batch;
+  }
+  auto hs_in = [&](int i) { return reinterpret_cast<DtState*>(I.pipe_host + slot * i); };
+  auto hs_out = [&](int i) { return reinterpret_cast<DtState*>(I.pipe_host + slot * i + sizeof(DtState)); };
+  auto he = [&](int i) { return reinterpret_cast<int*>(I.pipe_host + slot * i + 2 * sizeof(DtState)); };
+  // events: [0..1] upload landed, [2..3] upload buffer consumed, [4..5] result staged, [6..7] download done
+  cudaEvent_t* ev = I.pipe_ev;
+  I.reset_ties();
+  I.S.step = &I.ds->step;
+  const int cur0 = I.cur;
+  int64_t nl = 0;
+  for (int i = 0; i < n_batch; ++i) {
+    const int b = i & 1;
+    if (i >= 2) CK(cudaStreamWaitEvent(I.up_stream, ev[2 + b], 0));
+    CK(cudaMemcpyAsync(I.pipe_up[b], u_in[i], bytes, cudaMemcpyHostToDevice, I.up_stream));
+    CK(cudaEventRecord(ev[b], I.up_stream));
+    CK(cudaStreamWaitEvent(I.stream, ev[b], 0));
+    I.cur = cur0;
+    CK(cudaMemcpyAsync(I.ubuf[I.cur], I.pipe_up[b], bytes, cudaMemcpyDeviceToDevice, I.stream));
+    CK(cudaEventRecord(ev[2 + b], I.stream));
+    DtState* hs = hs_in(i);
+    *hs = DtState{};
+    hs->dmin_bits = static_cast<unsigned long long>(0x7e37e43c8800759cULL);  // bits of 1e300
+    hs->t = t0;
+    hs->step = -1;
+    hs->t_end = INFINITY;
+    hs->cfl = I.opt.cfl;
+    CK(cudaMemcpyAsync(I.ds, hs, sizeof(DtState), cudaMemcpyHostToDevice, I.stream));
+    nl += I.launch_dt_reduce(I.ubuf[I.cur]);
+    for (int s = 0; s < n_steps; ++s) {
+      if (I.opt.use_graphs && !I.timing) {
+        cudaGraphExec_t g = I.get_graph(rk, true, I.cur);
+        CK(cudaGraphLaunch(g, I.stream));
+        nl += I.graph_launches[rk][1][I.cur];
+      } else {
+        nl += I.launch_step(rk, true, I.ubuf[I.cur], I.ubuf[I.cur ^ 1], false);
+      }
+      I.cur ^= 1;
+    }
+    I.allreduce_error();
+    CK(cudaMemcpyAsync(he(i), I.S.err, 4 * sizeof(int), cudaMemcpyDeviceToHost, I.stream));
+    CK(cudaMemcpyAsync(hs_out(i), I.ds, sizeof(DtState), cudaMemcpyDeviceToHost, I.stream));
+    if (i >= 2) CK(cudaStreamWaitEvent(I.stream, ev[6 + b], 0));
+    CK(cudaMemcpyAsync(I.pipe_down[b], I.ubuf[I.cur], bytes, cudaMemcpyDeviceToDevice, I.stream));
+    CK(cudaEventRecord(ev[4 + b], I.stream));
+    CK(cudaStreamWaitEvent(I.down_stream, ev[4 + b], 0));
+    CK(cudaMemcpyAsync(u_out[i], I.pipe_down[b], bytes, cudaMemcpyDeviceToHost, I.down_stream));
+    CK(cudaEventRecord(ev[6 + b], I.down_stream));
+  }
+  I.launches = nl;
+  I.S.step = I.step_zero;
+  I.fetch_counts();
+  CK(cudaStreamSynchronize(I.stream));
+  CK(cudaStreamSynchronize(I.down_stream));
+  CK(cudaGetLastError());
+  I.stage_is_first = false;
+  I.adapt_lists();
+  for (int i = 0; i < n_batch; ++i) {
+    if (he(i)[0]) {
+      // the error word is sticky: entry i failed and the later entries did not run
+      I.cur = cur0;
+      const int k = he(i)[0], f = he(i)[1], c = he(i)[2];
+      try {
+        I.raise_device_error(k, f, c);
+      } catch (ApiError& e) {
+        throw ApiError(e.code, std::string(e.what()) + " (batch entry " + std::to_string(i) + ")");
+      }
+    }
+    if (t_out) t_out[i] = hs_out(i)->t + hs_out(i)->dt;
+  }
 }
 
 void GpuSolver::get_labels(uint8_t* out, bool step) {

@@ -29,6 +29,10 @@ class GpuSolver {
   // host state in -> n_steps graph-replayed steps -> host state out, with one
   // synchronisation (the host-buffer form of state() + advance loop)
   double advance_host(const double* u_in, double* u_out, int n_steps, int rk, double t0);
+  // n_batch independent states through advance_host, pipelined: uploads and
+  // downloads overlap the stepping of the neighbouring entries
+  void advance_host_batch(int n_batch, const double* const* u_in, double* const* u_out, int n_steps, int rk,
+                          double t0, double* t_out);
   // run_simulation's loop condition (run.cpp:96): steps while t < t_end - 1e-14 t_end, at most max_steps
   double run_until(int max_steps, int rk, double t0, double t_end, int64_t* census, double* dt_out, int* n_done);  // run.cpp:97-132
 

@@ -147,6 +147,20 @@ class Solver:
         self._ck(self._lib.ucfvb_advance_host(self._h, _dp(u_in), _dp(out), n_steps, rk, t0, C.byref(t)))
         return out, t.value
 
+    def advance_host_batch(self, u_in, n_steps: int = 1, rk: int = A.RK3, t0: float = 0.0, u_out=None):
+        """advance_host over independent states (an ensemble), pipelined: the PCIe copies of
+        neighbouring entries overlap the stepping. u_in / u_out: sequences of [n_cells][4] arrays
+        (pinned for true overlap). Returns (outs, t[n_batch])."""
+        ins = [np.ascontiguousarray(u, dtype=np.float64).reshape(self.n_cells, 4) for u in u_in]
+        outs = [np.empty_like(u) for u in ins] if u_out is None else list(u_out)
+        nb = len(ins)
+        tab_in = (A.c_dp * nb)(*[_dp(u) for u in ins])
+        tab_out = (A.c_dp * nb)(*[_dp(u) for u in outs])
+        t = np.zeros(nb)
+        self._ck(self._lib.ucfvb_advance_host_batch(self._h, nb, tab_in, tab_out, int(n_steps), int(rk), float(t0),
+                                                    _dp(t)))
+        return outs, t
+
     def run_log(self, n_steps: int, rk: int = A.RK3, t0: float = 0.0, t_end: float = float("inf")):
         """run_steps that also returns each step's dt: (t, census[n,4], dt[n])."""
         t = C.c_double()

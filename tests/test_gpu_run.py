@@ -151,3 +151,32 @@ def test_advance_host_matches_run_steps():
     import pytest
     with pytest.raises(A.NonPhysicalError):
         a.advance_host(bad, 1)
+
+
+def test_advance_host_batch_matches_serial():
+    """ucfvb_advance_host_batch (pipelined uploads / downloads over independent states)
+    gives every entry the bits of its own ucfvb_advance_host call; a failing entry is named."""
+    import numpy as np
+    import pytest
+    from paper_2510_25906_b200 import _abi as A
+    from paper_2510_25906_b200.mesh import Mesh, Stencils
+    from paper_2510_25906_b200.solver import Solver
+
+    mesh = Mesh.structured_tri(24, 24, (0.0, 0.0, 1.0, 1.0), jitter=0.1, seed=1, periodic="both", n_qp=2)
+    st = Stencils(mesh, 2)
+    o = A.options_from_dict(order=2, mode="hybrid", lambda1p=1e3, cfl=0.5)
+    ins = [mesh.project_initial(2, [0.5, 0.5, 0.01], seed=3 + i, degree=4) * (1.0 + 0.05 * i) for i in range(5)]
+    a = Solver(mesh, o, stencils=st)
+    for n_steps in (1, 2):
+        outs, ts = a.advance_host_batch(ins, n_steps)
+        for u, out, t in zip(ins, outs, ts):
+            ref, t_ref = a.advance_host(u, n_steps)
+            assert t == t_ref
+            np.testing.assert_array_equal(out, ref)
+    bad = [u.copy() for u in ins]
+    bad[3][5, 0] = -1.0
+    with pytest.raises(A.NonPhysicalError, match="batch entry 3"):
+        a.advance_host_batch(bad, 1)
+    # the solver is usable after the failure
+    outs, _ = a.advance_host_batch(ins[:2], 1)
+    np.testing.assert_array_equal(outs[1], a.advance_host(ins[1], 1)[0])

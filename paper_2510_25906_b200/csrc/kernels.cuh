@@ -80,10 +80,10 @@ struct Layout {
   const double* h;          // [n]
   const double* inv_vol;    // [n] 1/area
   // per-cell records of the troubled-cell operator rows (kernels_cells.cuh, CellRec)
-  const unsigned char* rec_ca;  // CWENOZ group A [n][CA]
-  const unsigned char* rec_cb;  // CWENOZ group B [n][CB]
-  const unsigned char* rec_ma;  // MUSCL group A  [n][MA]
-  const unsigned char* rec_mb;  // MUSCL group B  [n][MB]
+  const unsigned char* rec_ca;  // CWENOZ records [n][GC]: group A at 0
+  const unsigned char* rec_cb;  //   group B at CA (= rec_ca + CA)
+  const unsigned char* rec_ma;  // MUSCL records [n][GM]: group A at 0
+  const unsigned char* rec_mb;  //   group B at MA (= rec_ma + MA)
 };
 
 struct Physics {
@@ -349,31 +349,55 @@ __global__ void __launch_bounds__(kBlock) k_central(Layout L, Physics ph, Scratc
 // (detector.cpp:37-53 reads `in` only, so push == pull); Linear cells whose
 // pre-check failed become FirstOrder (fallback_check); the troubled classes
 // are compacted into lists with one atomic per warp (ballot + popc).
-template <int K, int NQ, int NF, int MMT, int MDT, bool UNI>
+// CPT cells per thread (cell = block base + i * kBlock + thread): on large
+// meshes the one-cell form is bound by its per-block latency chain (neighbour
+// ids -> raw labels -> block barrier -> returning global atomic -> list
+// store) and by ~n/128 same-address atomics per counter; CPT = 8 keeps eight
+// independent chains per thread in flight and issues one atomic per 1024 cells.
+template <int K, int NQ, int NF, int MMT, int MDT, bool UNI, int CPT>
 __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const double4* __restrict__ U, int flags,
                                                    int detect) {
   constexpr int Q = NF * NQ;
-  const int c = blockIdx.x * kBlock + threadIdx.x;
+  constexpr int NW = kBlock / 32;
+  const int base = blockIdx.x * (kBlock * CPT) + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  const int w = threadIdx.x >> 5;
   pdl_wait();
-  int lab = -1;
-  if (c < L.n && !*(volatile int*)S.err) {
-    const int r = S.raw[c];
-    if (detect) {
-      lab = r & 3;
+  const bool ok = !*(volatile int*)S.err;
+  int lab[CPT], raw[CPT], nb[CPT][NF];
 #pragma unroll
-      for (int j = 0; j < NF; ++j) {
-        const int nb = __ldg(L.nbr + aos(c, j, NF));
-        if (nb >= 0) {
-          const int rn = S.raw[nb] & 3;
-          lab = lab < rn ? rn : lab;
-        }
-      }
-    } else {
-      lab = S.labels[c];  // frozen classification (detect_every_stage = false)
+  for (int i = 0; i < CPT; ++i) {
+    const int c = base + i * kBlock;
+    const bool live = ok && c < L.n;
+    raw[i] = live ? S.raw[c] : 0;
+    lab[i] = -1;
+    if (detect) {
+#pragma unroll
+      for (int j = 0; j < NF; ++j) nb[i][j] = live ? __ldg(L.nbr + aos(c, j, NF)) : -1;
+    } else if (live) {
+      lab[i] = S.labels[c];  // frozen classification (detect_every_stage = false)
     }
-    if (lab == 0 && (r & 4)) lab = 3;
-    if (lab == 3) {
+  }
+  if (detect) {
+    int rn[CPT][NF];
+#pragma unroll
+    for (int i = 0; i < CPT; ++i)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) rn[i][j] = nb[i][j] >= 0 ? S.raw[nb[i][j]] & 3 : 0;
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      int l = raw[i] & 3;
+#pragma unroll
+      for (int j = 0; j < NF; ++j) l = l < rn[i][j] ? rn[i][j] : l;
+      lab[i] = (ok && base + i * kBlock < L.n) ? l : -1;
+    }
+  }
+  unsigned mc[CPT], mm[CPT];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = base + i * kBlock;
+    if (lab[i] == 0 && (raw[i] & 4)) lab[i] = 3;
+    if (lab[i] == 3) {
       const d4 u0 = ld4(&U[c]);
       const int nf = UNI ? NF : L.nfc[c];
 #pragma unroll
@@ -385,73 +409,56 @@ __global__ void __launch_bounds__(kBlock) k_spread(Layout L, Scratch S, const do
         for (int k = 0; k < K; ++k) st4(&S.dofs[aos(c, k, K)], z);
       }
     }
-    S.labels[c] = static_cast<uint8_t>(lab);
+    if (lab[i] >= 0) S.labels[c] = static_cast<uint8_t>(lab[i]);
+    mc[i] = __ballot_sync(kFull, lab[i] == 1);
+    mm[i] = __ballot_sync(kFull, lab[i] == 2);
   }
-  const unsigned mc = __ballot_sync(kFull, lab == 1);
-  const unsigned mm = __ballot_sync(kFull, lab == 2);
   const unsigned lt = (1u << lane) - 1u;
-  if (flags & FL_CHUNKS) {  // one entry per 32-cell chunk (= this warp) with troubled cells
-    // block-aggregated: one global atomic per block and class (the chunk lists
-    // are unordered; per-cell results do not depend on the order)
-    // The cell totals (counts[0]/[1]) are not list lengths here (list
-    // statistics only).
-    __shared__ int s_nc, s_nm, s_bc, s_bm, s_cc, s_cm;
-    if (threadIdx.x == 0) s_nc = s_nm = s_cc = s_cm = 0;
-    __syncthreads();
-    int pc = -1, pm = -1;
-    if (lane == 0 && mc) {
-      pc = atomicAdd(&s_nc, 1);
-      atomicAdd(&s_cc, __popc(mc));
-    }
-    if (lane == 0 && mm) {
-      pm = atomicAdd(&s_nm, 1);
-      atomicAdd(&s_cm, __popc(mm));
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      s_bc = s_nc ? atomicAdd(&S.counts[2], s_nc) : 0;
-      s_bm = s_nm ? atomicAdd(&S.counts[3], s_nm) : 0;
-      if (s_cc) atomicAdd(&S.counts[0], s_cc);
-      if (s_cm) atomicAdd(&S.counts[1], s_cm);
-    }
-    __syncthreads();
-    if (pc >= 0) S.chunks_c[s_bc + pc] = make_int2(c >> 5, static_cast<int>(mc));
-    if (pm >= 0) S.chunks_m[s_bm + pm] = make_int2(c >> 5, static_cast<int>(mm));
-    return;
-  }
-  // dense per-cell lists, block-aggregated: one global atomic per block and
-  // class; entries keep warp order inside the block (the lists are unordered
-  // across blocks; per-cell results do not depend on the order). The chunk
-  // totals (counts[2]/[3]) are list statistics only.
-  __shared__ int s_wc[kBlock / 32], s_wm[kBlock / 32], s_bc, s_bm;
-  const int w = threadIdx.x >> 5;
+  // per (i, warp) counts -> block-exclusive offsets in cell order; one global
+  // atomic per block and class (the lists are unordered across blocks;
+  // per-cell results do not depend on the order)
+  __shared__ int s_c[CPT * NW], s_m[CPT * NW], s_bc, s_bm;
+  const bool chunks = (flags & FL_CHUNKS) != 0;  // one entry per 32-cell chunk (= one warp iteration)
   if (lane == 0) {
-    s_wc[w] = __popc(mc);
-    s_wm[w] = __popc(mm);
+#pragma unroll
+    for (int i = 0; i < CPT; ++i) {
+      s_c[i * NW + w] = chunks ? (mc[i] ? 1 : 0) | (__popc(mc[i]) << 8) : __popc(mc[i]) | ((mc[i] ? 1 : 0) << 8);
+      s_m[i * NW + w] = chunks ? (mm[i] ? 1 : 0) | (__popc(mm[i]) << 8) : __popc(mm[i]) | ((mm[i] ? 1 : 0) << 8);
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int tc = 0, tm = 0, kc = 0, km = 0;
+    // low byte: list entries (cells, or chunks under FL_CHUNKS); high bits: the
+    // other total (list statistics only)
+    int tc = 0, tm = 0, xc = 0, xm = 0;
 #pragma unroll
-    for (int i = 0; i < kBlock / 32; ++i) {
-      tc += s_wc[i];
-      tm += s_wm[i];
-      kc += s_wc[i] ? 1 : 0;
-      km += s_wm[i] ? 1 : 0;
+    for (int i = 0; i < CPT * NW; ++i) {
+      const int a = s_c[i], b = s_m[i];
+      s_c[i] = tc;
+      s_m[i] = tm;
+      tc += a & 255;
+      tm += b & 255;
+      xc += a >> 8;
+      xm += b >> 8;
     }
-    s_bc = tc ? atomicAdd(&S.counts[0], tc) : 0;
-    s_bm = tm ? atomicAdd(&S.counts[1], tm) : 0;
-    if (kc) atomicAdd(&S.counts[2], kc);
-    if (km) atomicAdd(&S.counts[3], km);
+    const int ic = chunks ? 2 : 0, is = chunks ? 0 : 2;
+    s_bc = tc ? atomicAdd(&S.counts[ic], tc) : 0;
+    s_bm = tm ? atomicAdd(&S.counts[ic + 1], tm) : 0;
+    if (xc) atomicAdd(&S.counts[is], xc);
+    if (xm) atomicAdd(&S.counts[is + 1], xm);
   }
   __syncthreads();
-  int oc = s_bc, om = s_bm;
-  for (int i = 0; i < w; ++i) {
-    oc += s_wc[i];
-    om += s_wm[i];
+#pragma unroll
+  for (int i = 0; i < CPT; ++i) {
+    const int c = base + i * kBlock;
+    if (chunks) {
+      if (lane == 0 && mc[i]) S.chunks_c[s_bc + s_c[i * NW + w]] = make_int2(c >> 5, static_cast<int>(mc[i]));
+      if (lane == 0 && mm[i]) S.chunks_m[s_bm + s_m[i * NW + w]] = make_int2(c >> 5, static_cast<int>(mm[i]));
+    } else {
+      if (lab[i] == 1) S.list_c[s_bc + s_c[i * NW + w] + __popc(mc[i] & lt)] = c;
+      if (lab[i] == 2) S.list_m[s_bm + s_m[i * NW + w] + __popc(mm[i] & lt)] = c;
+    }
   }
-  if (lab == 1) S.list_c[oc + __popc(mc & lt)] = c;
-  if (lab == 2) S.list_m[om + __popc(mm & lt)] = c;
 }
 
 // ---------------------------------------------------------------------------

@@ -40,6 +40,11 @@ struct CellRec {
   static constexpr uint32_t MA = round16(MA_ID + MM * 4);
   static constexpr uint32_t MB_PHI = 0, MB_NBR = Q * 2 * 8, MB_DST = MB_NBR + NF * 4;
   static constexpr uint32_t MB = round16(MB_DST + Q * 4);
+  // in HBM a cell's CWENOZ groups A | B share one record, and so do its MUSCL
+  // groups, each record a whole number of 64-byte lines (the L2's DRAM fetch
+  // granularity): p = 3 CWENOZ 240 + 1120 -> 22 lines, MUSCL 368 + 144 = 8
+  // lines exactly; unaligned separate records touched ~1.5 more lines per cell
+  static constexpr uint32_t GC = (CA + CB + 63u) & ~63u, GM = (MA + MB + 63u) & ~63u;
   static constexpr uint32_t SCA = odd16(CA), SCB = odd16(CB), SMA = odd16(MA), SMB = odd16(MB);
   static constexpr uint32_t TILE_A = TC * (SCA > SMA ? SCA : SMA);  // TC cells per tile
   static constexpr uint32_t TILE_B = TC * (SCB > SMB ? SCB : SMB);
@@ -48,20 +53,19 @@ struct CellRec {
 
 // one thread per cell: AoSoA element e of cell c -> the cell's records
 template <int K, int NQ, int NF, int MM, int MD>
-__global__ void k_pack_records(Layout L, unsigned char* ca, unsigned char* cb, unsigned char* ma,
-                               unsigned char* mb) {
+__global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
   using R = CellRec<K, NQ, NF, MM, MD>;
   constexpr int Q = R::Q;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= L.n) return;
   {
-    double* pd = reinterpret_cast<double*>(ca + static_cast<size_t>(c) * R::CA + R::CA_PD);
-    int* id = reinterpret_cast<int*>(ca + static_cast<size_t>(c) * R::CA + R::CA_ID);
+    double* pd = reinterpret_cast<double*>(rc + static_cast<size_t>(c) * R::GC + R::CA_PD);
+    int* id = reinterpret_cast<int*>(rc + static_cast<size_t>(c) * R::GC + R::CA_ID);
     for (int e = 0; e < NF * MD * 2; ++e) pd[e] = L.pinv_dir[aos(c, e, NF * MD * 2)];
     for (int e = 0; e < NF * MD; ++e) id[e] = L.dir_idx[aos(c, e, NF * MD)];
   }
   {
-    unsigned char* r = cb + static_cast<size_t>(c) * R::CB;
+    unsigned char* r = rc + static_cast<size_t>(c) * R::GC + R::CA;
     double* oi = reinterpret_cast<double*>(r + R::CB_OI);
     double* ph = reinterpret_cast<double*>(r + R::CB_PHI);
     int* nb = reinterpret_cast<int*>(r + R::CB_NBR);
@@ -72,13 +76,13 @@ __global__ void k_pack_records(Layout L, unsigned char* ca, unsigned char* cb, u
     for (int e = 0; e < Q; ++e) ds[e] = L.dest[aos(c, e, Q)];
   }
   {
-    double* pl = reinterpret_cast<double*>(ma + static_cast<size_t>(c) * R::MA + R::MA_PL);
-    int* id = reinterpret_cast<int*>(ma + static_cast<size_t>(c) * R::MA + R::MA_ID);
+    double* pl = reinterpret_cast<double*>(rm + static_cast<size_t>(c) * R::GM + R::MA_PL);
+    int* id = reinterpret_cast<int*>(rm + static_cast<size_t>(c) * R::GM + R::MA_ID);
     for (int e = 0; e < MM * 2; ++e) pl[e] = L.pinv_lin[aos(c, e, MM * 2)];
     for (int e = 0; e < MM; ++e) id[e] = L.st_idx[aos(c, e, MM)];
   }
   {
-    unsigned char* r = mb + static_cast<size_t>(c) * R::MB;
+    unsigned char* r = rm + static_cast<size_t>(c) * R::GM + R::MA;
     double* p01 = reinterpret_cast<double*>(r + R::MB_PHI);
     int* nb = reinterpret_cast<int*>(r + R::MB_NBR);
     int* ds = reinterpret_cast<int*>(r + R::MB_DST);
@@ -146,18 +150,18 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     if (tid == 0) mbar_arrive_expect_tx(&bar[0], TC * (i < tc ? R::CA : R::MA));
     __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
-      bulk_g2s(ga + tid * R::SCA, L.rec_ca + static_cast<size_t>(c) * R::CA, R::CA, &bar[0]);
+      bulk_g2s(ga + tid * R::SCA, L.rec_ca + static_cast<size_t>(c) * R::GC, R::CA, &bar[0]);
     else
-      bulk_g2s(ga + tid * R::SMA, L.rec_ma + static_cast<size_t>(c) * R::MA, R::MA, &bar[0]);
+      bulk_g2s(ga + tid * R::SMA, L.rec_ma + static_cast<size_t>(c) * R::GM, R::MA, &bar[0]);
   };
   auto issue_b = [&](int i) {
     const int c = tile_cell(i, tid);
     if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * (i < tc ? R::CB : R::MB));
     __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
-      bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::CB, R::CB, &bar[1]);
+      bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::GC, R::CB, &bar[1]);
     else
-      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::MB, R::MB, &bar[1]);
+      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[1]);
   };
   if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);

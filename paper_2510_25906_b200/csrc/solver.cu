@@ -67,6 +67,9 @@ static void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   CK(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 
+// meshes from this size run k_spread with 8 cells per thread (kernels.cuh)
+constexpr int kSpreadWideCells = 1 << 20;
+
 // ---- kernel dispatch over (K, NQ, NF) ----------------------------------------
 struct KernelSet {
   void (*central)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
@@ -90,9 +93,9 @@ struct KernelSet {
   Launch cells = nullptr;
   void (*cells_setup)(int n_sm, int* grid, Launch* launch) = nullptr;
   int cells_grid = 0;
-  void (*pack_records)(cudaStream_t, const Layout&, unsigned char*, unsigned char*, unsigned char*,
-                       unsigned char*) = nullptr;
-  uint32_t rec_bytes[4] = {0, 0, 0, 0};  // CA, CB, MA, MB per cell
+  void (*pack_records)(cudaStream_t, const Layout&, unsigned char*, unsigned char*) = nullptr;
+  // per cell: CWENOZ record stride, group A bytes (= group B's offset), MUSCL record stride, group A bytes
+  uint32_t rec_bytes[4] = {0, 0, 0, 0};
 };
 
 using StageLaunch = void (*)(dim3, cudaStream_t, const Layout&, const Physics&, const Scratch&, const double4*, int);
@@ -133,7 +136,11 @@ KernelSet make_set() {
   s.central = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
                  int f) { launch_k(k_central<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, p, S, U, f); };
   s.spread = [](dim3 g, cudaStream_t st, const Layout& L, const Scratch& S, const double4* U, int f, int d) {
-    launch_k(k_spread<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, S, U, f, d);
+    // g.x = blocks of the one-cell-per-thread form; large meshes run 8 cells per thread
+    if (L.n >= kSpreadWideCells)
+      launch_k(k_spread<K, NQ, NF, MMT, MDT, UNI, 8>, dim3((g.x + 7) / 8), kBlock, 0, st, L, S, U, f, d);
+    else
+      launch_k(k_spread<K, NQ, NF, MMT, MDT, UNI, 1>, g, kBlock, 0, st, L, S, U, f, d);
   };
   s.cwenoz = [](dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S, const double4* U,
                 int f) { launch_k(k_cwenoz<K, NQ, NF, MMT, MDT, UNI>, g, kBlock, 0, st, L, p, S, U, f); };
@@ -170,14 +177,13 @@ KernelSet make_set() {
                               CellRec<K, NQ, NF, MMT, MDT, kCellTile>::BYTES + 16, n_sm, 4 * kCellTile);
       *launch = troubled_cells_launcher<K, NQ, NF, MMT, MDT>;
     };
-    s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* ca, unsigned char* cb, unsigned char* ma,
-                        unsigned char* mb) {
-      k_pack_records<K, NQ, NF, MMT, MDT><<<(L.n + 255) / 256, 256, 0, st>>>(L, ca, cb, ma, mb);
+    s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* rc, unsigned char* rm) {
+      k_pack_records<K, NQ, NF, MMT, MDT><<<(L.n + 255) / 256, 256, 0, st>>>(L, rc, rm);
     };
-    s.rec_bytes[0] = R::CA;
-    s.rec_bytes[1] = R::CB;
-    s.rec_bytes[2] = R::MA;
-    s.rec_bytes[3] = R::MB;
+    s.rec_bytes[0] = R::GC;
+    s.rec_bytes[1] = R::CA;
+    s.rec_bytes[2] = R::GM;
+    s.rec_bytes[3] = R::MA;
   }
   return s;
 }
@@ -752,13 +758,14 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
   L.h = dupload(H.h, own);
   L.inv_vol = dupload(H.inv_vol, own);
   if (I.ks.pack_records) {  // per-cell records of the troubled-cell rows (kernels_cells.cuh)
-    unsigned char* rec[4];
-    for (int i = 0; i < 4; ++i) rec[i] = dalloc<unsigned char>(static_cast<size_t>(H.n) * I.ks.rec_bytes[i], own);
-    L.rec_ca = rec[0];
-    L.rec_cb = rec[1];
-    L.rec_ma = rec[2];
-    L.rec_mb = rec[3];
-    I.ks.pack_records(I.stream, L, rec[0], rec[1], rec[2], rec[3]);
+    // one CWENOZ and one MUSCL record per cell (64-byte-line multiples), group B behind group A
+    unsigned char* rc = dalloc<unsigned char>(static_cast<size_t>(H.n) * I.ks.rec_bytes[0], own);
+    unsigned char* rm = dalloc<unsigned char>(static_cast<size_t>(H.n) * I.ks.rec_bytes[2], own);
+    L.rec_ca = rc;
+    L.rec_cb = rc + I.ks.rec_bytes[1];
+    L.rec_ma = rm;
+    L.rec_mb = rm + I.ks.rec_bytes[3];
+    I.ks.pack_records(I.stream, L, rc, rm);
     CK(cudaGetLastError());
   }
 

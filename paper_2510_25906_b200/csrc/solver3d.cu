@@ -1170,10 +1170,10 @@ __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
   }
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
-    const double* UL = &W.fp[(static_cast<size_t>(f) * NQ + q) * 2 * V5];
+    const double* UL = &W.fp[(static_cast<size_t>(f) * 2 * NQ + q) * V5];  // [face][side][q][5]
     double ul[5], ur[5], n[3], fl[5];
 #pragma unroll
-    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[V5 + v];
+    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[NQ * V5 + v];
 #pragma unroll
     for (int d = 0; d < 3; ++d) n[d] = D.fnrm[(static_cast<size_t>(f) * NQ + q) * 3 + d];
     ok = riemann3(P.hll, ul, ur, n, P.gamma, fl) && ok;
@@ -1203,10 +1203,10 @@ __global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3
   double t[V5];
   bool ok = true;
   {
-    const double* UL = &W.fp[(static_cast<size_t>(f) * NQ + q) * 2 * V5];
+    const double* UL = &W.fp[(static_cast<size_t>(f) * 2 * NQ + q) * V5];  // [face][side][q][5]
     double ul[5], ur[5], n[3], fl[5];
 #pragma unroll
-    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[V5 + v];
+    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[NQ * V5 + v];
 #pragma unroll
     for (int d = 0; d < 3; ++d) n[d] = D.fnrm[(static_cast<size_t>(f) * NQ + q) * 3 + d];
     ok = skip || riemann3(P.hll, ul, ur, n, P.gamma, fl);
@@ -1725,7 +1725,18 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     }
     D.central = upload_ao(s.central, n, M + 1);
     D.nbr = upload_ao(m.cell_nbr, n, NF);
-    D.slot = upload_ao(s.qp_slot, n, Q);
+    {
+      // device face-point order [face][side][q] (the view's slot is (face*nq + q)*2 + side): the
+      // points a cell writes on one face are one contiguous run of nq*40 bytes (config 4: five
+      // whole sectors, config 5: 7.5) instead of nq 40-byte pieces interleaved with the other side's
+      std::vector<int32_t> ds(static_cast<size_t>(n) * Q);
+      for (size_t i = 0; i < ds.size(); ++i) {
+        const int32_t sl = s.qp_slot[i];
+        const int32_t side = sl & 1, fq = sl >> 1, f = fq / NQ, q = fq - f * NQ;
+        ds[i] = (f * 2 + side) * NQ + q;
+      }
+      D.slot = upload_ao(ds.data(), n, Q);
+    }
     {
       std::vector<int32_t> cf(static_cast<size_t>(n) * NF);
       for (size_t i = 0; i < cf.size(); ++i) cf[i] = (m.cell_faces[i] << 1) | (m.cell_side[i] ? 1 : 0);
@@ -2007,9 +2018,16 @@ void GpuSolver3::get_labels(int which, uint8_t* out) {
 
 void GpuSolver3::get_face_values(double* out) {
   CK3(cudaSetDevice(p_->device));
-  CK3(cudaMemcpyAsync(out, p_->W.fp, sizeof(double) * static_cast<size_t>(p_->nF) * p_->NQ * 2 * V5,
-                      cudaMemcpyDeviceToHost, p_->st));
+  const int NQ = p_->NQ;
+  std::vector<double> dev(static_cast<size_t>(p_->nF) * NQ * 2 * V5);
+  CK3(cudaMemcpyAsync(dev.data(), p_->W.fp, sizeof(double) * dev.size(), cudaMemcpyDeviceToHost, p_->st));
   CK3(cudaStreamSynchronize(p_->st));
+  // device order [face][side][q] -> the view's slot order [face][q][side]
+  for (int64_t f = 0; f < p_->nF; ++f)
+    for (int q = 0; q < NQ; ++q)
+      for (int side = 0; side < 2; ++side)
+        for (int v = 0; v < V5; ++v)
+          out[((f * NQ + q) * 2 + side) * V5 + v] = dev[((f * 2 + side) * NQ + q) * V5 + v];
 }
 
 void GpuSolver3::census(int64_t out[4]) {

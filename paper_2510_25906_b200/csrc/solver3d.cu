@@ -209,6 +209,33 @@ __host__ __device__ constexpr size_t smem3_bytes(int G, int Q) {
   return 8 * static_cast<size_t>((G * 160 > Q * V5 * 33) ? G * 160 : Q * V5 * 33);
 }
 
+// Shared-memory strides of the lattice-class tensor-core (DMMA) kernels, all in
+// doubles. An m8n8k4 fragment load has lane (fr = lane / 4, fc = lane % 4) read
+// element (row 4*ks + fc, column fr) or (row fr, column fc): with a row stride
+// = 4 (mod 16) the 16 lanes of a half warp fall into 16 distinct 8-byte banks
+// (strides 160 / 32 / K = 19 gave 2- to 8-way conflicts: 47 % of the central
+// kernel's shared-memory wavefronts were replays).
+//   gather buffer  xs[row g][variable v][cell l] = g * kXS + v * kVS + l
+//   operator rows  pinv [M][KP], phi [Q][KP], OI [K][KP], KP = kpad(K)
+//   dofs           sd[v][k][cell] = (v * K + k) * kRS + cell
+// The gather itself is issued transposed: thread t copies (cell t / 5,
+// variable t % 5), so the five variables of a stencil member are one
+// contiguous 40-byte read and a warp's request touches 2-3 cache lines instead
+// of 10 (lane = cell at a 40-byte stride); kVS = 35 spreads the five
+// variables of a cell over different banks for those writes.
+constexpr int kXS = 180, kVS = 35, kRS = 36;
+__host__ __device__ constexpr int kpad(int K) {
+  int p = K;
+  while (p % 16 != 4 && p % 16 != 12) ++p;
+  return p;
+}
+// union buffer of a DMMA kernel: the gather [G][kXS], later face values [Q][5][33] + dofs [5][K][kRS]
+__host__ __device__ constexpr size_t dm_union(int G, int Q, int K) {
+  return (static_cast<size_t>(G) * kXS > static_cast<size_t>(Q * V5 * 33 + V5 * K * kRS))
+             ? static_cast<size_t>(G) * kXS
+             : static_cast<size_t>(Q * V5 * 33 + V5 * K * kRS);
+}
+
 // evaluate the reconstruction of (cell, var) at its Q face points, stage the
 // values for the positivity check, and report the bounds failure (fallback_check)
 // KE: number of leading dofs evaluated (MUSCL's limited r = 1 polynomial: 3, the
@@ -347,8 +374,16 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // and phi block (group B) are bulk-copied into shared memory one chunk ahead,
 // each refilled as soon as the solve / the evaluation has consumed it
 // (split-phase, as the 2D k_central_tma)
+// resident blocks per SM asked of the per-cell-row (p <= 2) central kernels
+#ifndef UCFVB_C3_MINB
+#define UCFVB_C3_MINB 2
+#endif
+// TMA variant: bulk L2 prefetch of the next chunk's phi block (read through L1 by the evaluation)
+#ifndef UCFVB_C3_PFPHI
+#define UCFVB_C3_PFPHI 0
+#endif
 template <int K, int M, int NF, int NQ, bool STAGED, bool TMA = false>
-__global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
+__global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
   // staged path on a detecting stage: the candidate face values are stored
@@ -362,10 +397,9 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
   // STAGED: pinv row [M][K], phi row [Q][K] and the centre values [5][32] past the union buffer
-  constexpr size_t kUnion = (STAGED && K >= 8) ? ((smem3_bytes(G, Q) / 8 > static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
-                                                      ? smem3_bytes(G, Q) / 8
-                                                      : static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
-                                               : smem3_bytes(G, Q) / 8;
+  constexpr bool DM = STAGED && K >= 8;  // tensor-core path (strides: see kXS)
+  constexpr int KP = DM ? kpad(K) : K;
+  constexpr size_t kUnion = DM ? dm_union(G, Q, K) : smem3_bytes(G, Q) / 8;
   double* sp = smem3 + kUnion;
   // per-cell operator rows (p <= 2): the chunk's pinv block is copied to shared
   // memory with 16-byte cp.async at the chunk start (all in flight at once)
@@ -402,8 +436,8 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
   int it = 0;
   if (STAGED) {
     const int t = blockIdx.x % D.n_ops;
-    for (int e = threadIdx.x; e < M * K; e += 160) sp[e] = D.pinv[ao(t, e, M * K)];
-    for (int e = threadIdx.x; e < Q * K; e += 160) sp[M * K + e] = D.phi[ao(t, e, Q * K)];
+    for (int e = threadIdx.x; e < M * K; e += 160) sp[(e / K) * KP + e % K] = D.pinv[ao(t, e, M * K)];
+    for (int e = threadIdx.x; e < Q * K; e += 160) sp[M * KP + (e / K) * KP + e % K] = D.phi[ao(t, e, Q * K)];
     __syncthreads();
   }
   for (int ch = blockIdx.x; ch < nch; ch += gridDim.x, ++it) {
@@ -419,6 +453,8 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       bulk_prefetch_l2(D.pinv + static_cast<size_t>(nx) * M * K * 32, M * K * 32 * 8);
       bulk_prefetch_l2(D.central + static_cast<size_t>(nx) * (M + 1) * 32, (M + 1) * 32 * 4);
     }
+    if (TMA && UCFVB_C3_PFPHI && !kTmaPhi && threadIdx.x == 32 && nxt < nch)
+      bulk_prefetch_l2(D.phi + static_cast<size_t>(nxt) * Q * K * 32, Q * K * 32 * 8);
     const bool pcs = PCS && D.n_ops == D.n;
     if (pcs) {
       const double* src = D.pinv + static_cast<size_t>(ch) * M * K * 32;
@@ -426,7 +462,19 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
     }
     // every stencil and neighbour value of this (cell, variable) in flight at
     // once: G fire-and-forget 8-byte cp.async copies into shared memory
-    {
+    if constexpr (DM) {
+      // transposed: thread (cell gl, variable gv) -- one member's five variables are one 40-byte read
+      const int gl = threadIdx.x / V5, gv = threadIdx.x - gl * V5;
+      const int gc = min((ch << 5) + gl, D.n - 1);
+      int id[G];
+#pragma unroll
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
+#pragma unroll
+      for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(gc, i, NF)];
+#pragma unroll
+      for (int g = 0; g < G; ++g) cp_async8(&xs[g * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
+      cp_async_commit();
+    } else {
       int id[G];
 #pragma unroll
       for (int m = 0; m < M; ++m) id[m] = D.central[ao(cc, m + 1, M + 1)];
@@ -450,11 +498,13 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
     if (pcs) __syncthreads();  // the pinv block is copied by all threads
     if (TMA) mbar_wait(&bar[0], it & 1);
     double lo = u0, hi = u0;
+    if constexpr (!DM) {
 #pragma unroll
-    for (int i = 0; i < NF; ++i) {
-      const double x = xs[(M + i) * 160 + threadIdx.x];
-      lo = smin(lo, x);
-      hi = smax(hi, x);
+      for (int i = 0; i < NF; ++i) {
+        const double x = xs[(M + i) * 160 + threadIdx.x];
+        lo = smin(lo, x);
+        hi = smax(hi, x);
+      }
     }
     double a[K];
 #pragma unroll
@@ -464,9 +514,15 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       // (variable v) is the GEMM a(K x 32) = pinv(K x M) . dU(M x 32) on the
       // fp64 tensor cores, m in k-steps of 4 (the oracle's fma order)
       constexpr int MT = (K + 7) / 8, KS = (M + 3) / 4;
-      double* su0 = sp + M * K + Q * K;  // [5][32] centre values
+      double* su0 = sp + M * KP + Q * KP;  // [5][32] centre values
       su0[threadIdx.x] = u0;
-      __syncthreads();  // every thread's gather landed (fragments read other lanes' columns)
+      __syncthreads();  // every thread's gather landed (each value was copied by another thread)
+#pragma unroll
+      for (int i = 0; i < NF; ++i) {
+        const double x = xs[(M + i) * kXS + v * kVS + lane];
+        lo = smin(lo, x);
+        hi = smax(hi, x);
+      }
       double dacc[MT][4][2];
 #pragma unroll
       for (int i = 0; i < MT; ++i)
@@ -480,31 +536,31 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int k = 8 * i + fr;
-          af[i] = (k < K && m < M) ? sp[m * K + k] : 0.0;
+          af[i] = (k < K && m < M) ? sp[m * KP + k] : 0.0;
         }
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int cl = 8 * t + fr;
-          const double bf = m < M ? xs[m * 160 + v * 32 + cl] - su0[v * 32 + cl] : 0.0;
+          const double bf = m < M ? xs[m * kXS + v * kVS + cl] - su0[v * 32 + cl] : 0.0;
 #pragma unroll
           for (int i = 0; i < MT; ++i) dmma884(dacc[i][t][0], dacc[i][t][1], af[i], bf);
         }
       }
       __syncthreads();  // gather buffer consumed: it carries the dofs back to their lanes
-      double* sd = xs + Q * V5 * 33;  // [5][K][32], past the face-value buffer
+      double* sd = xs + Q * V5 * 33;  // [5][K][kRS], past the face-value buffer
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int k = 8 * i + fr;
           if (k < K) {
-            sd[(v * K + k) * 32 + 8 * t + 2 * fc] = dacc[i][t][0];
-            sd[(v * K + k) * 32 + 8 * t + 2 * fc + 1] = dacc[i][t][1];
+            sd[(v * K + k) * kRS + 8 * t + 2 * fc] = dacc[i][t][0];
+            sd[(v * K + k) * kRS + 8 * t + 2 * fc + 1] = dacc[i][t][1];
           }
         }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < K; ++k) a[k] = sd[(v * K + k) * 32 + lane];
+      for (int k = 0; k < K; ++k) a[k] = sd[(v * K + k) * kRS + lane];
     } else {
       double2 w = make_double2(0.0, 0.0);
 #pragma unroll
@@ -540,8 +596,8 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
         // the tensor cores, k in steps of 4 from C = u0 (evaluate_cell's fma order)
         constexpr int QT = (Q + 7) / 8, KS2 = (K + 3) / 4;
         const double* sd = xs + Q * V5 * 33;
-        const double* sph = sp + M * K;
-        const double* su0 = sp + M * K + Q * K;
+        const double* sph = sp + M * KP;
+        const double* su0 = sp + M * KP + Q * KP;
         const int fr = lane >> 2, fc = lane & 3;
         double f[QT][4][2];
 #pragma unroll
@@ -558,11 +614,11 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
 #pragma unroll
           for (int i = 0; i < QT; ++i) {
             const int q = 8 * i + fr;
-            af[i] = (q < Q && k < K) ? sph[q * K + k] : 0.0;
+            af[i] = (q < Q && k < K) ? sph[q * KP + k] : 0.0;
           }
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            const double bf = k < K ? sd[(v * K + k) * 32 + 8 * t + fr] : 0.0;
+            const double bf = k < K ? sd[(v * K + k) * kRS + 8 * t + fr] : 0.0;
 #pragma unroll
             for (int i = 0; i < QT; ++i) dmma884(f[i][t][0], f[i][t][1], af[i], bf);
           }
@@ -591,7 +647,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? 2 : 4) k3_central(Dev3 D
       if (kTmaPhi) mbar_wait(&bar[1], it & 1);
       if (eval)
         eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
-                              STAGED ? sp + M * K : nullptr, kTmaPhi ? sphc : nullptr);
+                              STAGED ? sp + M * KP : nullptr, kTmaPhi ? sphc : nullptr);
     }
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
@@ -724,19 +780,20 @@ template <int K, int M, int NF, int NQ, bool STAGED>
 __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
-  constexpr int EP = M * K, ED = NF * 3 * MD3, EO = (K * K + 1) & ~1;  // region sizes (even: phi is read as double2)
   // DM: lattice-class chunks (one operator row per block) run the central
-  // solve and the face evaluation on the fp64 tensor cores (see k3_central)
+  // solve and the face evaluation on the fp64 tensor cores (see k3_central; strides: kXS)
   constexpr bool DM = STAGED && K >= 8;
-  constexpr size_t kU0 = smem3_bytes(G, Q) / 8, kU1 = static_cast<size_t>(Q * V5 * 33 + V5 * K * 32);
-  constexpr size_t kUnion = (DM && kU1 > kU0) ? kU1 : kU0;
+  constexpr int KP = DM ? kpad(K) : K;  // row stride of the staged pinv / OI / phi rows
+  constexpr int EPG = M * K;            // pinv elements per operator row in global memory
+  constexpr int EP = M * KP, ED = NF * 3 * MD3, EO = (K * KP + 1) & ~1;  // region sizes (even: phi is read as double2)
+  constexpr size_t kUnion = DM ? dm_union(G, Q, K) : smem3_bytes(G, Q) / 8;
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
   double* sd = xs + Q * V5 * 33;  // DM: dofs [5][K][32] past the face values
   // STAGED: this block's lattice type's rows: pinv | pinv_dir | OI | phi | (DM: centre values [5][32]) | dir members
   double* sp = smem3 + kUnion;
-  double* su0 = sp + EP + ED + EO + Q * K;
+  double* su0 = sp + EP + ED + EO + Q * KP;
   int* sdm = reinterpret_cast<int*>(su0 + (DM ? 160 : 0));
   int* scell = sdm + NF * MD3;  // DM: the chunk's cells
   // forced CWENOZ on per-cell rows (p <= 2): the list is the identity, so each
@@ -750,10 +807,10 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
   const int cnt = W.counters[cnt_idx(W, kCwList, t)];
   const int32_t* list = list_of(W, kCwList, t);
   if (STAGED) {
-    for (int e = threadIdx.x; e < EP; e += 160) sp[e] = D.pinv[ao(t, e, EP)];
+    for (int e = threadIdx.x; e < EPG; e += 160) sp[(e / K) * KP + e % K] = D.pinv[ao(t, e, EPG)];
     for (int e = threadIdx.x; e < ED; e += 160) sp[EP + e] = D.pinv_dir[ao(t, e, ED)];
-    for (int e = threadIdx.x; e < K * K; e += 160) sp[EP + ED + e] = D.oi[ao(t, e, K * K)];
-    for (int e = threadIdx.x; e < Q * K; e += 160) sp[EP + ED + EO + e] = D.phi[ao(t, e, Q * K)];
+    for (int e = threadIdx.x; e < K * K; e += 160) sp[EP + ED + (e / K) * KP + e % K] = D.oi[ao(t, e, K * K)];
+    for (int e = threadIdx.x; e < Q * K; e += 160) sp[EP + ED + EO + (e / K) * KP + e % K] = D.phi[ao(t, e, Q * K)];
     for (int e = threadIdx.x; e < NF * MD3; e += 160) sdm[e] = D.dirm[ao(t, e, NF * MD3)];
     __syncthreads();
   }
@@ -770,7 +827,17 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
     // the M central-stencil values in flight at once (cp.async); the central
     // solve is recomputed here (bit-identical to k3_central's) instead of
     // storing K x 5 dofs for every cell
-    {
+    if constexpr (DM) {
+      // transposed: thread (cell gl, variable gv) -- one member's five variables are one 40-byte read
+      const int gl = threadIdx.x / V5, gv = threadIdx.x - gl * V5;
+      const int gc = list[base + gl < cnt ? base + gl : base];
+      int id[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
+#pragma unroll
+      for (int m = 0; m < M; ++m) cp_async8(&xs[m * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[m]) * V5 + gv]);
+      cp_async_commit();
+    } else {
       int id[M];
 #pragma unroll
       for (int m = 0; m < M; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
@@ -798,7 +865,7 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
         const double x = xs[m * 160 + threadIdx.x] - u0;
 #pragma unroll
         for (int k = 0; k < K; ++k)
-          p1[k] = __fma_rn(STAGED ? sp[m * K + k]
+          p1[k] = __fma_rn(STAGED ? sp[m * KP + k]
                                   : (pcs ? spc[(m * K + k) * 32 + lane] : D.pinv[ao(op, m * K + k, M * K)]),
                            x, p1[k]);
       }
@@ -813,7 +880,8 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       double x[MD3];
 #pragma unroll
       for (int m = 0; m < MD3; ++m)
-        x[m] = xs[((STAGED ? sdm[s * MD3 + m] : D.dirm[ao(op, s * MD3 + m, NF * MD3)]) - 1) * 160 + threadIdx.x] - u0;
+        x[m] = (DM ? xs[(sdm[s * MD3 + m] - 1) * kXS + v * kVS + lane]
+                   : xs[((STAGED ? sdm[s * MD3 + m] : D.dirm[ao(op, s * MD3 + m, NF * MD3)]) - 1) * 160 + threadIdx.x]) - u0;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
         double acc = 0.0;
@@ -840,12 +908,12 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int k = 8 * i + fr;
-          af[i] = (k < K && m < M) ? sp[m * K + k] : 0.0;
+          af[i] = (k < K && m < M) ? sp[m * KP + k] : 0.0;
         }
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
           const int cl = 8 * tt + fr;
-          const double bf = m < M ? xs[m * 160 + v * 32 + cl] - su0[v * 32 + cl] : 0.0;
+          const double bf = m < M ? xs[m * kXS + v * kVS + cl] - su0[v * 32 + cl] : 0.0;
 #pragma unroll
           for (int i = 0; i < MT; ++i) dmma884(dacc[i][tt][0], dacc[i][tt][1], af[i], bf);
         }
@@ -857,13 +925,13 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
         for (int tt = 0; tt < 4; ++tt) {
           const int k = 8 * i + fr;
           if (k < K) {
-            sd[(v * K + k) * 32 + 8 * tt + 2 * fc] = dacc[i][tt][0];
-            sd[(v * K + k) * 32 + 8 * tt + 2 * fc + 1] = dacc[i][tt][1];
+            sd[(v * K + k) * kRS + 8 * tt + 2 * fc] = dacc[i][tt][0];
+            sd[(v * K + k) * kRS + 8 * tt + 2 * fc + 1] = dacc[i][tt][1];
           }
         }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = sd[(v * K + k) * 32 + lane];
+      for (int k = 0; k < K; ++k) p1[k] = sd[(v * K + k) * kRS + lane];
       __syncwarp();
     }
 #pragma unroll
@@ -881,7 +949,7 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       // t(K x 32) = OI(K x K) . p1(K x 32) on the tensor cores (warp v's variable)
       constexpr int MT = (K + 7) / 8, KS3 = (K + 3) / 4;
 #pragma unroll
-      for (int k = 0; k < K; ++k) sd[(v * K + k) * 32 + lane] = p1[k];
+      for (int k = 0; k < K; ++k) sd[(v * K + k) * kRS + lane] = p1[k];
       __syncwarp();
       double tacc[MT][4][2];
 #pragma unroll
@@ -895,11 +963,11 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
           const int k = 8 * i + fr;
-          af[i] = (k < K && q < K) ? sp[EP + ED + k * K + q] : 0.0;
+          af[i] = (k < K && q < K) ? sp[EP + ED + k * KP + q] : 0.0;
         }
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
-          const double bf = q < K ? sd[(v * K + q) * 32 + 8 * tt + fr] : 0.0;
+          const double bf = q < K ? sd[(v * K + q) * kRS + 8 * tt + fr] : 0.0;
 #pragma unroll
           for (int i = 0; i < MT; ++i) dmma884(tacc[i][tt][0], tacc[i][tt][1], af[i], bf);
         }
@@ -911,27 +979,27 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
         for (int tt = 0; tt < 4; ++tt) {
           const int k = 8 * i + fr;
           if (k < K) {
-            sd[(v * K + k) * 32 + 8 * tt + 2 * fc] = tacc[i][tt][0];
-            sd[(v * K + k) * 32 + 8 * tt + 2 * fc + 1] = tacc[i][tt][1];
+            sd[(v * K + k) * kRS + 8 * tt + 2 * fc] = tacc[i][tt][0];
+            sd[(v * K + k) * kRS + 8 * tt + 2 * fc + 1] = tacc[i][tt][1];
           }
         }
       __syncwarp();
 #pragma unroll
-      for (int k = 0; k < K; ++k) si0 = __fma_rn(p1[k], sd[(v * K + k) * 32 + lane], si0);
+      for (int k = 0; k < K; ++k) si0 = __fma_rn(p1[k], sd[(v * K + k) * kRS + lane], si0);
       __syncwarp();
     } else {
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         double t = 0.0;
 #pragma unroll
-        for (int q = 0; q < K; ++q) t = __fma_rn(STAGED ? sp[EP + ED + k * K + q] : D.oi[ao(op, k * K + q, K * K)], p1[q], t);
+        for (int q = 0; q < K; ++q) t = __fma_rn(STAGED ? sp[EP + ED + k * KP + q] : D.oi[ao(op, k * K + q, K * K)], p1[q], t);
         si0 = __fma_rn(p1[k], t, si0);
       }
     }
     const double o00 = (STAGED ? sp[EP + ED + (0)] : D.oi[ao(op, 0, K * K)]), o01 = (STAGED ? sp[EP + ED + (1)] : D.oi[ao(op, 1, K * K)]), o02 = (STAGED ? sp[EP + ED + (2)] : D.oi[ao(op, 2, K * K)]);
-    const double o10 = (STAGED ? sp[EP + ED + (K)] : D.oi[ao(op, K, K * K)]), o11 = (STAGED ? sp[EP + ED + (K + 1)] : D.oi[ao(op, K + 1, K * K)]), o12 = (STAGED ? sp[EP + ED + (K + 2)] : D.oi[ao(op, K + 2, K * K)]);
-    const double o20 = (STAGED ? sp[EP + ED + (2 * K)] : D.oi[ao(op, 2 * K, K * K)]), o21 = (STAGED ? sp[EP + ED + (2 * K + 1)] : D.oi[ao(op, 2 * K + 1, K * K)]),
-                 o22 = (STAGED ? sp[EP + ED + (2 * K + 2)] : D.oi[ao(op, 2 * K + 2, K * K)]);
+    const double o10 = (STAGED ? sp[EP + ED + (KP)] : D.oi[ao(op, K, K * K)]), o11 = (STAGED ? sp[EP + ED + (KP + 1)] : D.oi[ao(op, K + 1, K * K)]), o12 = (STAGED ? sp[EP + ED + (KP + 2)] : D.oi[ao(op, K + 2, K * K)]);
+    const double o20 = (STAGED ? sp[EP + ED + (2 * KP)] : D.oi[ao(op, 2 * K, K * K)]), o21 = (STAGED ? sp[EP + ED + (2 * KP + 1)] : D.oi[ao(op, 2 * K + 1, K * K)]),
+                 o22 = (STAGED ? sp[EP + ED + (2 * KP + 2)] : D.oi[ao(op, 2 * K + 2, K * K)]);
     double si[NF];
     double tau = 0.0;
 #pragma unroll
@@ -978,7 +1046,7 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       // face values F(Q x 32) = u0 + phi(Q x K) . bl(K x 32) on the tensor cores
       constexpr int QT = (Q + 7) / 8, KS2 = (K + 3) / 4;
 #pragma unroll
-      for (int k = 0; k < K; ++k) sd[(v * K + k) * 32 + lane] = bl[k];
+      for (int k = 0; k < K; ++k) sd[(v * K + k) * kRS + lane] = bl[k];
       __syncwarp();
       const double* sph = sp + EP + ED + EO;
       double f[QT][4][2];
@@ -996,11 +1064,11 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
 #pragma unroll
         for (int i = 0; i < QT; ++i) {
           const int q = 8 * i + fr;
-          af[i] = (q < Q && k < K) ? sph[q * K + k] : 0.0;
+          af[i] = (q < Q && k < K) ? sph[q * KP + k] : 0.0;
         }
 #pragma unroll
         for (int tt = 0; tt < 4; ++tt) {
-          const double bf = k < K ? sd[(v * K + k) * 32 + 8 * tt + fr] : 0.0;
+          const double bf = k < K ? sd[(v * K + k) * kRS + 8 * tt + fr] : 0.0;
 #pragma unroll
           for (int i = 0; i < QT; ++i) dmma884(f[i][tt][0], f[i][tt][1], af[i], bf);
         }
@@ -1356,11 +1424,11 @@ Kern3 kern3() {
   k.smem_cwenoz = smem3_bytes(M, Q) + (K * M <= 200 ? 8 * static_cast<size_t>(M * K * 32) : 0);
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
-  k.smem_central_staged = std::max(smem3_bytes(M + NF, Q), 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32)) +
-                          8 * static_cast<size_t>(M * K + Q * K + 160);
-  k.smem_cwenoz_staged = (K >= 8 ? std::max(smem3_bytes(M, Q), 8 * static_cast<size_t>(Q * V5 * 33 + V5 * K * 32))
-                                  : smem3_bytes(M, Q)) +
-                         8 * static_cast<size_t>(M * K + NF * 3 * MD3 + ((K * K + 1) & ~1) + Q * K +
+  constexpr int KP = K >= 8 ? kpad(K) : K;
+  k.smem_central_staged = (K >= 8 ? 8 * dm_union(M + NF, Q, K) : smem3_bytes(M + NF, Q)) +
+                          8 * static_cast<size_t>(M * KP + Q * KP + 160);
+  k.smem_cwenoz_staged = (K >= 8 ? 8 * dm_union(M, Q, K) : smem3_bytes(M, Q)) +
+                         8 * static_cast<size_t>(M * KP + NF * 3 * MD3 + ((K * KP + 1) & ~1) + Q * KP +
                                                  (K >= 8 ? 160 : 0)) +
                          4 * static_cast<size_t>(NF * MD3 + 32);
   k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);

@@ -104,10 +104,7 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
 #ifndef UCFVB_CELLS_TILE
 #define UCFVB_CELLS_TILE 8
 #endif
-// L2 prefetch of the next tile's own state rows and central dofs (one tile ahead)
-#ifndef UCFVB_CELLS_PFD
-#define UCFVB_CELLS_PFD 0
-#endif
+
 // cells per tile; a block is 4 * kCellTile threads
 constexpr int kCellTile = UCFVB_CELLS_TILE;
 template <int K, int NQ, int NF, int MM, int MD>
@@ -175,23 +172,12 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool venkat = ph.limiter == 1;
   int it = 0;
-  int c_next = static_cast<int>(blockIdx.x) < nitems ? tile_cell(blockIdx.x, slot) : 0;
   for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
     const uint32_t par = it & 1;
     const int next = i + gridDim.x;
     const bool cw = i < tc;
     const bool mine = cw ? i * TC + slot < nc : (i - tc) * TC + slot < nm;
-    const int c = UCFVB_CELLS_PFD ? c_next : tile_cell(i, slot);
-    if (UCFVB_CELLS_PFD && next < nitems) {
-      // the next tile's cell: its own state row and (CWENOZ) central dofs are DRAM
-      // misses at the head of that tile's dependency chain -- pull them into L2 now
-      c_next = tile_cell(next, slot);
-      if (v == 0) prefetch_l2(U + c_next);
-      if (next < tc) {
-#pragma unroll
-        for (int k = v; k < K; k += 4) prefetch_l2(S.dofs + aos(c_next, k, K));
-      }
-    }
+    const int c = tile_cell(i, slot);
     const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
     double vals[Q];
     double lo = u0, hi = u0;

@@ -229,6 +229,13 @@ __host__ __device__ constexpr int kpad(int K) {
   while (p % 16 != 4 && p % 16 != 12) ++p;
   return p;
 }
+// lattice-class MUSCL: gather rows of kMS doubles (5 variables at kVS), then the face values
+constexpr int kMS = 5 * kVS;
+__host__ __device__ constexpr size_t muscl_union(int G, int Q) {
+  const size_t u = (static_cast<size_t>(G) * kMS > static_cast<size_t>(Q * V5 * 33)) ? static_cast<size_t>(G) * kMS
+                                                                                    : static_cast<size_t>(Q * V5 * 33);
+  return (u + 1) & ~static_cast<size_t>(1);  // the operator rows behind it are read as double2
+}
 // union buffer of a DMMA kernel: the gather [G][kXS], later face values [Q][5][33] + dofs [5][K][kRS]
 __host__ __device__ constexpr size_t dm_union(int G, int Q, int K) {
   return (static_cast<size_t>(G) * kXS > static_cast<size_t>(Q * V5 * 33 + V5 * K * kRS))
@@ -357,6 +364,33 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
   __syncthreads();
 }
 
+// The block stores a chunk's staged face values run by run: with side-major
+// face points the NQ points a cell owns on one face are NQ * 40 contiguous
+// bytes, so consecutive threads take consecutive doubles of a (cell, face) run
+// and a warp's store covers whole sectors (per-thread stores of one variable
+// hit one 8-byte piece of 32 different sectors).
+template <int NF, int NQ>
+__device__ __forceinline__ void coop_store_runs(const Dev3& D, const Work3& W, int cb, double (*sval)[V5][33]) {
+  constexpr int Q = NF * NQ, RL = NQ * V5, RPI = 160 / RL;  // run length (doubles), runs per pass
+  const int r_in = threadIdx.x / RL, j = threadIdx.x - r_in * RL;
+  const int q = j / V5, w = j - q * V5;
+  if (r_in >= RPI) return;
+#pragma unroll 4
+  for (int r0 = 0; r0 < 32 * NF; r0 += RPI) {
+    const int r = r0 + r_in;
+    const int l = r / NF, lf = r - l * NF;
+    if (r < 32 * NF && cb + l < D.n) {
+      const int sl = __ldg(&D.slot[ao(cb + l, lf * NQ + q, Q)]);
+      W.fp[static_cast<size_t>(sl) * V5 + w] = sval[lf * NQ + q][w][l];
+    }
+  }
+}
+
+// per-cell-row central kernel: store the candidates cooperatively (coop_store_runs)
+#ifndef UCFVB_C3_COOP
+#define UCFVB_C3_COOP 1
+#endif
+
 // ---- central: solve + evaluate + NAD + fallback pre-check -----------------------------
 // STAGED: lattice-class operators on a type-blocked mesh (every chunk one
 // type): the grid is a multiple of the type count, so block b only ever sees
@@ -367,6 +401,16 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 // TMA staging of the phi block as well (pinv + phi: 1 block/SM, config 4
 // central 3.85 ms/stage; pinv only: 3 blocks/SM, 3.51 ms; cp.async pinv at the
 // chunk start: 3.61 ms). UCFVB_TMA3_PHI=1 builds the pinv + phi variant.
+// UCFVB_C3_RING=1: the phi block streams through a ring of kRingSlots
+// shared-memory slots, one slot = the rows of QG = 4 face points (4 K 32
+// doubles), bulk-copied three pieces ahead: the five variable-warps read each
+// phi line from shared memory instead of five times through L1 (the L1 tag
+// stage was the busiest unit of this kernel), and the footprint stays at two
+// blocks per SM (whole-block staging, UCFVB_TMA3_PHI, leaves one).
+#ifndef UCFVB_C3_RING
+#define UCFVB_C3_RING 0
+#endif
+constexpr int kRingSlots = 3;
 #ifndef UCFVB_TMA3_PHI
 #define UCFVB_TMA3_PHI 0
 #endif
@@ -380,7 +424,7 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
 #endif
 // TMA variant: bulk L2 prefetch of the next chunk's phi block (read through L1 by the evaluation)
 #ifndef UCFVB_C3_PFPHI
-#define UCFVB_C3_PFPHI 0
+#define UCFVB_C3_PFPHI 1
 #endif
 template <int K, int M, int NF, int NQ, bool STAGED, bool TMA = false>
 __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
@@ -406,7 +450,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
   constexpr bool PCS = !STAGED && !TMA && K * M <= 200;
   double* spc = smem3 + kUnion;
   double* sphc = spc + M * K * 32;  // TMA: the chunk's phi block
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sphc + (UCFVB_TMA3_PHI ? Q * K * 32 : 0));  // TMA: [0] pinv, [1] phi
+  constexpr bool kRing = TMA && UCFVB_C3_RING && !UCFVB_TMA3_PHI && (Q % 4 == 0);
+  constexpr int kPiece = 4 * K * 32, kPieces = Q / 4;  // doubles per ring slot; pieces per chunk
+  // TMA: [0] pinv, [1] phi (whole block) or [1 .. kRingSlots] the ring's full barriers
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sphc + (UCFVB_TMA3_PHI ? Q * K * 32 : (kRing ? kRingSlots * kPiece : 0)));
   __shared__ int s_sev[2][32], s_bf[2][32], s_pos[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   if (blockIdx.x == 0 && threadIdx.x < 2 * W.ntl) W.counters[kCnt0 + threadIdx.x] = 0;  // list lengths of this stage
@@ -421,14 +468,27 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
     mbar_arrive_expect_tx(&bar[1], kPhiBytes);
     bulk_g2s(sphc, D.phi + static_cast<size_t>(ch) * Q * K * 32, kPhiBytes, &bar[1]);
   };
+  // ring piece gp of this block's chunk sequence: chunk blockIdx.x + (gp / kPieces) * gridDim.x, piece gp % kPieces
+  auto issue_piece = [&](int gp) {
+    const int chp = blockIdx.x + (gp / kPieces) * static_cast<int>(gridDim.x);
+    if (chp >= nch) return;
+    const int slot = gp % kRingSlots;
+    mbar_arrive_expect_tx(&bar[1 + slot], kPiece * 8);
+    bulk_g2s(sphc + slot * kPiece, D.phi + static_cast<size_t>(chp) * Q * K * 32 + static_cast<size_t>(gp % kPieces) * kPiece,
+             kPiece * 8, &bar[1 + slot]);
+  };
   if (TMA) {
     if (threadIdx.x == 0) {
       mbar_init(&bar[0], 1);
       mbar_init(&bar[1], 1);
+      if (kRing)
+        for (int i = 1; i < kRingSlots; ++i) mbar_init(&bar[1 + i], 1);
       mbar_fence_init();
       if (static_cast<int>(blockIdx.x) < nch) {
         issue_pinv(blockIdx.x);
         if (kTmaPhi) issue_phi(blockIdx.x);
+        if (kRing)
+          for (int i = 0; i < kRingSlots; ++i) issue_piece(i);
       }
     }
     __syncthreads();
@@ -453,7 +513,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
       bulk_prefetch_l2(D.pinv + static_cast<size_t>(nx) * M * K * 32, M * K * 32 * 8);
       bulk_prefetch_l2(D.central + static_cast<size_t>(nx) * (M + 1) * 32, (M + 1) * 32 * 4);
     }
-    if (TMA && UCFVB_C3_PFPHI && !kTmaPhi && threadIdx.x == 32 && nxt < nch)
+    if (TMA && UCFVB_C3_PFPHI && !kTmaPhi && !kRing && threadIdx.x == 32 && nxt < nch)
       bulk_prefetch_l2(D.phi + static_cast<size_t>(nxt) * Q * K * 32, Q * K * 32 * 8);
     const bool pcs = PCS && D.n_ops == D.n;
     if (pcs) {
@@ -645,9 +705,44 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
       }
     } else {
       if (kTmaPhi) mbar_wait(&bar[1], it & 1);
-      if (eval)
-        eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
-                              STAGED ? sp + M * KP : nullptr, kTmaPhi ? sphc : nullptr);
+      if constexpr (kRing) {
+        // phi by pieces of four face points through the ring (every chunk consumes its
+        // kPieces pieces whether or not it evaluates, so the ring's order is fixed)
+#pragma unroll
+        for (int g = 0; g < kPieces; ++g) {
+          const int gp = it * kPieces + g, slot = gp % kRingSlots;
+          mbar_wait(&bar[1 + slot], (gp / kRingSlots) & 1);
+          if (eval) {
+            const double* ph = sphc + slot * kPiece;
+            int gs[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) gs[j] = UCFVB_C3_COOP ? 0 : (sl ? sl[4 * g + j] : D.slot[ao(c, 4 * g + j, Q)]);
+            double val[4] = {u0, u0, u0, u0};
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+              for (int j = 0; j < 4; ++j) val[j] = __fma_rn(a[k], ph[(j * K + k) * 32 + lane], val[j]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if (!UCFVB_C3_COOP && act) W.fp[static_cast<size_t>(gs[j]) * V5 + v] = val[j];
+              sval[4 * g + j][v][lane] = val[j];
+              if (chk) viol = smax(viol, smax(lo - val[j], val[j] - hi));
+            }
+          }
+          __syncthreads();  // every warp is done with this slot: refill it three pieces ahead
+          if (threadIdx.x == 0) {
+            fence_proxy_async_smem();
+            issue_piece(gp + kRingSlots);
+          }
+        }
+      } else if (eval) {
+        if constexpr (TMA && UCFVB_C3_COOP)
+          eval_store<K, NQ, NF, K, false>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
+                                          nullptr, kTmaPhi ? sphc : nullptr);
+        else
+          eval_store<K, NQ, NF>(D, W, c, op, v, lane, act, u0, a, sval, chk, lo, hi, viol, sl,
+                                STAGED ? sp + M * KP : nullptr, kTmaPhi ? sphc : nullptr);
+      }
     }
     // per checked variable: deactivation, severity vote and bounds failure
     if (chk && eval) {
@@ -702,6 +797,9 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
 #pragma unroll
         for (int q = 0; q < Q; ++q) W.fp[static_cast<size_t>(sl[q]) * V5 + w] = sval[q][w][l];
       }
+    }
+    if constexpr (TMA && UCFVB_C3_COOP) {
+      if (eval) coop_store_runs<NF, NQ>(D, W, ch << 5, sval);
     }
     __syncthreads();
     if (kTmaPhi && threadIdx.x == 0 && nxt < nch) {  // phi consumed: the next chunk's
@@ -1110,7 +1208,10 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
   extern __shared__ __align__(16) double smem3[];
   double* xs = smem3;
   auto sval = reinterpret_cast<double (*)[V5][33]>(smem3);
-  double* sp = smem3 + smem3_bytes(G, Q) / 8;  // STAGED: pinv_lin [3][M] | phi [Q][K]
+  // STAGED (lattice classes): the gathers are issued transposed (thread = (cell t / 5, variable
+  // t % 5): a member's five variables are one 40-byte read) into rows of kMS doubles
+  constexpr int XS = STAGED ? kMS : 160, VS = STAGED ? kVS : 32;
+  double* sp = smem3 + (STAGED ? muscl_union(G, Q) : smem3_bytes(G, Q) / 8);  // STAGED: pinv_lin [3][M] | phi [Q][K]
   __shared__ int s_fail[32];
   const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
   const int t = STAGED ? blockIdx.x % W.ntl : 0;
@@ -1129,12 +1230,14 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     const double u0 = U[static_cast<size_t>(c) * V5 + v];
     // two gathers of H1 and H2 values (all of each in flight), so the gather
     // buffer fits inside the face-value buffer: twice the resident blocks
+    const int gl = STAGED ? threadIdx.x / V5 : lane, gv = STAGED ? threadIdx.x - gl * V5 : v;  // gather mapping
+    const int gc = STAGED ? list[base + gl < cnt ? base + gl : base] : c;
     {
       int id[H1];
 #pragma unroll
-      for (int m = 0; m < H1; ++m) id[m] = D.central[ao(c, m + 1, M + 1)];
+      for (int m = 0; m < H1; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
 #pragma unroll
-      for (int g = 0; g < H1; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      for (int g = 0; g < H1; ++g) cp_async8(&xs[g * XS + gv * VS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
       cp_async_commit();
     }
     // face-point slots, loaded while the gather is in flight (p <= 2; for p = 3
@@ -1146,20 +1249,22 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       for (int q = 0; q < (kHoist ? NF * NQ : 0); ++q) slh[q] = D.slot[ao(c, q, NF * NQ)];
     }
     const int* sl = kHoist ? slh : nullptr;
+    // the second half's ids, in flight during the first wait
+    int id2[H2];
+#pragma unroll
+    for (int m = H1; m < M; ++m) id2[m - H1] = D.central[ao(gc, m + 1, M + 1)];
+#pragma unroll
+    for (int i = 0; i < NF; ++i) id2[M - H1 + i] = D.nbr[ao(gc, i, NF)];
     cp_async_wait_all();
+    if (STAGED) __syncthreads();  // each value was copied by another thread
     double l0 = 0.0, l1 = 0.0, l2 = 0.0;
     double xv[H1];  // first half consumed into registers before the buffer is reused
 #pragma unroll
-    for (int m = 0; m < H1; ++m) xv[m] = xs[m * 160 + threadIdx.x];
+    for (int m = 0; m < H1; ++m) xv[m] = xs[m * XS + v * VS + lane];
+    if (STAGED) __syncthreads(); else __syncwarp();
     {
-      int id[H2];
 #pragma unroll
-      for (int m = H1; m < M; ++m) id[m - H1] = D.central[ao(c, m + 1, M + 1)];
-#pragma unroll
-      for (int i = 0; i < NF; ++i) id[M - H1 + i] = D.nbr[ao(c, i, NF)];
-      __syncwarp();
-#pragma unroll
-      for (int g = 0; g < H2; ++g) cp_async8(&xs[g * 160 + threadIdx.x], &U[static_cast<size_t>(id[g]) * V5 + v]);
+      for (int g = 0; g < H2; ++g) cp_async8(&xs[g * XS + gv * VS + gl], &U[static_cast<size_t>(id2[g]) * V5 + gv]);
       cp_async_commit();
     }
 #pragma unroll
@@ -1170,9 +1275,10 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
       l2 = __fma_rn((STAGED ? sp[2 * M + m] : D.pinv_lin[ao(op, 2 * M + m, 3 * M)]), x, l2);
     }
     cp_async_wait_all();
+    if (STAGED) __syncthreads();
 #pragma unroll
     for (int m = H1; m < M; ++m) {
-      const double x = xs[(m - H1) * 160 + threadIdx.x] - u0;
+      const double x = xs[(m - H1) * XS + v * VS + lane] - u0;
       l0 = __fma_rn((STAGED ? sp[0 * M + m] : D.pinv_lin[ao(op, 0 * M + m, 3 * M)]), x, l0);
       l1 = __fma_rn((STAGED ? sp[1 * M + m] : D.pinv_lin[ao(op, 1 * M + m, 3 * M)]), x, l1);
       l2 = __fma_rn((STAGED ? sp[2 * M + m] : D.pinv_lin[ao(op, 2 * M + m, 3 * M)]), x, l2);
@@ -1180,7 +1286,7 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     double lo = u0, hi = u0;
 #pragma unroll
     for (int i = 0; i < NF; ++i) {
-      const double x = xs[(M - H1 + i) * 160 + threadIdx.x];
+      const double x = xs[(M - H1 + i) * XS + v * VS + lane];
       lo = smin(lo, x);
       hi = smax(hi, x);
     }
@@ -1431,11 +1537,14 @@ Kern3 kern3() {
                          8 * static_cast<size_t>(M * KP + NF * 3 * MD3 + ((K * KP + 1) & ~1) + Q * KP +
                                                  (K >= 8 ? 160 : 0)) +
                          4 * static_cast<size_t>(NF * MD3 + 32);
-  k.smem_muscl_staged = k.smem_muscl + 8 * static_cast<size_t>(3 * M + Q * K);
+  k.smem_muscl_staged = 8 * muscl_union(M - M / 2 + NF, Q) + 8 * static_cast<size_t>(3 * M + Q * K);
   k.central = k3_central<K, M, NF, NQ, false>;
   if constexpr (K * M <= 200) {
     k.central_tma = k3_central<K, M, NF, NQ, false, true>;
-    k.smem_central_tma = smem3_bytes(M + NF, Q) + 8 * static_cast<size_t>(M * K * 32 + (UCFVB_TMA3_PHI ? Q * K * 32 : 0)) + 16;
+    k.smem_central_tma = smem3_bytes(M + NF, Q) +
+                         8 * static_cast<size_t>(M * K * 32 + (UCFVB_TMA3_PHI ? Q * K * 32
+                                                                               : (UCFVB_C3_RING && Q % 4 == 0 ? kRingSlots * 4 * K * 32 : 0))) +
+                         8 * (1 + kRingSlots);
   }
   k.central_staged = k3_central<K, M, NF, NQ, true>;
   k.spread = k3_spread<NF, NQ>;

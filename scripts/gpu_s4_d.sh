@@ -1,0 +1,14 @@
+# session-4: staged MUSCL transposed gather (new vs base) on config 5; config-4 central coop stores
+cd "$GRAFT_REPO_ROOT"
+timeout 900 python -m pytest tests/test_gpu_3d.py -m gpu -q -x 2>&1 | tail -3
+for v in base new base new; do
+  echo -n "$v "; UCFVB_LIB=scratch/ab/$v.so timeout 600 python scripts/prof3d.py --config 5 --warmup 2 --steps 3 2>&1 | tail -1 | cut -c1-220
+done
+for r in 1 2; do
+for v in new c3coop; do
+  echo -n "$v "; UCFVB_LIB=scratch/ab/$v.so timeout 600 python scripts/prof3d.py --config 4 --warmup 2 --steps 3 2>&1 | tail -1 | cut -c1-220
+done
+done
+for v in new c3coop; do
+  echo -n "$v "; UCFVB_LIB=scratch/ab/$v.so timeout 600 python scripts/prof3d.py --config 4c --warmup 2 --steps 3 2>&1 | tail -1 | cut -c1-220
+done

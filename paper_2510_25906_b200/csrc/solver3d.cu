@@ -158,6 +158,7 @@ struct Dev3 {
 
 struct Phys3 {
   double gamma, cfl, lambda1p, weno_eps, weno_b, lam0, lams;
+  double inv_lam0;  // RN(1 / lam0) for div_rn (exact_math.h)
   MarginParams mg;
   int mode, limiter, hll;
 };
@@ -310,17 +311,21 @@ __device__ __forceinline__ void eval_store(const Dev3& D, const Work3& W, int c,
 // contiguous 40-byte record instead of scattered 8-byte stores per variable):
 // config 5 weights 26.4 -> 22.8 ms/stage; per-cell-row kernels (config 4c)
 // keep the per-thread stores (cooperative measured 4.76 vs 4.65 ms).
+// scell: (COOP) the cell this thread stores for, thread t <-> (list entry t / 5,
+// variable t % 5), or -1: its face-point slots are requested on entry, so their
+// latency is covered by the bounds / positivity votes (L1 prefetch; loaded cold group by group
+// between the stores they were 25 % of the lattice-class CWENOZ kernel's stall samples)
 template <int NF, int NQ, bool COOP>
 __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P, const Work3& W, int c, int v,
                                                   int lane, bool act, double u0, bool chk, double blo, double bhi,
-                                                  double viol, double (*sval)[V5][33], int* s_fail) {
+                                                  double viol, double (*sval)[V5][33], int* s_fail, int scell = -1) {
   constexpr int Q = NF * NQ;
-  __shared__ int s_cell[32];
   __shared__ double s_u0[V5][32];
-  if (v == 0) {
-    s_fail[lane] = 0;
-    if (COOP) s_cell[lane] = act ? c : -1;
+  if (COOP && scell >= 0) {  // the five threads of a cell touch its Q slot lines between them (no registers held)
+#pragma unroll
+    for (int q = threadIdx.x % V5; q < Q; q += V5) prefetch_l1(&D.slot[ao(scell, q, Q)]);
   }
+  if (v == 0) s_fail[lane] = 0;
   if (COOP) s_u0[v][lane] = u0;
   __syncthreads();
   if (P.mode == UCFVB_HYBRID) {
@@ -341,15 +346,14 @@ __device__ __forceinline__ void troubled_fallback(const Dev3& D, const Phys3& P,
   if constexpr (COOP) {
     if (act && v == 0 && s_fail[lane]) W.labels[c] = UCFVB_SCHEME_FIRST;
     const int l = threadIdx.x / V5, w = threadIdx.x - l * V5;  // thread (cell l, variable w)
-    const int cell = s_cell[l];
-    if (cell >= 0) {
+    if (scell >= 0) {
       const bool fail = s_fail[l] != 0;
-      constexpr int G = 4;  // slot loads a group at a time (register pressure of the CWENOZ kernel)
+      constexpr int G = 4;  // slot loads (L1 hits after the prefetch) a group at a time: register pressure
 #pragma unroll 1
       for (int q0 = 0; q0 < Q; q0 += G) {
         int sl[G];
 #pragma unroll
-        for (int j = 0; j < G; ++j) sl[j] = q0 + j < Q ? D.slot[ao(cell, q0 + j, Q)] : 0;
+        for (int j = 0; j < G; ++j) sl[j] = q0 + j < Q ? __ldg(&D.slot[ao(scell, q0 + j, Q)]) : 0;
 #pragma unroll
         for (int j = 0; j < G; ++j)
           if (q0 + j < Q) W.fp[static_cast<size_t>(sl[j]) * V5 + w] = fail ? s_u0[w][l] : sval[q0 + j][w][l];
@@ -408,7 +412,7 @@ __device__ __forceinline__ void coop_store_runs(const Dev3& D, const Work3& W, i
 // stage was the busiest unit of this kernel), and the footprint stays at two
 // blocks per SM (whole-block staging, UCFVB_TMA3_PHI, leaves one).
 #ifndef UCFVB_C3_RING
-#define UCFVB_C3_RING 0
+#define UCFVB_C3_RING 1
 #endif
 constexpr int kRingSlots = 3;
 #ifndef UCFVB_TMA3_PHI
@@ -1038,8 +1042,11 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       p1[1] -= P.lams * dir[s][1];
       p1[2] -= P.lams * dir[s][2];
     }
+    // x / lam0 and x / wsum as div_rn (correctly rounded from the rounded reciprocal,
+    // exact_math.h: the same bits as the IEEE division, a fifth of its instructions)
+    const bool rl = P.lam0 >= 0x1p-60;
 #pragma unroll
-    for (int k = 0; k < K; ++k) p1[k] /= P.lam0;
+    for (int k = 0; k < K; ++k) p1[k] = rl ? div_rn(p1[k], P.lam0, P.inv_lam0) : p1[k] / P.lam0;
     // SI_0 = p1' OI p1 (row then dot) and the directional SI from the 3x3 block
     // SI_0 = p1' OI p1: t_k = sum_q OI_kq p1_q, si0 = sum_k p1_k t_k, fused, in the oracle's order
     double si0 = 0.0;
@@ -1122,9 +1129,11 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       om[s] = P.lams * (1.0 + tau / (P.weno_eps + si[s]));
       wsum += om[s];
     }
-    om0 /= wsum;
+    const double rw = 1.0 / wsum;  // wsum >= lam0 > 0
+    const bool rwok = rl && wsum <= 0x1p60;
+    om0 = rwok ? div_rn(om0, wsum, rw) : om0 / wsum;
 #pragma unroll
-    for (int s = 0; s < NF; ++s) om[s] /= wsum;
+    for (int s = 0; s < NF; ++s) om[s] = rwok ? div_rn(om[s], wsum, rw) : om[s] / wsum;
     double* bl = p1;  // blended in place (same operations; saves K registers)
 #pragma unroll
     for (int k = 0; k < K; ++k) bl[k] = om0 * p1[k];
@@ -1195,7 +1204,9 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
       eval_store<K, NQ, NF, K, !STAGED>(D, W, c, op, v, lane, act, u0, bl, sval, chk, blo, bhi, viol, sl,
                                              STAGED ? sp + EP + ED + EO : nullptr);
     }
-    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+    const int sl_l = threadIdx.x / V5;  // cooperative stores: thread <-> (list entry sl_l, variable)
+    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail,
+                                      (STAGED && base + sl_l < cnt) ? list[base + sl_l] : -1);
   }
 }
 
@@ -1314,7 +1325,9 @@ __global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const 
     }
     eval_store<K, NQ, NF, 3, !STAGED>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
                                            STAGED ? sp + 3 * M : nullptr);
-    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail);
+    const int sl_l = threadIdx.x / V5;  // cooperative stores: thread <-> (list entry sl_l, variable)
+    troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail,
+                                      (STAGED && base + sl_l < cnt) ? list[base + sl_l] : -1);
   }
 }
 
@@ -1401,6 +1414,56 @@ __global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3
   for (int v = 0; v < V5; ++v) W.ff[static_cast<size_t>(f) * V5 + v] = skip ? 0.0 : tot[v];
 }
 
+// Point counts that are not a power of two (6-point triangle faces): 32 / NQ
+// faces per warp, lane = (face, point), the warp's last 32 % NQ lanes idle
+// (2 of 32 for NQ = 6). A warp reads its faces' points as one contiguous run
+// of side-major rows, every lane carries one Riemann problem (a sixth of the
+// registers and latency chain of the thread-per-face form), and the face's
+// lanes sum the weighted fluxes in q order through shuffles.
+#ifndef UCFVB_FLUX3_PACK
+#define UCFVB_FLUX3_PACK 1
+#endif
+template <int NQ>
+__global__ void __launch_bounds__(128) k3_face_flux_pack(Dev3 D, Phys3 P, Work3 W) {
+  constexpr int FPW = 32 / NQ;  // faces per warp
+  if (halted(W)) return;        // block-uniform
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int fl0 = lane / NQ;
+  const bool lane_on = fl0 < FPW;
+  const int fl = lane_on ? fl0 : FPW - 1, q0 = lane_on ? lane - fl0 * NQ : 0;
+  const int64_t f0 = warp * FPW + fl;
+  const bool in = lane_on && f0 < D.nF;
+  const int f = f0 < D.nF ? static_cast<int>(f0) : D.nF - 1;
+  const int q = q0;
+  const bool skip = D.fown && D.fown[f] == 2;  // subdomain boundary face of a halo cell
+  double t[V5];
+  bool ok = true;
+  {
+    const double* UL = &W.fp[(static_cast<size_t>(f) * 2 * NQ + q) * V5];  // [face][side][q][5]
+    double ul[5], ur[5], n[3], fl5[5];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) ul[v] = UL[v], ur[v] = UL[NQ * V5 + v];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) n[d] = D.fnrm[(static_cast<size_t>(f) * NQ + q) * 3 + d];
+    ok = skip || riemann3(P.hll, ul, ur, n, P.gamma, fl5);
+    const double w = D.fwa[static_cast<size_t>(f) * NQ + q];
+#pragma unroll
+    for (int v = 0; v < V5; ++v) t[v] = w * fl5[v];
+  }
+  const int base = fl * NQ;
+  double tot[V5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int j = 0; j < NQ; ++j)
+#pragma unroll
+    for (int v = 0; v < V5; ++v) tot[v] += __shfl_sync(0xffffffffu, t[v], base + j);
+  const bool fail = ((__ballot_sync(0xffffffffu, !ok && in) >> base) & ((1u << NQ) - 1u)) != 0;
+  if (!in || q0 != 0) return;
+  if (fail && (!D.fown || D.fown[f] == 1)) atomicMin(&W.counters[kBadFace], f);
+#pragma unroll
+  for (int v = 0; v < V5; ++v) W.ff[static_cast<size_t>(f) * V5 + v] = skip ? 0.0 : tot[v];
+}
+
 // ---- gather + RK combination (solver.cpp:296-311, time_integrator.cpp:31-38) --------------
 // out = wa*ua + wb*ub + (wr*dt)*res, res = -acc*(1/vol); store_res keeps res (compute_residual tap / RK54)
 // cells: nullable list of the cells to update (n_cells of them); else cells [0, D.n)
@@ -1453,10 +1516,26 @@ __global__ void k3_rk54_final(Work3 W, int64_t N, double* u, const double* ub, c
 }
 
 // SSP-RK3 final stage result (written out of place) -> U, owned cells, when no failure was recorded
-__global__ void k3_commit(Work3 W, int64_t N, double* __restrict__ u, const double* __restrict__ src) {
-  if (failed_before(W)) return;  // block-uniform
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < N) u[i] = src[i];
+// (one failure check per block, 16-byte copies, four per thread: the one-double-per-thread
+// form with three volatile counter loads in every thread ran at 0.6 TB/s)
+__global__ void __launch_bounds__(256) k3_commit(Work3 W, int64_t N, double* __restrict__ u,
+                                                 const double* __restrict__ src) {
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = failed_before(W) ? 1 : 0;
+  __syncthreads();
+  if (s_fail) return;
+  const int64_t n2 = N >> 1;  // both arrays are cudaMalloc-aligned
+  const double2* s2 = reinterpret_cast<const double2*>(src);
+  double2* u2 = reinterpret_cast<double2*>(u);
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * 1024 + threadIdx.x;
+  double2 x[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (b + j * 256 < n2) x[j] = s2[b + j * 256];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (b + j * 256 < n2) u2[b + j * 256] = x[j];
+  if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) u[N - 1] = src[N - 1];
 }
 
 // ---- max_stable_dt (solver.cpp:103-111) ----------------------------------------------------
@@ -1478,8 +1557,16 @@ __global__ void __launch_bounds__(256) k3_dt(Dev3 D, Phys3 P, Work3 W, const dou
     }
     if (!ok) atomicMin(&W.counters[kBadCell], c);
   }
+  // one atomic per block (min is order-free; per warp it was 393 k same-address atomics on config 5)
   for (int o = 16; o; o >>= 1) dt = smin(dt, __shfl_xor_sync(0xffffffffu, dt, o));
-  if ((threadIdx.x & 31) == 0) atomicMin(W.dtmin, static_cast<unsigned long long>(__double_as_longlong(dt)));
+  __shared__ double s_dt[8];
+  if ((threadIdx.x & 31) == 0) s_dt[threadIdx.x >> 5] = dt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 1; i < 8; ++i) dt = smin(dt, s_dt[i]);
+    atomicMin(W.dtmin, static_cast<unsigned long long>(__double_as_longlong(dt)));
+  }
 }
 
 // halo exchange: owned values a peer holds as halo, packed in its order
@@ -1558,6 +1645,9 @@ Kern3 kern3() {
   if constexpr ((NQ & (NQ - 1)) == 0) {
     k.flux = k3_face_flux_lanes<NQ>;
     k.flux_lanes = NQ;
+  } else if (UCFVB_FLUX3_PACK && NQ <= 16) {
+    k.flux = k3_face_flux_pack<NQ>;
+    k.flux_lanes = -(32 / NQ);  // negative: faces per warp
   } else {
     k.flux = k3_face_flux<NQ>;
     k.flux_lanes = 1;
@@ -1715,7 +1805,12 @@ struct GpuSolver3::Impl {
     }
     mark(3);
     if (first) CK3(cudaMemcpyAsync(step_labels, W.labels, n, cudaMemcpyDeviceToDevice, st));
-    kern.flux<<<static_cast<unsigned>((static_cast<int64_t>(nF) * kern.flux_lanes + 127) / 128), 128, 0, st>>>(D, P, W);
+    {
+      // threads: one per face, flux_lanes per face, or (flux_lanes < 0) a warp per -flux_lanes faces
+      const int64_t thr = kern.flux_lanes > 0 ? static_cast<int64_t>(nF) * kern.flux_lanes
+                                              : (static_cast<int64_t>(nF) + (-kern.flux_lanes) - 1) / (-kern.flux_lanes) * 32;
+      kern.flux<<<static_cast<unsigned>((thr + 127) / 128), 128, 0, st>>>(D, P, W);
+    }
     mark(4);
     if (sent_cells) {
       // subdomain: owned cells only, the cells peers hold first; with NCCL the
@@ -1758,7 +1853,7 @@ struct GpuSolver3::Impl {
       launch_stage(ua, false, ub, U, ua, 0.75, 0.25, 0.25, nullptr, 1);
       launch_stage(ub, false, uc, U, ub, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, nullptr, 1, false);
       allreduce_errors();
-      k3_commit<<<static_cast<unsigned>((NO + 255) / 256), 256, 0, st>>>(W, NO, U, uc);
+      k3_commit<<<static_cast<unsigned>((NO / 2 + 1023) / 1024 + 1), 256, 0, st>>>(W, NO, U, uc);
       ++launches;
       exchange(U);
       return;
@@ -1961,6 +2056,7 @@ GpuSolver3::GpuSolver3(const ucfvb3_mesh_view& m, const ucfvb3_stencil_view& s, 
     P.gamma = o.gamma, P.cfl = o.cfl, P.lambda1p = o.lambda1p, P.weno_eps = o.weno_eps, P.weno_b = o.weno_b;
     P.lam0 = 1.0 - 1.0 / o.lambda1p;            // reconstruct.cpp:113
     P.lams = (1.0 - P.lam0) / (I.NF + 1 - 1);   // reconstruct.cpp:114
+    P.inv_lam0 = 1.0 / P.lam0;
     P.mg = MarginParams{o.margins.alpha_m, o.margins.beta_m, o.margins.alpha_w, o.margins.beta_w, o.margins.kappa,
                         o.margins.deact_n};
     P.mode = o.mode, P.limiter = o.limiter, P.hll = o.riemann == UCFVB_HLL ? 1 : 0;

@@ -55,6 +55,10 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 __device__ __forceinline__ void prefetch_l2(const void* src) {
   asm volatile("prefetch.global.L2 [%0];\n" ::"l"(src) : "memory");
 }
+// prefetch one global line into L1 (no registers held, no completion)
+__device__ __forceinline__ void prefetch_l1(const void* src) {
+  asm volatile("prefetch.global.L1 [%0];\n" ::"l"(src) : "memory");
+}
 // 16-byte asynchronous global -> shared copy (L2 only)
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");

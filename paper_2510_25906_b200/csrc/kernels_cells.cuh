@@ -11,13 +11,17 @@
 //
 // Records (built once on the device from the AoSoA arrays by k_pack_records;
 // the arithmetic reads the same operator bytes in the same order):
-//   CWENOZ  A: pinv_dir [s][m][k<2] (f64), directional member ids [s][m] (i32)
-//           B: OI [k][q], phi [lq][k] (f64), face neighbours [j], face-point slots [lq] (i32)
-//   MUSCL   A: pinv_linear [m][k<2] (f64), central member ids [m] (i32)
-//           B: phi01 [lq][k<2] (f64), face neighbours [j], face-point slots [lq] (i32)
-// Group A feeds the directional / r=1 solves and is refilled with the next
-// tile as soon as they are done; group B feeds the blend / limiter,
-// evaluation, fallback and scatter (split-phase, as k_troubled_split).
+//   CWENOZ  A:  pinv_dir [s][m][k<2] (f64), directional member ids [s][m], face neighbours [j] (i32)
+//           B1: OI [k][q] (f64)
+//           B2: phi [lq][k] (f64), face-point slots [lq] (i32)
+//   MUSCL   A:  pinv_linear [m][k<2] (f64), central member ids [m], face neighbours [j] (i32)
+//           B2: phi01 [lq][k<2] (f64), face-point slots [lq] (i32)
+// Split-phase refill, one shared-memory slot per group and an mbarrier each:
+// group A (directional / r=1 solves, fallback bounds) is refilled with the
+// next tile as soon as the solves are done, B1 as soon as the smoothness
+// indicators are, B2 after the evaluation -- every group is requested most of
+// a tile before it is read (measured neutral on config 3 against B1 + B2
+// requested together at the tile's end: profiles/round2.md).
 #pragma once
 
 #include "kernels_tma.cuh"
@@ -32,17 +36,18 @@ __host__ __device__ constexpr uint32_t odd16(uint32_t x) { return ((x >> 4) & 1u
 template <int K, int NQ, int NF, int MM, int MD, int TC = 32>
 struct CellRec {
   static constexpr int Q = NF * NQ;
-  static constexpr uint32_t CA_PD = 0, CA_ID = NF * MD * 2 * 8;
-  static constexpr uint32_t CA = round16(CA_ID + NF * MD * 4);
-  static constexpr uint32_t CB_OI = 0, CB_PHI = K * K * 8, CB_NBR = CB_PHI + Q * K * 8, CB_DST = CB_NBR + NF * 4;
-  static constexpr uint32_t CB = round16(CB_DST + Q * 4);
-  static constexpr uint32_t MA_PL = 0, MA_ID = MM * 2 * 8;
-  static constexpr uint32_t MA = round16(MA_ID + MM * 4);
-  static constexpr uint32_t MB_PHI = 0, MB_NBR = Q * 2 * 8, MB_DST = MB_NBR + NF * 4;
+  static constexpr uint32_t CA_PD = 0, CA_ID = NF * MD * 2 * 8, CA_NBR = CA_ID + NF * MD * 4;
+  static constexpr uint32_t CA = round16(CA_NBR + NF * 4);
+  static constexpr uint32_t CB_OI = 0, CB1 = round16(K * K * 8);  // B1 = [0, CB1)
+  static constexpr uint32_t CB_PHI = CB1, CB_DST = CB_PHI + Q * K * 8;
+  static constexpr uint32_t CB = round16(CB_DST + Q * 4);         // B2 = [CB1, CB)
+  static constexpr uint32_t MA_PL = 0, MA_ID = MM * 2 * 8, MA_NBR = MA_ID + MM * 4;
+  static constexpr uint32_t MA = round16(MA_NBR + NF * 4);
+  static constexpr uint32_t MB_PHI = 0, MB_DST = Q * 2 * 8;
   static constexpr uint32_t MB = round16(MB_DST + Q * 4);
-  // in HBM a cell's CWENOZ groups A | B share one record, and so do its MUSCL
+  // in HBM a cell's CWENOZ groups A | B1 | B2 share one record, and so do its MUSCL
   // groups, each record a whole number of 64-byte lines (the L2's DRAM fetch
-  // granularity): p = 3 CWENOZ 240 + 1120 -> 22 lines, MUSCL 368 + 144 = 8
+  // granularity): p = 3 CWENOZ 256 + 1120 -> 22 lines, MUSCL 384 + 128 = 8
   // lines exactly; unaligned separate records touched ~1.5 more lines per cell
   static constexpr uint32_t GC = (CA + CB + 63u) & ~63u, GM = (MA + MB + 63u) & ~63u;
   static constexpr uint32_t SCA = odd16(CA), SCB = odd16(CB), SMA = odd16(MA), SMB = odd16(MB);
@@ -63,16 +68,15 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
     int* id = reinterpret_cast<int*>(rc + static_cast<size_t>(c) * R::GC + R::CA_ID);
     for (int e = 0; e < NF * MD * 2; ++e) pd[e] = L.pinv_dir[aos(c, e, NF * MD * 2)];
     for (int e = 0; e < NF * MD; ++e) id[e] = L.dir_idx[aos(c, e, NF * MD)];
+    for (int e = 0; e < NF; ++e) id[NF * MD + e] = L.nbr[aos(c, e, NF)];
   }
   {
     unsigned char* r = rc + static_cast<size_t>(c) * R::GC + R::CA;
     double* oi = reinterpret_cast<double*>(r + R::CB_OI);
     double* ph = reinterpret_cast<double*>(r + R::CB_PHI);
-    int* nb = reinterpret_cast<int*>(r + R::CB_NBR);
     int* ds = reinterpret_cast<int*>(r + R::CB_DST);
     for (int e = 0; e < K * K; ++e) oi[e] = L.oi[aos(c, e, K * K)];
     for (int e = 0; e < Q * K; ++e) ph[e] = L.phi[aos(c, e, Q * K)];
-    for (int e = 0; e < NF; ++e) nb[e] = L.nbr[aos(c, e, NF)];
     for (int e = 0; e < Q; ++e) ds[e] = L.dest[aos(c, e, Q)];
   }
   {
@@ -80,14 +84,13 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
     int* id = reinterpret_cast<int*>(rm + static_cast<size_t>(c) * R::GM + R::MA_ID);
     for (int e = 0; e < MM * 2; ++e) pl[e] = L.pinv_lin[aos(c, e, MM * 2)];
     for (int e = 0; e < MM; ++e) id[e] = L.st_idx[aos(c, e, MM)];
+    for (int e = 0; e < NF; ++e) id[MM + e] = L.nbr[aos(c, e, NF)];
   }
   {
     unsigned char* r = rm + static_cast<size_t>(c) * R::GM + R::MA;
     double* p01 = reinterpret_cast<double*>(r + R::MB_PHI);
-    int* nb = reinterpret_cast<int*>(r + R::MB_NBR);
     int* ds = reinterpret_cast<int*>(r + R::MB_DST);
     for (int e = 0; e < Q * 2; ++e) p01[e] = L.phi01[aos(c, e, Q * 2)];
-    for (int e = 0; e < NF; ++e) nb[e] = L.nbr[aos(c, e, NF)];
     for (int e = 0; e < Q; ++e) ds[e] = L.dest[aos(c, e, Q)];
   }
 }
@@ -104,6 +107,14 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
 #ifndef UCFVB_CELLS_TILE
 #define UCFVB_CELLS_TILE 8
 #endif
+// 1: group B1 (OI rows) refilled as soon as the smoothness indicators are done
+// (0: together with B2 at the tile's end, the two-group schedule)
+#ifndef UCFVB_CELLS_B3
+#define UCFVB_CELLS_B3 1
+#endif
+#ifndef UCFVB_CELLS_CN
+#define UCFVB_CELLS_CN 1
+#endif
 
 // cells per tile; a block is 4 * kCellTile threads
 constexpr int kCellTile = UCFVB_CELLS_TILE;
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
   using R = CellRec<K, NQ, NF, MM, MD, TC>;
   constexpr int Q = R::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B1 (CWENOZ), [2] group B2
   unsigned char* const ga = smem;
   unsigned char* const gb = smem + R::TILE_A;
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
@@ -129,6 +140,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     s_nm = S.counts[1];
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -155,29 +167,44 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     else
       bulk_g2s(ga + tid * R::SMA, L.rec_ma + static_cast<size_t>(c) * R::GM, R::MA, &bar[0]);
   };
-  auto issue_b = [&](int i) {
+  // B1 (the OI rows) exists for CWENOZ tiles only: those are a prefix of every
+  // block's item sequence, so its barrier's parity is the iteration's as well
+  auto issue_b1 = [&](int i) {
+    if (i >= tc) return;
     const int c = tile_cell(i, tid);
-    if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * (i < tc ? R::CB : R::MB));
+    if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * R::CB1);
+    __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
+    bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::GC, R::CB1, &bar[1]);
+  };
+  auto issue_b2 = [&](int i) {
+    const int c = tile_cell(i, tid);
+    if (tid == 0) mbar_arrive_expect_tx(&bar[2], TC * (i < tc ? R::CB - R::CB1 : R::MB));
     __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
-      bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::GC, R::CB, &bar[1]);
+      bulk_g2s(gb + tid * R::SCB + R::CB1, L.rec_cb + static_cast<size_t>(c) * R::GC + R::CB1, R::CB - R::CB1,
+               &bar[2]);
     else
-      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[1]);
+      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[2]);
   };
   if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);
-    issue_b(blockIdx.x);
+    issue_b1(blockIdx.x);
+    issue_b2(blockIdx.x);
   }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool venkat = ph.limiter == 1;
   int it = 0;
+  int c_next = (UCFVB_CELLS_CN && static_cast<int>(blockIdx.x) < nitems) ? tile_cell(blockIdx.x, slot) : 0;
   for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
     const uint32_t par = it & 1;
     const int next = i + gridDim.x;
     const bool cw = i < tc;
     const bool mine = cw ? i * TC + slot < nc : (i - tc) * TC + slot < nm;
-    const int c = tile_cell(i, slot);
+    // the next tile's list entry is requested a tile ahead (UCFVB_CELLS_CN): its
+    // L2 round trip leaves the head of that tile's dependency chain
+    const int c = UCFVB_CELLS_CN ? c_next : tile_cell(i, slot);
+    if (UCFVB_CELLS_CN && next < nitems) c_next = tile_cell(next, slot);
     const double u0 = __ldg(Ud + 4 * static_cast<size_t>(c) + v);
     double vals[Q];
     double lo = u0, hi = u0;
@@ -192,6 +219,10 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
       const unsigned char* ra = ga + slot * R::SCA;
       const double* spd = reinterpret_cast<const double*>(ra + R::CA_PD);
       const int* sdi = reinterpret_cast<const int*>(ra + R::CA_ID);
+      const int* snb = reinterpret_cast<const int*>(ra + R::CA_NBR);
+      int nbv[NF];
+#pragma unroll
+      for (int j = 0; j < NF; ++j) nbv[j] = snb[j];
       double um[NF][MD];
 #pragma unroll
       for (int s = 0; s < NF; ++s)
@@ -226,18 +257,14 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) p1[k] = rl ? div_rn(p1[k], lam0, ph.inv_lam0) : p1[k] / lam0;
+      double xn[NF];  // fallback bounds' neighbour values, in flight during the blend
+#pragma unroll
+      for (int j = 0; j < NF; ++j) xn[j] = nbv[j] >= 0 ? __ldg(Ud + 4 * static_cast<size_t>(nbv[j]) + v) : 0.0;
       mbar_wait(&bar[1], par);
       const unsigned char* rb = gb + slot * R::SCB;
       const double* soi = reinterpret_cast<const double*>(rb + R::CB_OI);
       const double* sph = reinterpret_cast<const double*>(rb + R::CB_PHI);
-      const int* snb = reinterpret_cast<const int*>(rb + R::CB_NBR);
       const int* sdst = reinterpret_cast<const int*>(rb + R::CB_DST);
-      int nbv[NF];
-#pragma unroll
-      for (int j = 0; j < NF; ++j) nbv[j] = snb[j];
-      double xn[NF];  // fallback bounds' neighbour values, in flight during the blend
-#pragma unroll
-      for (int j = 0; j < NF; ++j) xn[j] = nbv[j] >= 0 ? __ldg(Ud + 4 * static_cast<size_t>(nbv[j]) + v) : 0.0;
       double si0 = 0.0;
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -247,6 +274,13 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         si0 += p1[k] * t;
       }
       const double o00 = soi[0], o01 = soi[1], o10 = soi[K], o11 = soi[K + 1];
+      if (UCFVB_CELLS_B3) {
+        __syncthreads();  // group B1 consumed: request the next tile's
+        if (tid < TC && next < nitems) {
+          fence_proxy_async_smem();
+          issue_b1(next);
+        }
+      }
       double sis[NF];
       double tau = 0.0;
 #pragma unroll
@@ -278,6 +312,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         p1[0] += w * dir[s][0];
         p1[1] += w * dir[s][1];
       }
+      mbar_wait(&bar[2], par);
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) {
         vals[lq] = u0;
@@ -302,6 +337,9 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
       const unsigned char* ra = ga + slot * R::SMA;
       const double* spl = reinterpret_cast<const double*>(ra + R::MA_PL);
       const int* sid = reinterpret_cast<const int*>(ra + R::MA_ID);
+      int nbm[NF];  // face neighbours (read before group A is refilled)
+#pragma unroll
+      for (int j = 0; j < NF; ++j) nbm[j] = reinterpret_cast<const int*>(ra + R::MA_NBR)[j];
       double um[MM];
 #pragma unroll
       for (int m = 0; m < MM; ++m) um[m] = __ldg(Ud + 4 * static_cast<size_t>(sid[m]) + v);
@@ -317,14 +355,13 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         fence_proxy_async_smem();
         issue_a(next);
       }
-      mbar_wait(&bar[1], par);
+      mbar_wait(&bar[2], par);
       const unsigned char* rb = gb + slot * R::SMB;
       const double* sp01 = reinterpret_cast<const double*>(rb + R::MB_PHI);
-      const int* snb = reinterpret_cast<const int*>(rb + R::MB_NBR);
       const int* sdst = reinterpret_cast<const int*>(rb + R::MB_DST);
 #pragma unroll
       for (int j = 0; j < NF; ++j) {
-        const int nb = snb[j];
+        const int nb = nbm[j];
         if (nb >= 0) {
           const double x = __ldg(Ud + 4 * static_cast<size_t>(nb) + v);
           lo = smin(lo, x);
@@ -353,10 +390,11 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) dst[lq] = sdst[lq];
     }
-    __syncthreads();  // group B consumed: request the next tile's
+    __syncthreads();  // group B2 consumed: request the next tile's
     if (tid < TC && next < nitems) {
       fence_proxy_async_smem();
-      issue_b(next);
+      if (!UCFVB_CELLS_B3) issue_b1(next);
+      issue_b2(next);
     }
     if (UCFVB_CELLS_PF && next < nitems && v == 0) {
       // the next tile's member rows of U into L2 while this tile finishes

@@ -422,6 +422,10 @@ constexpr int kRingSlots = 3;
 // and phi block (group B) are bulk-copied into shared memory one chunk ahead,
 // each refilled as soon as the solve / the evaluation has consumed it
 // (split-phase, as the 2D k_central_tma)
+// lattice-class central kernel: L1 prefetch of the next chunk's stencil-id lines
+#ifndef UCFVB_C5_PFID
+#define UCFVB_C5_PFID 1
+#endif
 // resident blocks per SM asked of the per-cell-row (p <= 2) central kernels
 #ifndef UCFVB_C3_MINB
 #define UCFVB_C3_MINB 2
@@ -527,6 +531,12 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
     // every stencil and neighbour value of this (cell, variable) in flight at
     // once: G fire-and-forget 8-byte cp.async copies into shared memory
     if constexpr (DM) {
+      if (UCFVB_C5_PFID && nxt < nch && threadIdx.x < M + 1 + NF) {
+        // the next chunk's stencil-id and neighbour lines (one 128-byte line per member) into L1:
+        // their round trip leaves the head of that chunk's ids -> gather dependency chain
+        const int e = threadIdx.x;
+        prefetch_l1(e <= M ? &D.central[ao(nxt << 5, e, M + 1)] : &D.nbr[ao(nxt << 5, e - M - 1, NF)]);
+      }
       // transposed: thread (cell gl, variable gv) -- one member's five variables are one 40-byte read
       const int gl = threadIdx.x / V5, gv = threadIdx.x - gl * V5;
       const int gc = min((ch << 5) + gl, D.n - 1);

@@ -151,6 +151,14 @@ int32_t ucfvb3_run_steps(ucfvb3_solver* h, int32_t n_steps, double t0, int32_t r
  * -> host state out, one synchronisation (as ucfvb_advance_host) */
 int32_t ucfvb3_advance_host(ucfvb3_solver* h, const double* u_in, double* u_out, int32_t n_steps, int32_t rk,
                             double t0, double* t_out);
+/* ucfvb3_advance_host over n_batch independent states of the mesh, pipelined
+ * as ucfvb_advance_host_batch (include/ucfvb.h): the upload of entry i+1 and
+ * the download of entry i-1 overlap the stepping of entry i; every entry's
+ * bits equal its own ucfvb3_advance_host call. t_out (nullable): [n_batch].
+ * Every entry starts from reset error counters; the first failing entry is
+ * reported (its u_out is its failing step's input), the others are unaffected. */
+int32_t ucfvb3_advance_host_batch(ucfvb3_solver* h, int32_t n_batch, const double* const* u_in,
+                                  double* const* u_out, int32_t n_steps, int32_t rk, double t0, double* t_out);
 int32_t ucfvb3_compute_residual(ucfvb3_solver* h, const double* u, double t, double* out);
 /* which = 0: labels of the last stage; 1: step labels (first stage of the last step) */
 int32_t ucfvb3_get_labels(ucfvb3_solver* h, int32_t which, uint8_t* out);

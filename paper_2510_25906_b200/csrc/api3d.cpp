@@ -139,6 +139,14 @@ int32_t ucfvb3_advance_host(ucfvb3_solver* h, const double* u_in, double* u_out,
     if (t_out) *t_out = t;
   });
 }
+int32_t ucfvb3_advance_host_batch(ucfvb3_solver* h, int32_t n_batch, const double* const* u_in,
+                                  double* const* u_out, int32_t n_steps, int32_t rk, double t0, double* t_out) {
+  NEED(h);
+  return guard3(h, [&] {
+    if (!u_in || !u_out) throw ucfvb::ApiError(UCFVB_INVALID, "advance_host_batch: null pointer table");
+    h->s->advance_host_batch(n_batch, u_in, u_out, n_steps, rk, t0, t_out);
+  });
+}
 int32_t ucfvb3_compute_residual(ucfvb3_solver* h, const double* u, double t, double* out) {
   NEED(h);
   return guard3(h, [&] { h->s->compute_residual(u, t, out); });

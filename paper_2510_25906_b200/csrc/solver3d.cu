@@ -849,13 +849,25 @@ __global__ void __launch_bounds__(256) k3_spread(Dev3 D, Work3 W, const double* 
       // fallback_check demotes the Linear candidate (solver.cpp:256-262), or a
       // frozen FirstOrder label (apply_troubled's constant branch): first-order values
       lab = UCFVB_SCHEME_FIRST;
-      for (int q = 0; q < Q; ++q) {
-        double* dst = &W.fp[static_cast<size_t>(D.slot[ao(c, q, Q)]) * V5];
-#pragma unroll
-        for (int v = 0; v < V5; ++v) dst[v] = U[static_cast<size_t>(c) * V5 + v];
-      }
     }
     W.labels[c] = static_cast<uint8_t>(lab);
+  }
+  {
+    // first-order face values, written by the whole warp per demoted cell: lane e of pass j
+    // stores value (point e / 5, variable e % 5), so a face's points go out as contiguous runs
+    // (one thread per cell wrote 120 scattered 8-byte stores with 4 of 5 lanes idle)
+    unsigned fo = __ballot_sync(0xffffffffu, ok && lab == UCFVB_SCHEME_FIRST);
+    const int c0 = c - lane;
+    while (fo) {
+      const int l = __ffs(fo) - 1;
+      fo &= fo - 1;
+      const int cc = c0 + l;
+#pragma unroll
+      for (int e = lane; e < Q * V5; e += 32) {
+        const int q = e / V5, v = e - q * V5;
+        W.fp[static_cast<size_t>(D.slot[ao(cc, q, Q)]) * V5 + v] = U[static_cast<size_t>(cc) * V5 + v];
+      }
+    }
   }
   // warp-aggregated appends to the CWENOZ / MUSCL lists
   for (int L = 0; L < 2; ++L) {
@@ -1714,6 +1726,20 @@ struct GpuSolver3::Impl {
   uint8_t* step_labels = nullptr;
   int32_t* h_counters = nullptr;
   double* h_dt = nullptr;
+  // advance_host_batch: device staging per direction, copy streams, events, pinned per-entry results
+  double* pipe_up[2] = {nullptr, nullptr};
+  double* pipe_down[2] = {nullptr, nullptr};
+  cudaStream_t up_st = nullptr, down_st = nullptr;
+  cudaEvent_t pipe_ev[8] = {};
+  char* pipe_host = nullptr;
+  int pipe_slots = 0;
+  void free_pipe() {
+    if (pipe_host) cudaFreeHost(pipe_host);
+    for (auto& e : pipe_ev)
+      if (e) cudaEventDestroy(e);
+    if (up_st) cudaStreamDestroy(up_st);
+    if (down_st) cudaStreamDestroy(down_st);
+  }
   int64_t launches = 0, graph_launches = 0;
   int central_grid = 0, cw_grid = 0, mu_grid = 0;
   // decomposition: owned cells first; NCCL halo exchange after every stage
@@ -2163,6 +2189,7 @@ GpuSolver3::~GpuSolver3() {
   for (void* q : I.owned) cudaFree(q);
   if (I.h_counters) cudaFreeHost(I.h_counters);
   if (I.h_dt) cudaFreeHost(I.h_dt);
+  I.free_pipe();
   if (I.st) cudaStreamDestroy(I.st);
   if (I.comm_st) cudaStreamDestroy(I.comm_st);
   if (I.ev_fork) cudaEventDestroy(I.ev_fork);
@@ -2264,6 +2291,91 @@ double GpuSolver3::advance_host(const double* u_in, double* u_out, int n_steps, 
   if (I.h_counters[kBadCell] != 0x7fffffff)
     throw ApiError(UCFVB_NONPHYSICAL, "non-physical state in cell " + std::to_string(I.h_counters[kBadCell]));
   return I.h_dt[0];
+}
+
+// advance_host over independent states, pipelined as the 2D ucfvb_advance_host_batch: the upload
+// of entry i+1 and the download of entry i-1 run on copy streams while entry i is stepped (two
+// device staging buffers per direction, device-to-device copies into and out of U).
+void GpuSolver3::advance_host_batch(int n_batch, const double* const* u_in, double* const* u_out, int n_steps, int rk,
+                                    double t0, double* t_out) {
+  Impl& I = *p_;
+  if (rk != UCFVB_RK3 && rk != UCFVB_RK54) throw ApiError(UCFVB_INVALID, "advance_host_batch: unknown integrator");
+  if (n_steps <= 0) throw ApiError(UCFVB_INVALID, "advance_host_batch: n_steps must be >= 1");
+  if (n_batch <= 0) throw ApiError(UCFVB_INVALID, "advance_host_batch: n_batch must be >= 1");
+  for (int i = 0; i < n_batch; ++i)
+    if (!u_in[i] || !u_out[i]) throw ApiError(UCFVB_INVALID, "advance_host_batch: null state pointer");
+  CK3(cudaSetDevice(I.device));
+  const size_t count = static_cast<size_t>(I.n) * V5, bytes = sizeof(double) * count;
+  if (!I.pipe_up[0]) {
+    for (int i = 0; i < 2; ++i) {
+      I.pipe_up[i] = dalloc<double>(count, I.owned);
+      I.pipe_down[i] = dalloc<double>(count, I.owned);
+    }
+    CK3(cudaStreamCreateWithFlags(&I.up_st, cudaStreamNonBlocking));
+    CK3(cudaStreamCreateWithFlags(&I.down_st, cudaStreamNonBlocking));
+    for (auto& e : I.pipe_ev) CK3(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  // pinned per entry: t0 (in), final t (out), the four error counters (out), the counters' reset values (in)
+  const size_t slot = 2 * sizeof(double) + 8 * sizeof(int32_t);
+  if (I.pipe_slots < n_batch) {
+    if (I.pipe_host) CK3(cudaFreeHost(I.pipe_host));
+    I.pipe_host = nullptr;
+    CK3(cudaMallocHost(&I.pipe_host, slot * n_batch));
+    I.pipe_slots = n_batch;
+  }
+  auto h_t = [&](int i) { return reinterpret_cast<double*>(I.pipe_host + slot * i); };
+  auto h_c = [&](int i) { return reinterpret_cast<int32_t*>(I.pipe_host + slot * i + 2 * sizeof(double)); };
+  if (!I.timing && (!I.step_graph || I.graph_rk != rk)) I.capture(rk);
+  // events: [0..1] upload landed, [2..3] upload buffer consumed, [4..5] result staged, [6..7] download done
+  cudaEvent_t* ev = I.pipe_ev;
+  for (int i = 0; i < n_batch; ++i) {
+    const int b = i & 1;
+    if (i >= 2) CK3(cudaStreamWaitEvent(I.up_st, ev[2 + b], 0));
+    CK3(cudaMemcpyAsync(I.pipe_up[b], u_in[i], bytes, cudaMemcpyHostToDevice, I.up_st));
+    CK3(cudaEventRecord(ev[b], I.up_st));
+    CK3(cudaStreamWaitEvent(I.st, ev[b], 0));
+    CK3(cudaMemcpyAsync(I.U, I.pipe_up[b], bytes, cudaMemcpyDeviceToDevice, I.st));
+    CK3(cudaEventRecord(ev[2 + b], I.st));
+    const int32_t init[4] = {0, 0, 0x7fffffff, 0x7fffffff};  // halt, -, bad face, bad cell (reset_errors)
+    std::memcpy(h_c(i) + 4, init, sizeof init);
+    CK3(cudaMemcpyAsync(I.W.counters, h_c(i) + 4, sizeof init, cudaMemcpyHostToDevice, I.st));
+    h_t(i)[0] = t0;
+    CK3(cudaMemcpyAsync(I.W.t, &h_t(i)[0], sizeof(double), cudaMemcpyHostToDevice, I.st));
+    for (int s = 0; s < n_steps; ++s) {
+      if (I.timing) {
+        I.dt_kernels();
+        I.step(rk);
+        k3_time_add<<<1, 1, 0, I.st>>>(I.W);
+        ++I.launches;
+      } else {
+        CK3(cudaGraphLaunch(I.step_graph, I.st));
+        I.launches += I.graph_launches;
+      }
+    }
+    CK3(cudaMemcpyAsync(&h_t(i)[1], I.W.t, sizeof(double), cudaMemcpyDeviceToHost, I.st));
+    CK3(cudaMemcpyAsync(h_c(i), I.W.counters, 4 * sizeof(int32_t), cudaMemcpyDeviceToHost, I.st));
+    if (i >= 2) CK3(cudaStreamWaitEvent(I.st, ev[6 + b], 0));
+    CK3(cudaMemcpyAsync(I.pipe_down[b], I.U, bytes, cudaMemcpyDeviceToDevice, I.st));
+    CK3(cudaEventRecord(ev[4 + b], I.st));
+    CK3(cudaStreamWaitEvent(I.down_st, ev[4 + b], 0));
+    CK3(cudaMemcpyAsync(u_out[i], I.pipe_down[b], bytes, cudaMemcpyDeviceToHost, I.down_st));
+    CK3(cudaEventRecord(ev[6 + b], I.down_st));
+  }
+  CK3(cudaStreamSynchronize(I.st));
+  CK3(cudaStreamSynchronize(I.down_st));
+  CK3(cudaGetLastError());
+  I.reset_errors();
+  for (int i = 0; i < n_batch; ++i) {
+    // every entry starts from reset counters: a failing entry (its result is its failing step's
+    // input) leaves the others untouched; the first one is reported
+    if (h_c(i)[kBadFace] != 0x7fffffff)
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state at face " + std::to_string(h_c(i)[kBadFace]) +
+                                            " (batch entry " + std::to_string(i) + ")");
+    if (h_c(i)[kBadCell] != 0x7fffffff)
+      throw ApiError(UCFVB_NONPHYSICAL, "non-physical state in cell " + std::to_string(h_c(i)[kBadCell]) +
+                                            " (batch entry " + std::to_string(i) + ")");
+    if (t_out) t_out[i] = h_t(i)[1];
+  }
 }
 
 void GpuSolver3::compute_residual(const double* u, double t, double* out) {

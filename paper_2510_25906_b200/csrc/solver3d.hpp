@@ -24,6 +24,8 @@ class GpuSolver3 {
   void advance(double dt, double t, int rk);
   double run_steps(int n_steps, double t0, int rk);
   double advance_host(const double* u_in, double* u_out, int n_steps, int rk, double t0);
+  void advance_host_batch(int n_batch, const double* const* u_in, double* const* u_out, int n_steps, int rk,
+                          double t0, double* t_out);
   void compute_residual(const double* u, double t, double* out);
   void get_labels(int which, uint8_t* out);
   void get_face_values(double* out);

@@ -70,6 +70,8 @@ def lib():
             "ucfvb3_run_steps": (C.c_int32, [H, C.c_int32, C.c_double, C.c_int32, _dp]),
             "ucfvb3_compute_residual": (C.c_int32, [H, _dp, C.c_double, _dp]),
             "ucfvb3_advance_host": (C.c_int32, [H, _dp, _dp, C.c_int32, C.c_int32, C.c_double, _dp]),
+            "ucfvb3_advance_host_batch": (C.c_int32, [H, C.c_int32, C.POINTER(_dp), C.POINTER(_dp), C.c_int32,
+                                                  C.c_int32, C.c_double, _dp]),
             "ucfvb3_get_labels": (C.c_int32, [H, C.c_int32, P(C.c_uint8)]),
             "ucfvb3_get_face_values": (C.c_int32, [H, _dp]),
             "ucfvb3_get_census": (C.c_int32, [H, P(C.c_int64)]),
@@ -314,6 +316,19 @@ class Solver3:
         _ck(lib().ucfvb3_advance_host(self._h, u_in.ctypes.data_as(_dp), out.ctypes.data_as(_dp), n_steps, rk, t0,
                                       C.byref(t)), self._h)
         return out, t.value
+
+    def advance_host_batch(self, u_in, n_steps=1, rk=A.RK3, t0=0.0, u_out=None):
+        """advance_host over independent states, pipelined (uploads / downloads overlap the stepping).
+        Returns (outs, t[n_batch])."""
+        ins = [np.ascontiguousarray(u, dtype=np.float64).reshape(self.n, NV) for u in u_in]
+        outs = [np.empty_like(u) for u in ins] if u_out is None else list(u_out)
+        nb = len(ins)
+        tab_in = (_dp * nb)(*[u.ctypes.data_as(_dp) for u in ins])
+        tab_out = (_dp * nb)(*[u.ctypes.data_as(_dp) for u in outs])
+        t = np.zeros(nb)
+        _ck(lib().ucfvb3_advance_host_batch(self._h, nb, tab_in, tab_out, n_steps, rk, t0, t.ctypes.data_as(_dp)),
+            self._h)
+        return outs, t
 
     def compute_residual(self, u, t=0.0):
         u = np.ascontiguousarray(u, dtype=np.float64)

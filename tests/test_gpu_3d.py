@@ -303,6 +303,26 @@ def test_advance_host_matches_run_steps3():
         gpu.advance_host(bad, 1)
 
 
+def test_advance_host_batch_matches_serial3():
+    """ucfvb3_advance_host_batch (pipelined uploads / downloads over independent states): every
+    entry has the bits of its own ucfvb3_advance_host call; a failing entry is named and leaves
+    the others untouched."""
+    m, st, o, u0, gpu, cpu = build(TET, 2, 0.05, IC_BLAST, mode="hybrid")
+    ins = [u0 * (1.0 + 0.03 * i) for i in range(5)]
+    for n_steps in (1, 2):
+        outs, ts = gpu.advance_host_batch(ins, n_steps)
+        for u, out, t in zip(ins, outs, ts):
+            ref, t_ref = gpu.advance_host(u, n_steps)
+            assert t == t_ref
+            np.testing.assert_array_equal(out, ref)
+    bad = [u.copy() for u in ins]
+    bad[2][3, 0] = -1.0
+    with pytest.raises(A.NonPhysicalError, match="batch entry 2"):
+        gpu.advance_host_batch(bad, 1)
+    outs, _ = gpu.advance_host_batch(ins[:2], 1)
+    np.testing.assert_array_equal(outs[1], gpu.advance_host(ins[1], 1)[0])
+
+
 @pytest.mark.parametrize("order", [2, 3])
 def test_staged_tensor_core_path_with_troubled_cells(order):
     """Type-blocked lattice-class mesh (8^3 cubes x 6 tets: staged rows, DMMA

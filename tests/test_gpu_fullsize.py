@@ -193,3 +193,39 @@ def test_class_list_policies_bit_identical(name, scale):
     assert int(pad(lab == 1).any(1).sum()) <= sc["cwenoz_chunks"] <= int(pad(lab >= 1).any(1).sum())
     assert int(pad(lab == 2).any(1).sum()) <= sc["muscl_chunks"] <= int(pad(lab >= 1).any(1).sum())
     assert 32 * sc["cwenoz_chunks"] >= sc["cwenoz_cells"] and 32 * sc["muscl_chunks"] >= sc["muscl_cells"]
+
+
+@pytest.mark.parametrize("policy", ["chunks", "lists"])
+def test_wide_spread_ragged_mesh_against_oracle(policy):
+    """A jittered p = 2 mesh of 727 x 727 x 2 = 1,057,058 triangles: above the size where
+    k_spread runs eight cells per thread, and not a multiple of its 1,024-cell block (nor of the
+    32-cell chunk), with all three NAD classes present (shock into a sine wave, periodic in y,
+    transmissive in x). One stage and one SSP-RK3 step against the oracle port: labels identical,
+    residual within 1e-10, with chunk lists and with per-cell lists."""
+    from oracle.port import PortSolver
+    from tests.cases import SHOCK_SINE
+
+    mesh = Mesh.structured_tri(727, 727, (-5.0, 0.0, 5.0, 1.0), jitter=0.1, seed=5, periodic="y", n_qp=2)
+    assert mesh.n_cells == 1_057_058 and mesh.n_cells % 1024 != 0 and mesh.n_cells % 32 != 0
+    st = Stencils(mesh, 2)
+    bcs = make_bcs({"left": "outflow", "right": "outflow"})
+    o = A.options_from_dict(order=2, mode="hybrid", lambda1p=1e3, cfl=0.5)
+    u0 = mesh.project_initial(1, SHOCK_SINE, seed=1, degree=4)
+    g = Solver(mesh, o, bcs, stencils=st)
+    g.set_list_policy(policy)
+    cpu = PortSolver(mesh.view, st.view, o, bcs, keep=(mesh, st))
+    r_gpu = g.compute_residual(u0, 0.0)
+    r_cpu = cpu.compute_residual(u0, 0.0, 1)
+    lab = g.labels()
+    np.testing.assert_array_equal(lab, cpu.labels())
+    census = np.bincount(lab, minlength=4)
+    assert census[0] > 0 and census[1] > 0 and census[2] > 0, census
+    assert scaled_err(r_gpu, r_cpu) <= 1e-10
+    g.state = u0
+    cpu.state = u0.copy()
+    dt = g.max_stable_dt()
+    assert dt == cpu.max_stable_dt()
+    g.advance(dt, 0.0, A.RK3)
+    cpu.advance(dt, 0.0, A.RK3)
+    np.testing.assert_array_equal(g.step_labels(), cpu.labels(step=True))
+    assert scaled_err(g.state, cpu.state) <= 1e-10

@@ -18,10 +18,11 @@
 //           B2: phi01 [lq][k<2] (f64), face-point slots [lq] (i32)
 // Split-phase refill, one shared-memory slot per group and an mbarrier each:
 // group A (directional / r=1 solves, fallback bounds) is refilled with the
-// next tile as soon as the solves are done, B1 as soon as the smoothness
-// indicators are, B2 after the evaluation -- every group is requested most of
-// a tile before it is read (measured neutral on config 3 against B1 + B2
-// requested together at the tile's end: profiles/round2.md).
+// next tile as soon as the solves are done, group B = B1 | B2 (one copy) after
+// the evaluation. (Refilling B1 on its own as soon as the smoothness
+// indicators were done measured neutral and cost a third bulk copy per cell --
+// a bulk copy with per-lane addresses is ~9 issued instructions, 12 % of this
+// kernel's instructions with three copies per cell: profiles/round2.md.)
 #pragma once
 
 #include "kernels_tma.cuh"
@@ -95,6 +96,43 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
   }
 }
 
+// fallback_check's verdict for the cells of a single-warp tile (group_demote,
+// kernels.cuh): the positivity check needs the four variables of a face point
+// in one lane. Each lane writes its variable of the cell's Q points to a
+// [point][variable] scratch row (the tile's dead group-B region), and lane v
+// reads points v, v + 4, ... as two 16-byte loads -- ~15 instructions where the
+// shuffle transpose (group_nonphysical) took ~90 (12 % of this kernel's).
+// All 32 lanes of the warp call it; the scratch is free again on return.
+__host__ __device__ constexpr uint32_t demote_stride(int Q) { return odd16(32u * Q); }  // bytes per cell
+template <int Q>
+__device__ __forceinline__ bool tile_demote(const Physics& ph, int v, int slot, double lo, double hi,
+                                            const double* vals, unsigned char* scratch) {
+  double dm, dw;
+  compute_margins(ph.mp, hi - lo, dm, dw);
+  double* sc = reinterpret_cast<double*>(scratch + slot * demote_stride(Q));
+#pragma unroll
+  for (int lq = 0; lq < Q; ++lq) sc[lq * 4 + v] = vals[lq];
+  __syncwarp();
+  bool bad = false;
+#pragma unroll
+  for (int r = 0; r < (Q + 3) / 4; ++r) {
+    const int q = 4 * r + v;
+    if (q < Q) {
+      const double2 a = *reinterpret_cast<const double2*>(sc + q * 4);
+      const double2 b = *reinterpret_cast<const double2*>(sc + q * 4 + 2);
+      const double st[NV] = {a.x, a.y, b.x, b.y};
+      bad |= !is_physical(st, ph.gamma);
+    }
+  }
+  if (v == 0 || v == 3) {
+#pragma unroll
+    for (int lq = 0; lq < Q; ++lq) bad |= smax(lo - vals[lq], vals[lq] - hi) > dm;
+  }
+  bad = grp_any(bad);
+  __syncwarp();
+  return bad;
+}
+
 // Work items: tiles of 32 list entries, CWENOZ tiles [0, tc) then MUSCL tiles.
 // Four lanes per cell (lane v = conserved variable v); arithmetic identical
 // to k_troubled_split / k_cwenoz / k_muscl.
@@ -106,11 +144,6 @@ __global__ void k_pack_records(Layout L, unsigned char* rc, unsigned char* rm) {
 #endif
 #ifndef UCFVB_CELLS_TILE
 #define UCFVB_CELLS_TILE 8
-#endif
-// 1: group B1 (OI rows) refilled as soon as the smoothness indicators are done
-// (0: together with B2 at the tile's end, the two-group schedule)
-#ifndef UCFVB_CELLS_B3
-#define UCFVB_CELLS_B3 1
 #endif
 #ifndef UCFVB_CELLS_CN
 #define UCFVB_CELLS_CN 1
@@ -125,7 +158,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
   using R = CellRec<K, NQ, NF, MM, MD, TC>;
   constexpr int Q = R::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B1 (CWENOZ), [2] group B2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B
   unsigned char* const ga = smem;
   unsigned char* const gb = smem + R::TILE_A;
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
@@ -140,7 +173,6 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     s_nm = S.counts[1];
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -167,29 +199,18 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     else
       bulk_g2s(ga + tid * R::SMA, L.rec_ma + static_cast<size_t>(c) * R::GM, R::MA, &bar[0]);
   };
-  // B1 (the OI rows) exists for CWENOZ tiles only: those are a prefix of every
-  // block's item sequence, so its barrier's parity is the iteration's as well
-  auto issue_b1 = [&](int i) {
-    if (i >= tc) return;
+  auto issue_b = [&](int i) {
     const int c = tile_cell(i, tid);
-    if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * R::CB1);
-    __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
-    bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::GC, R::CB1, &bar[1]);
-  };
-  auto issue_b2 = [&](int i) {
-    const int c = tile_cell(i, tid);
-    if (tid == 0) mbar_arrive_expect_tx(&bar[2], TC * (i < tc ? R::CB - R::CB1 : R::MB));
+    if (tid == 0) mbar_arrive_expect_tx(&bar[1], TC * (i < tc ? R::CB : R::MB));
     __syncwarp(TC == 32 ? 0xffffffffu : (1u << TC) - 1u);
     if (i < tc)
-      bulk_g2s(gb + tid * R::SCB + R::CB1, L.rec_cb + static_cast<size_t>(c) * R::GC + R::CB1, R::CB - R::CB1,
-               &bar[2]);
+      bulk_g2s(gb + tid * R::SCB, L.rec_cb + static_cast<size_t>(c) * R::GC, R::CB, &bar[1]);
     else
-      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[2]);
+      bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[1]);
   };
   if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);
-    issue_b1(blockIdx.x);
-    issue_b2(blockIdx.x);
+    issue_b(blockIdx.x);
   }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
@@ -255,8 +276,20 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         p1[0] -= lams * dir[s][0];
         p1[1] -= lams * dir[s][1];
       }
+      {
+        // one range test for the batch (exact_math.h): all numerators in range ->
+        // the reciprocal form for all, else the IEEE division for all (same bits)
+        bool okb = rl;
 #pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = rl ? div_rn(p1[k], lam0, ph.inv_lam0) : p1[k] / lam0;
+        for (int k = 0; k < K; ++k) okb = okb && div_rn_ok(p1[k]);
+        if (okb) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) p1[k] = div_rn_unchecked(p1[k], lam0, ph.inv_lam0);
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) p1[k] = p1[k] / lam0;
+        }
+      }
       double xn[NF];  // fallback bounds' neighbour values, in flight during the blend
 #pragma unroll
       for (int j = 0; j < NF; ++j) xn[j] = nbv[j] >= 0 ? __ldg(Ud + 4 * static_cast<size_t>(nbv[j]) + v) : 0.0;
@@ -274,13 +307,6 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         si0 += p1[k] * t;
       }
       const double o00 = soi[0], o01 = soi[1], o10 = soi[K], o11 = soi[K + 1];
-      if (UCFVB_CELLS_B3) {
-        __syncthreads();  // group B1 consumed: request the next tile's
-        if (tid < TC && next < nitems) {
-          fence_proxy_async_smem();
-          issue_b1(next);
-        }
-      }
       double sis[NF];
       double tau = 0.0;
 #pragma unroll
@@ -301,9 +327,20 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
       }
       const double rw = 1.0 / wsum;  // wsum >= lam0 > 0
       const bool rwok = rl && wsum <= 0x1p60;
-      om0 = rwok ? div_rn(om0, wsum, rw) : om0 / wsum;
+      {
+        bool okb = rwok && div_rn_ok(om0);
 #pragma unroll
-      for (int s = 0; s < NF; ++s) oms[s] = rwok ? div_rn(oms[s], wsum, rw) : oms[s] / wsum;
+        for (int s = 0; s < NF; ++s) okb = okb && div_rn_ok(oms[s]);
+        if (okb) {
+          om0 = div_rn_unchecked(om0, wsum, rw);
+#pragma unroll
+          for (int s = 0; s < NF; ++s) oms[s] = div_rn_unchecked(oms[s], wsum, rw);
+        } else {
+          om0 = om0 / wsum;
+#pragma unroll
+          for (int s = 0; s < NF; ++s) oms[s] = oms[s] / wsum;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
 #pragma unroll
@@ -312,7 +349,6 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         p1[0] += w * dir[s][0];
         p1[1] += w * dir[s][1];
       }
-      mbar_wait(&bar[2], par);
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) {
         vals[lq] = u0;
@@ -355,7 +391,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         fence_proxy_async_smem();
         issue_a(next);
       }
-      mbar_wait(&bar[2], par);
+      mbar_wait(&bar[1], par);
       const unsigned char* rb = gb + slot * R::SMB;
       const double* sp01 = reinterpret_cast<const double*>(rb + R::MB_PHI);
       const int* sdst = reinterpret_cast<const int*>(rb + R::MB_DST);
@@ -390,11 +426,17 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) dst[lq] = sdst[lq];
     }
-    __syncthreads();  // group B2 consumed: request the next tile's
+    __syncthreads();  // group B consumed (its face-point slots are in registers)
+    // fallback verdict first: the positivity check transposes the tile's face
+    // values through the dead group-B region (tile_demote), then the refill
+    bool demote = false;
+    constexpr bool kScratchFits = TC * demote_stride(Q) <= R::TILE_B;  // (not for p = 1 quadrilaterals)
+    if (flags & FL_FALLBACK)
+      demote = kScratchFits ? tile_demote<Q>(ph, v, slot, lo, hi, vals, gb) : group_demote<Q>(ph, v, lo, hi, vals, Q);
+    if (4 * TC > 32) __syncthreads();  // multi-warp tiles: every warp's scratch reads precede the refill
     if (tid < TC && next < nitems) {
       fence_proxy_async_smem();
-      if (!UCFVB_CELLS_B3) issue_b1(next);
-      issue_b2(next);
+      issue_b(next);
     }
     if (UCFVB_CELLS_PF && next < nitems && v == 0) {
       // the next tile's member rows of U into L2 while this tile finishes
@@ -409,8 +451,6 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         for (int m = 0; m < MM; ++m) prefetch_l2(U + nid[m]);
       }
     }
-    bool demote = false;
-    if (flags & FL_FALLBACK) demote = group_demote<Q>(ph, v, lo, hi, vals, Q);
     if (mine) {
 #pragma unroll
       for (int lq = 0; lq < Q; ++lq) fv[4 * static_cast<size_t>(dst[lq]) + v] = demote ? u0 : vals[lq];

@@ -436,8 +436,19 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
         p1[0] -= lams * dir[s][0];
         p1[1] -= lams * dir[s][1];
       }
+      {
+        // one range test for the batch (exact_math.h), as k_troubled_cells
+        bool okb = rl;
 #pragma unroll
-      for (int k = 0; k < K; ++k) p1[k] = rl ? div_rn(p1[k], lam0, ph.inv_lam0) : p1[k] / lam0;
+        for (int k = 0; k < K; ++k) okb = okb && div_rn_ok(p1[k]);
+        if (okb) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) p1[k] = div_rn_unchecked(p1[k], lam0, ph.inv_lam0);
+        } else {
+#pragma unroll
+          for (int k = 0; k < K; ++k) p1[k] = p1[k] / lam0;
+        }
+      }
       mbar_wait(&bar[1], par);
       const double* soi = reinterpret_cast<const double*>(gb);
       const double* sph = reinterpret_cast<const double*>(gb + St::C_OI);
@@ -471,9 +482,20 @@ __global__ void __launch_bounds__(kBlock) k_troubled_split(Layout L, Physics ph,
       }
       const double rw = 1.0 / wsum;  // wsum >= lam0 > 0
       const bool rwok = rl && wsum <= 0x1p60;
-      om0 = rwok ? div_rn(om0, wsum, rw) : om0 / wsum;
+      {
+        bool okb = rwok && div_rn_ok(om0);
 #pragma unroll
-      for (int s = 0; s < NF; ++s) oms[s] = rwok ? div_rn(oms[s], wsum, rw) : oms[s] / wsum;
+        for (int s = 0; s < NF; ++s) okb = okb && div_rn_ok(oms[s]);
+        if (okb) {
+          om0 = div_rn_unchecked(om0, wsum, rw);
+#pragma unroll
+          for (int s = 0; s < NF; ++s) oms[s] = div_rn_unchecked(oms[s], wsum, rw);
+        } else {
+          om0 = om0 / wsum;
+#pragma unroll
+          for (int s = 0; s < NF; ++s) oms[s] = oms[s] / wsum;
+        }
+      }
 #pragma unroll
       for (int k = 0; k < K; ++k) p1[k] = om0 * p1[k];
 #pragma unroll

@@ -117,7 +117,7 @@ void troubled_split_launcher(dim3 g, cudaStream_t st, const Layout& L, const Phy
 template <int K, int NQ, int NF, int MM, int MD>
 void troubled_cells_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                              const double4* U, int f) {
-  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(4 * kCellTile), CellRec<K, NQ, NF, MM, MD, kCellTile>::BYTES + 32,
+  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(4 * kCellTile), CellRec<K, NQ, NF, MM, MD, kCellTile>::BYTES + 16,
            st, L, p, S, U, f);
 }
 
@@ -174,7 +174,7 @@ KernelSet make_set() {
     using R = CellRec<K, NQ, NF, MMT, MDT>;
     s.cells_setup = [](int n_sm, int* grid, KernelSet::Launch* launch) {
       *grid = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT>,
-                              CellRec<K, NQ, NF, MMT, MDT, kCellTile>::BYTES + 32, n_sm, 4 * kCellTile);
+                              CellRec<K, NQ, NF, MMT, MDT, kCellTile>::BYTES + 16, n_sm, 4 * kCellTile);
       *launch = troubled_cells_launcher<K, NQ, NF, MMT, MDT>;
     };
     s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* rc, unsigned char* rm) {

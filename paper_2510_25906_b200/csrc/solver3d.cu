@@ -512,6 +512,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
     const int c = (ch << 5) + lane;
     const bool act = c < D.n;
     const int cc = act ? c : (D.n - 1);
+    if (v == 0) s_pos[lane] = 0;  // read last before the previous iteration's final barrier
     const int op = D.opi[cc];
     const int nxt = ch + static_cast<int>(gridDim.x);
     if (!TMA && D.n_ops == D.n && threadIdx.x == 0 && ch + static_cast<int>(gridDim.x) < nch) {
@@ -657,7 +658,10 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
         }
       }
     }
-    __syncthreads();  // the gather buffer becomes the face-value buffer
+    // the gather buffer becomes the face-value buffer (DM: every gather read precedes the
+    // barrier after the solve, and until the barrier behind the evaluation each warp only
+    // touches its own dofs rows)
+    if (!DM) __syncthreads();
     if (TMA && threadIdx.x == 0 && nxt < nch) {  // pinv consumed: the next chunk's
       fence_proxy_async_smem();
       issue_pinv(nxt);
@@ -781,8 +785,9 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_ce
       s_sev[t][lane] = sev;
       s_bf[t][lane] = viol > dm;
     }
-    if (v == 0) s_pos[lane] = 0;
-    __syncthreads();
+    // the face values are visible (DM: the barrier behind the evaluation; s_pos was cleared
+    // at the top of the iteration)
+    if (!DM) __syncthreads();
     if (eval && nad) {
       // positivity of every face value of the 32 cells, spread over the block
       for (int p = threadIdx.x; p < Q * 32; p += 160) {

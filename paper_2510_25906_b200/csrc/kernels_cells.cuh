@@ -148,10 +148,6 @@ __device__ __forceinline__ bool tile_demote(const Physics& ph, int v, int slot, 
 #ifndef UCFVB_CELLS_CN
 #define UCFVB_CELLS_CN 1
 #endif
-// lane 0 issues a tile's bulk copies (needs UCFVB_CELLS_CN: the next tile's cells a tile ahead)
-#ifndef UCFVB_CELLS_L0
-#define UCFVB_CELLS_L0 0
-#endif
 
 // cells per tile; a block is 4 * kCellTile threads
 constexpr int kCellTile = UCFVB_CELLS_TILE;
@@ -212,31 +208,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     else
       bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[1]);
   };
-  // UCFVB_CELLS_L0 (single-warp tiles): lane 0 issues the tile's TC copies itself, the cells
-  // handed over by shuffles from the compute lanes (lane 4 j holds slot j's cell). With one
-  // copy per lane the compiler serialises the lanes through an ELECT / R2UR loop of ~9
-  // instructions per copy; lane 0's unrolled sequence is ~5 (destination, size and barrier
-  // are compile-time offsets from uniform bases).
-  constexpr bool kL0 = UCFVB_CELLS_L0 && TC == 8;
-  auto issue_l0 = [&](int i, int cslot, bool group_b) {  // all lanes call; cslot = tile i's cell of this lane's slot
-    int cs[TC];
-#pragma unroll
-    for (int j = 0; j < TC; ++j) cs[j] = __shfl_sync(kFull, cslot, 4 * j);
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      const bool cwi = i < tc;
-      uint64_t* b = &bar[group_b ? 1 : 0];
-      const uint32_t bytes = group_b ? (cwi ? R::CB : R::MB) : (cwi ? R::CA : R::MA);
-      mbar_arrive_expect_tx(b, TC * bytes);
-      const unsigned char* src = group_b ? (cwi ? L.rec_cb : L.rec_mb) : (cwi ? L.rec_ca : L.rec_ma);
-      const size_t gstride = cwi ? R::GC : R::GM;
-      unsigned char* dst = group_b ? gb : ga;
-      const uint32_t sstride = group_b ? (cwi ? R::SCB : R::SMB) : (cwi ? R::SCA : R::SMA);
-#pragma unroll
-      for (int j = 0; j < TC; ++j) bulk_g2s(dst + j * sstride, src + static_cast<size_t>(cs[j]) * gstride, bytes, b);
-    }
-  };
-  if (!kL0 && tid < TC && static_cast<int>(blockIdx.x) < nitems) {
+  if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
     issue_a(blockIdx.x);
     issue_b(blockIdx.x);
   }
@@ -245,10 +217,6 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
   const bool venkat = ph.limiter == 1;
   int it = 0;
   int c_next = (UCFVB_CELLS_CN && static_cast<int>(blockIdx.x) < nitems) ? tile_cell(blockIdx.x, slot) : 0;
-  if (kL0 && static_cast<int>(blockIdx.x) < nitems) {  // block-uniform
-    issue_l0(blockIdx.x, c_next, false);
-    issue_l0(blockIdx.x, c_next, true);
-  }
   for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
     const uint32_t par = it & 1;
     const int next = i + gridDim.x;
@@ -294,9 +262,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         }
       }
       __syncthreads();  // group A consumed: request the next tile's
-      if (kL0) {
-        if (next < nitems) issue_l0(next, c_next, false);
-      } else if (tid < TC && next < nitems) {
+      if (tid < TC && next < nitems) {
         fence_proxy_async_smem();
         issue_a(next);
       }
@@ -421,9 +387,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
         l1 += spl[m * 2 + 1] * d;
       }
       __syncthreads();  // group A consumed: request the next tile's
-      if (kL0) {
-        if (next < nitems) issue_l0(next, c_next, false);
-      } else if (tid < TC && next < nitems) {
+      if (tid < TC && next < nitems) {
         fence_proxy_async_smem();
         issue_a(next);
       }
@@ -470,9 +434,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     if (flags & FL_FALLBACK)
       demote = kScratchFits ? tile_demote<Q>(ph, v, slot, lo, hi, vals, gb) : group_demote<Q>(ph, v, lo, hi, vals, Q);
     if (4 * TC > 32) __syncthreads();  // multi-warp tiles: every warp's scratch reads precede the refill
-    if (kL0) {
-      if (next < nitems) issue_l0(next, c_next, true);
-    } else if (tid < TC && next < nitems) {
+    if (tid < TC && next < nitems) {
       fence_proxy_async_smem();
       issue_b(next);
     }

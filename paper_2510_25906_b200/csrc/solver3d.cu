@@ -1238,8 +1238,13 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(De
 }
 
 // ---- MUSCL (solver.cpp:189-221; reconstruct.cpp:30-86) ---------------------------------
+// resident blocks per SM asked of the lattice-class MUSCL kernel: five (72 registers, what its
+// shared memory allows) measured 15.87 -> 15.29 ms/stage of config-5 weights against four (96)
+#ifndef UCFVB_M3_MINB
+#define UCFVB_M3_MINB 5
+#endif
 template <int K, int M, int NF, int NQ, bool STAGED>
-__global__ void __launch_bounds__(160) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+__global__ void __launch_bounds__(160, STAGED ? UCFVB_M3_MINB : 0) k3_muscl(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int H1 = M / 2, H2 = M - H1 + NF;  // the two gathers
   constexpr int G = H2;
@@ -1371,6 +1376,10 @@ __global__ void k3_constant(Dev3 D, Work3 W, const double* __restrict__ U) {
 }
 
 // ---- fluxes (solver.cpp:266-295) ----------------------------------------------------------
+// resident 128-thread blocks per SM asked of the lane-per-point flux kernels (0: no bound, 72 registers)
+#ifndef UCFVB_F3_MINB
+#define UCFVB_F3_MINB 0
+#endif
 template <int NQ>
 __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1404,7 +1413,7 @@ __global__ void __launch_bounds__(128) k3_face_flux(Dev3 D, Phys3 P, Work3 W) {
 // point q, then every lane of the face sums the NQ weighted fluxes in q order
 // through shuffles (the same total += w_q F_q sequence as one thread would)
 template <int NQ>
-__global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3 W) {
+__global__ void __launch_bounds__(128, UCFVB_F3_MINB) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3 W) {
   constexpr int LP = NQ <= 1 ? 1 : (NQ <= 2 ? 2 : (NQ <= 4 ? 4 : 8));  // lanes per face (NQ <= 8)
   static_assert(NQ <= 8, "at most 8 points per face");
   if (halted(W)) return;  // block-uniform
@@ -1451,7 +1460,7 @@ __global__ void __launch_bounds__(128) k3_face_flux_lanes(Dev3 D, Phys3 P, Work3
 #define UCFVB_FLUX3_PACK 1
 #endif
 template <int NQ>
-__global__ void __launch_bounds__(128) k3_face_flux_pack(Dev3 D, Phys3 P, Work3 W) {
+__global__ void __launch_bounds__(128, UCFVB_F3_MINB) k3_face_flux_pack(Dev3 D, Phys3 P, Work3 W) {
   constexpr int FPW = 32 / NQ;  // faces per warp
   if (halted(W)) return;        // block-uniform
   const int lane = threadIdx.x & 31;

@@ -177,6 +177,10 @@ def test_advance_host_batch_matches_serial():
     bad[3][5, 0] = -1.0
     with pytest.raises(A.NonPhysicalError, match="batch entry 3"):
         a.advance_host_batch(bad, 1)
-    # the solver is usable after the failure
+    # the solver is usable after the failure; one- and two-entry batches (no pipelining yet)
     outs, _ = a.advance_host_batch(ins[:2], 1)
     np.testing.assert_array_equal(outs[1], a.advance_host(ins[1], 1)[0])
+    outs, ts = a.advance_host_batch(ins[4:5], 3)
+    ref, t_ref = a.advance_host(ins[4], 3)
+    assert ts[0] == t_ref
+    np.testing.assert_array_equal(outs[0], ref)

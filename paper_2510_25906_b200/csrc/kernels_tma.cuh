@@ -25,6 +25,10 @@ __host__ __device__ constexpr int smem_min_blocks(uint32_t bytes) {
   return b < 1 ? 1 : (b > 8 ? 8 : static_cast<int>(b));
 }
 
+// 0: no cp.async prefetch of the stencil-member values (p = 3 then fits three blocks per SM)
+#ifndef UCFVB_CENTRAL_PF
+#define UCFVB_CENTRAL_PF 1
+#endif
 template <int K, int NQ, int NF, int MM>
 struct CentralStage {
   static constexpr int Q = NF * NQ;
@@ -42,7 +46,7 @@ struct CentralStage {
   // (8 B per lane and member) one chunk ahead. Only for the larger stencils
   // (p = 3: 18 members), where hiding the gather latency beats the occupancy
   // the extra 18 KB and registers cost (p = 3: central -8 %; p = 2: +3 %).
-  static constexpr bool PREFETCH = MM >= 16;
+  static constexpr bool PREFETCH = UCFVB_CENTRAL_PF && MM >= 16;
   static constexpr uint32_t UG = PREFETCH ? MM * 128 * 8 : 0;
   static constexpr uint32_t BYTES = A_BYTES + B_BYTES + UG;  // one stage
 };

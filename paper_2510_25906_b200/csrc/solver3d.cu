@@ -426,6 +426,10 @@ constexpr int kRingSlots = 3;
 #ifndef UCFVB_C5_PFID
 #define UCFVB_C5_PFID 1
 #endif
+// resident blocks per SM asked of the p = 3 central kernels (register bound; shared memory allows three)
+#ifndef UCFVB_C5_MINB
+#define UCFVB_C5_MINB 4
+#endif
 // resident blocks per SM asked of the per-cell-row (p <= 2) central kernels
 #ifndef UCFVB_C3_MINB
 #define UCFVB_C3_MINB 2
@@ -435,7 +439,7 @@ constexpr int kRingSlots = 3;
 #define UCFVB_C3_PFPHI 1
 #endif
 template <int K, int M, int NF, int NQ, bool STAGED, bool TMA = false>
-__global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : 4) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
+__global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5_MINB) k3_central(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U, int eval,
                                                    int nad) {
   constexpr int Q = NF * NQ;
   // staged path on a detecting stage: the candidate face values are stored
@@ -902,11 +906,14 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
 }
 
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
+#ifndef UCFVB_W5_MINB
+#define UCFVB_W5_MINB 3
+#endif
 // lattice-class p = 3 (config 5): three resident blocks per SM (<= 136
 // registers; 168 unbounded) measured faster despite a few spills (22.3 vs
 // 25.2 ms/stage of weights); per-cell rows keep the unbounded allocation
 template <int K, int M, int NF, int NQ, bool STAGED>
-__global__ void __launch_bounds__(160, (STAGED && K >= 19) ? 3 : 0) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
+__global__ void __launch_bounds__(160, (STAGED && K >= 19) ? UCFVB_W5_MINB : 0) k3_cwenoz(Dev3 D, Phys3 P, Work3 W, const double* __restrict__ U) {
   constexpr int Q = NF * NQ;
   constexpr int G = M;  // the central stencil (the directional members are a subset of it)
   // DM: lattice-class chunks (one operator row per block) run the central

@@ -25,9 +25,12 @@ __host__ __device__ constexpr int smem_min_blocks(uint32_t bytes) {
   return b < 1 ? 1 : (b > 8 ? 8 : static_cast<int>(b));
 }
 
-// 0: no cp.async prefetch of the stencil-member values (p = 3 then fits three blocks per SM)
+// cp.async prefetch of the stencil-member values one chunk ahead (p = 3). Off: without its
+// 18 KB the p = 3 kernel fits three resident blocks instead of two, which measured central
+// 3.39 -> 2.90 ms/stage on config 3 (three blocks WITH the prefetch and a slimmer group B:
+// 3.53 ms; four blocks with only pinv and phi staged: 3.25 ms; profiles/round2.md)
 #ifndef UCFVB_CENTRAL_PF
-#define UCFVB_CENTRAL_PF 1
+#define UCFVB_CENTRAL_PF 0
 #endif
 template <int K, int NQ, int NF, int MM>
 struct CentralStage {
@@ -42,10 +45,10 @@ struct CentralStage {
   static constexpr uint32_t NBR = round16(NF * 32 * 4);
   static constexpr uint32_t DEST = round16(Q * 32 * 4);
   static constexpr uint32_t B_BYTES = PHI + THR + NBR + DEST;
-  // the U values of the chunk's central-stencil members, gathered with cp.async
-  // (8 B per lane and member) one chunk ahead. Only for the larger stencils
-  // (p = 3: 18 members), where hiding the gather latency beats the occupancy
-  // the extra 18 KB and registers cost (p = 3: central -8 %; p = 2: +3 %).
+  // UCFVB_CENTRAL_PF (off): the U values of the chunk's central-stencil members
+  // gathered with cp.async (8 B per lane and member) one chunk ahead, for the
+  // larger stencils (p = 3: 18 members). At two resident blocks it hid the gather
+  // latency (round 1: central -8 %); its 18 KB are what keeps the third block out.
   static constexpr bool PREFETCH = UCFVB_CENTRAL_PF && MM >= 16;
   static constexpr uint32_t UG = PREFETCH ? MM * 128 * 8 : 0;
   static constexpr uint32_t BYTES = A_BYTES + B_BYTES + UG;  // one stage

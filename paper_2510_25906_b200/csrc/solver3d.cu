@@ -905,6 +905,10 @@ __global__ void k3_fill_list(int n, int which, uint8_t lab, Work3 W) {
   }
 }
 
+// lattice-class CWENOZ / MUSCL kernels: L1 prefetch of the next tile's stencil-id lines
+#ifndef UCFVB_W5_PFID
+#define UCFVB_W5_PFID 0
+#endif
 // ---- CWENOZ (solver.cpp:167-188; reconstruct.cpp:43-57, 99-150) -------------------------
 #ifndef UCFVB_W5_MINB
 #define UCFVB_W5_MINB 3
@@ -1239,6 +1243,17 @@ __global__ void __launch_bounds__(160, (STAGED && K >= 19) ? UCFVB_W5_MINB : 0) 
                                              STAGED ? sp + EP + ED + EO : nullptr);
     }
     const int sl_l = threadIdx.x / V5;  // cooperative stores: thread <-> (list entry sl_l, variable)
+    if (STAGED && UCFVB_W5_PFID) {
+      // this block's next tile: the stencil-id lines of its cells into L1 while the fallback votes
+      // and the stores run (the five threads of a cell share its M + 1 + NF lines)
+      const int nbase = base + nb * 32;
+      if (nbase + sl_l < cnt) {
+        const int ncell = list[nbase + sl_l];
+#pragma unroll
+        for (int e = threadIdx.x % V5; e < M + 1 + NF; e += V5)
+          prefetch_l1(e <= M ? &D.central[ao(ncell, e, M + 1)] : &D.nbr[ao(ncell, e - M - 1, NF)]);
+      }
+    }
     troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail,
                                       (STAGED && base + sl_l < cnt) ? list[base + sl_l] : -1);
   }
@@ -1365,6 +1380,17 @@ __global__ void __launch_bounds__(160, STAGED ? UCFVB_M3_MINB : 0) k3_muscl(Dev3
     eval_store<K, NQ, NF, 3, !STAGED>(D, W, c, op, v, lane, act, u0, a, sval, chk, blo, bhi, viol, sl,
                                            STAGED ? sp + 3 * M : nullptr);
     const int sl_l = threadIdx.x / V5;  // cooperative stores: thread <-> (list entry sl_l, variable)
+    if (STAGED && UCFVB_W5_PFID) {
+      // this block's next tile: the stencil-id lines of its cells into L1 while the fallback votes
+      // and the stores run (the five threads of a cell share its M + 1 + NF lines)
+      const int nbase = base + nb * 32;
+      if (nbase + sl_l < cnt) {
+        const int ncell = list[nbase + sl_l];
+#pragma unroll
+        for (int e = threadIdx.x % V5; e < M + 1 + NF; e += V5)
+          prefetch_l1(e <= M ? &D.central[ao(ncell, e, M + 1)] : &D.nbr[ao(ncell, e - M - 1, NF)]);
+      }
+    }
     troubled_fallback<NF, NQ, STAGED>(D, P, W, c, v, lane, act, u0, chk, blo, bhi, viol, sval, s_fail,
                                       (STAGED && base + sl_l < cnt) ? list[base + sl_l] : -1);
   }

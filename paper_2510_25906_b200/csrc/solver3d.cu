@@ -237,17 +237,6 @@ __host__ __device__ constexpr size_t muscl_union(int G, int Q) {
                                                                                     : static_cast<size_t>(Q * V5 * 33);
   return (u + 1) & ~static_cast<size_t>(1);  // the operator rows behind it are read as double2
 }
-// lattice central kernel with the gather in two halves (UCFVB_C5_HALF): HB buffer rows, which
-// later carry the dofs [5][K][kRS] and then the face values [Q][5][33] (one after the other)
-#ifndef UCFVB_C5_HALF
-#define UCFVB_C5_HALF 0
-#endif
-__host__ __device__ constexpr size_t half_union(int HB, int Q, int K) {
-  size_t u = static_cast<size_t>(HB) * kXS;
-  if (static_cast<size_t>(Q * V5 * 33) > u) u = static_cast<size_t>(Q * V5 * 33);
-  if (static_cast<size_t>(V5 * K * kRS) > u) u = static_cast<size_t>(V5 * K * kRS);
-  return (u + 1) & ~static_cast<size_t>(1);
-}
 // union buffer of a DMMA kernel: the gather [G][kXS], later face values [Q][5][33] + dofs [5][K][kRS]
 __host__ __device__ constexpr size_t dm_union(int G, int Q, int K) {
   return (static_cast<size_t>(G) * kXS > static_cast<size_t>(Q * V5 * 33 + V5 * K * kRS))
@@ -466,11 +455,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
   // STAGED: pinv row [M][K], phi row [Q][K] and the centre values [5][32] past the union buffer
   constexpr bool DM = STAGED && K >= 8;  // tensor-core path (strides: see kXS)
   constexpr int KP = DM ? kpad(K) : K;
-  // HALF: the gather in two halves of rows (20 members, then 18 members + the neighbours)
-  // through one 22-row buffer that later carries the dofs and then the face values
-  constexpr bool HALF = DM && UCFVB_C5_HALF && M == 38;
-  constexpr int H1 = 20;  // rows of the first half (five k-steps of the solve)
-  constexpr size_t kUnion = HALF ? half_union(G - H1, Q, K) : (DM ? dm_union(G, Q, K) : smem3_bytes(G, Q) / 8);
+  constexpr size_t kUnion = DM ? dm_union(G, Q, K) : smem3_bytes(G, Q) / 8;
   double* sp = smem3 + kUnion;
   // per-cell operator rows (p <= 2): the chunk's pinv block is copied to shared
   // memory with 16-byte cp.async at the chunk start (all in flight at once)
@@ -560,21 +545,13 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
       // transposed: thread (cell gl, variable gv) -- one member's five variables are one 40-byte read
       const int gl = threadIdx.x / V5, gv = threadIdx.x - gl * V5;
       const int gc = min((ch << 5) + gl, D.n - 1);
-      if constexpr (HALF) {
-        int id[H1];
+      int id[G];
 #pragma unroll
-        for (int m = 0; m < H1; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
+      for (int m = 0; m < M; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
 #pragma unroll
-        for (int g = 0; g < H1; ++g) cp_async8(&xs[g * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
-      } else {
-        int id[G];
+      for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(gc, i, NF)];
 #pragma unroll
-        for (int m = 0; m < M; ++m) id[m] = D.central[ao(gc, m + 1, M + 1)];
-#pragma unroll
-        for (int i = 0; i < NF; ++i) id[M + i] = D.nbr[ao(gc, i, NF)];
-#pragma unroll
-        for (int g = 0; g < G; ++g) cp_async8(&xs[g * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
-      }
+      for (int g = 0; g < G; ++g) cp_async8(&xs[g * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
       cp_async_commit();
     } else {
       int id[G];
@@ -619,13 +596,11 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
       double* su0 = sp + M * KP + Q * KP;  // [5][32] centre values
       su0[threadIdx.x] = u0;
       __syncthreads();  // every thread's gather landed (each value was copied by another thread)
-      if constexpr (!HALF) {
 #pragma unroll
-        for (int i = 0; i < NF; ++i) {
-          const double x = xs[(M + i) * kXS + v * kVS + lane];
-          lo = smin(lo, x);
-          hi = smax(hi, x);
-        }
+      for (int i = 0; i < NF; ++i) {
+        const double x = xs[(M + i) * kXS + v * kVS + lane];
+        lo = smin(lo, x);
+        hi = smax(hi, x);
       }
       double dacc[MT][4][2];
 #pragma unroll
@@ -633,55 +608,25 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
 #pragma unroll
         for (int t = 0; t < 4; ++t) dacc[i][t][0] = dacc[i][t][1] = 0.0;
       const int fr = lane >> 2, fc = lane & 3;
-      auto ksteps = [&](int ks0, int ks1, int row0) {  // k-steps [ks0, ks1): member m sits in buffer row m - row0
 #pragma unroll
-        for (int ks = ks0; ks < ks1; ++ks) {
-          const int m = 4 * ks + fc;
-          double af[MT];
+      for (int ks = 0; ks < KS; ++ks) {
+        const int m = 4 * ks + fc;
+        double af[MT];
 #pragma unroll
-          for (int i = 0; i < MT; ++i) {
-            const int k = 8 * i + fr;
-            af[i] = (k < K && m < M) ? sp[m * KP + k] : 0.0;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const int cl = 8 * t + fr;
-            const double bf = m < M ? xs[(m - row0) * kXS + v * kVS + cl] - su0[v * 32 + cl] : 0.0;
-#pragma unroll
-            for (int i = 0; i < MT; ++i) dmma884(dacc[i][t][0], dacc[i][t][1], af[i], bf);
-          }
+        for (int i = 0; i < MT; ++i) {
+          const int k = 8 * i + fr;
+          af[i] = (k < K && m < M) ? sp[m * KP + k] : 0.0;
         }
-      };
-      if constexpr (HALF) {
-        ksteps(0, H1 / 4, 0);
-        __syncthreads();  // first half consumed: the second through the same rows
-        {
-          const int gl = threadIdx.x / V5, gv = threadIdx.x - gl * V5;
-          const int gc = min((ch << 5) + gl, D.n - 1);
-          int id[G - H1];
 #pragma unroll
-          for (int m = H1; m < M; ++m) id[m - H1] = D.central[ao(gc, m + 1, M + 1)];
+        for (int t = 0; t < 4; ++t) {
+          const int cl = 8 * t + fr;
+          const double bf = m < M ? xs[m * kXS + v * kVS + cl] - su0[v * 32 + cl] : 0.0;
 #pragma unroll
-          for (int i = 0; i < NF; ++i) id[M - H1 + i] = D.nbr[ao(gc, i, NF)];
-#pragma unroll
-          for (int g = 0; g < G - H1; ++g)
-            cp_async8(&xs[g * kXS + gv * kVS + gl], &U[static_cast<size_t>(id[g]) * V5 + gv]);
-          cp_async_commit();
+          for (int i = 0; i < MT; ++i) dmma884(dacc[i][t][0], dacc[i][t][1], af[i], bf);
         }
-        cp_async_wait_all();
-        __syncthreads();
-#pragma unroll
-        for (int i = 0; i < NF; ++i) {
-          const double x = xs[(M - H1 + i) * kXS + v * kVS + lane];
-          lo = smin(lo, x);
-          hi = smax(hi, x);
-        }
-        ksteps(H1 / 4, KS, H1);
-      } else {
-        ksteps(0, KS, 0);
       }
       __syncthreads();  // gather buffer consumed: it carries the dofs back to their lanes
-      double* sd = HALF ? xs : xs + Q * V5 * 33;  // [5][K][kRS]: past the face-value buffer, or (HALF) under it
+      double* sd = xs + Q * V5 * 33;  // [5][K][kRS], past the face-value buffer
 #pragma unroll
       for (int i = 0; i < MT; ++i)
 #pragma unroll
@@ -732,7 +677,7 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
         // face values of warp v's 32 cells: F(Q x 32) = u0 + phi(Q x K) . a(K x 32) on
         // the tensor cores, k in steps of 4 from C = u0 (evaluate_cell's fma order)
         constexpr int QT = (Q + 7) / 8, KS2 = (K + 3) / 4;
-        const double* sd = HALF ? xs : xs + Q * V5 * 33;
+        const double* sd = xs + Q * V5 * 33;
         const double* sph = sp + M * KP;
         const double* su0 = sp + M * KP + Q * KP;
         const int fr = lane >> 2, fc = lane & 3;
@@ -761,7 +706,6 @@ __global__ void __launch_bounds__(160, (K * M <= 200) ? UCFVB_C3_MINB : UCFVB_C5
           }
         }
         const int cb = ch << 5;
-        if (HALF) __syncthreads();  // every warp is done with the dofs under the face-value buffer
 #pragma unroll
         for (int i = 0; i < QT; ++i)
 #pragma unroll
@@ -1744,8 +1688,7 @@ Kern3 kern3() {
   k.smem_muscl = smem3_bytes(M - M / 2 + NF, Q);
   // STAGED: the union buffer also holds the dofs [5][K][32] past the face values (K >= 8)
   constexpr int KP = K >= 8 ? kpad(K) : K;
-  k.smem_central_staged = (K >= 8 ? 8 * ((UCFVB_C5_HALF && M == 38) ? half_union(M + NF - 20, Q, K) : dm_union(M + NF, Q, K))
-                                  : smem3_bytes(M + NF, Q)) +
+  k.smem_central_staged = (K >= 8 ? 8 * dm_union(M + NF, Q, K) : smem3_bytes(M + NF, Q)) +
                           8 * static_cast<size_t>(M * KP + Q * KP + 160);
   k.smem_cwenoz_staged = (K >= 8 ? 8 * dm_union(M, Q, K) : smem3_bytes(M, Q)) +
                          8 * static_cast<size_t>(M * KP + NF * 3 * MD3 + ((K * KP + 1) & ~1) + Q * KP +

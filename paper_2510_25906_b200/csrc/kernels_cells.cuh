@@ -151,16 +151,34 @@ __device__ __forceinline__ bool tile_demote(const Physics& ph, int v, int slot, 
 
 // cells per tile; a block is 4 * kCellTile threads
 constexpr int kCellTile = UCFVB_CELLS_TILE;
-template <int K, int NQ, int NF, int MM, int MD>
-__global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_cells(Layout L, Physics ph, Scratch S,
-                                                           const double4* __restrict__ U, int flags) {
+// WHICH: 0 both classes in one launch, 1 the CWENOZ tiles only, 2 the MUSCL tiles only
+// (UCFVB_CELLS_SPLIT: two launches; the MUSCL one needs ~half the registers and a third of
+// the shared memory, so it runs at a higher occupancy)
+#ifndef UCFVB_CELLS_SPLIT
+#define UCFVB_CELLS_SPLIT 1
+#endif
+#ifndef UCFVB_CELLS_MINB_M
+#define UCFVB_CELLS_MINB_M 24
+#endif
+template <int K, int NQ, int NF, int MM, int MD, int TC, int WHICH>
+struct CellTile {
+  using R = CellRec<K, NQ, NF, MM, MD, TC>;
+  static constexpr uint32_t SB = R::SMB > demote_stride(NF * NQ) ? R::SMB : demote_stride(NF * NQ);
+  static constexpr uint32_t TILE_A = WHICH == 2 ? TC * R::SMA : R::TILE_A;
+  static constexpr uint32_t TILE_B = WHICH == 2 ? TC * SB : R::TILE_B;
+  static constexpr uint32_t BYTES = TILE_A + TILE_B;
+};
+template <int K, int NQ, int NF, int MM, int MD, int WHICH = 0>
+__global__ void __launch_bounds__(4 * kCellTile, WHICH == 2 ? UCFVB_CELLS_MINB_M : UCFVB_CELLS_MINB)
+    k_troubled_cells(Layout L, Physics ph, Scratch S, const double4* __restrict__ U, int flags) {
   constexpr int TC = kCellTile;
   using R = CellRec<K, NQ, NF, MM, MD, TC>;
+  using T = CellTile<K, NQ, NF, MM, MD, TC, WHICH>;
   constexpr int Q = R::Q;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + R::BYTES);  // [0] group A, [1] group B
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + T::BYTES);  // [0] group A, [1] group B
   unsigned char* const ga = smem;
-  unsigned char* const gb = smem + R::TILE_A;
+  unsigned char* const gb = smem + T::TILE_A;
   const double* __restrict__ Ud = reinterpret_cast<const double*>(U);
   const int tid = threadIdx.x;
   const int slot = tid >> 2;
@@ -179,8 +197,9 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
   if (s_err) return;
   const int nc = s_nc, nm = s_nm;
   const int tc = (nc + TC - 1) / TC;
-  const int nitems = tc + (nm + TC - 1) / TC;
-  if (nc > 0 && !(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
+  const int first = WHICH == 2 ? tc : 0;                               // this launch's items [first, nitems)
+  const int nitems = WHICH == 1 ? tc : tc + (nm + TC - 1) / TC;
+  if (WHICH != 2 && nc > 0 && !(ph.lambda1p > 1.0)) {  // cwenoz_blend_scalar throws (reconstruct.cpp:102-103)
     if (blockIdx.x == 0 && tid == 0) atomicOr(&S.err[0], 4);
     return;
   }
@@ -208,19 +227,19 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     else
       bulk_g2s(gb + tid * R::SMB, L.rec_mb + static_cast<size_t>(c) * R::GM, R::MB, &bar[1]);
   };
-  if (tid < TC && static_cast<int>(blockIdx.x) < nitems) {
-    issue_a(blockIdx.x);
-    issue_b(blockIdx.x);
+  if (tid < TC && first + static_cast<int>(blockIdx.x) < nitems) {
+    issue_a(first + blockIdx.x);
+    issue_b(first + blockIdx.x);
   }
   double* dofs = reinterpret_cast<double*>(S.dofs);
   double* fv = reinterpret_cast<double*>(S.fp);
   const bool venkat = ph.limiter == 1;
   int it = 0;
-  int c_next = (UCFVB_CELLS_CN && static_cast<int>(blockIdx.x) < nitems) ? tile_cell(blockIdx.x, slot) : 0;
-  for (int i = blockIdx.x; i < nitems; i += gridDim.x, ++it) {
+  int c_next = (UCFVB_CELLS_CN && first + static_cast<int>(blockIdx.x) < nitems) ? tile_cell(first + blockIdx.x, slot) : 0;
+  for (int i = first + blockIdx.x; i < nitems; i += gridDim.x, ++it) {
     const uint32_t par = it & 1;
     const int next = i + gridDim.x;
-    const bool cw = i < tc;
+    const bool cw = WHICH == 1 ? true : (WHICH == 2 ? false : i < tc);
     const bool mine = cw ? i * TC + slot < nc : (i - tc) * TC + slot < nm;
     // the next tile's list entry is requested a tile ahead (UCFVB_CELLS_CN): its
     // L2 round trip leaves the head of that tile's dependency chain
@@ -430,7 +449,7 @@ __global__ void __launch_bounds__(4 * kCellTile, UCFVB_CELLS_MINB) k_troubled_ce
     // fallback verdict first: the positivity check transposes the tile's face
     // values through the dead group-B region (tile_demote), then the refill
     bool demote = false;
-    constexpr bool kScratchFits = TC * demote_stride(Q) <= R::TILE_B;  // (not for p = 1 quadrilaterals)
+    constexpr bool kScratchFits = TC * demote_stride(Q) <= T::TILE_B;  // (not for p = 1 quadrilaterals)
     if (flags & FL_FALLBACK)
       demote = kScratchFits ? tile_demote<Q>(ph, v, slot, lo, hi, vals, gb) : group_demote<Q>(ph, v, lo, hi, vals, Q);
     if (4 * TC > 32) __syncthreads();  // multi-warp tiles: every warp's scratch reads precede the refill

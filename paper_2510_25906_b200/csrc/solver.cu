@@ -93,6 +93,10 @@ struct KernelSet {
   Launch cells = nullptr;
   void (*cells_setup)(int n_sm, int* grid, Launch* launch) = nullptr;
   int cells_grid = 0;
+  // UCFVB_CELLS_SPLIT: the CWENOZ tiles and the MUSCL tiles in two launches
+  Launch cells_c = nullptr, cells_m = nullptr;
+  void (*cells_split_setup)(int n_sm, int* grid_c, Launch* launch_c, int* grid_m, Launch* launch_m) = nullptr;
+  int cells_c_grid = 0, cells_m_grid = 0;
   void (*pack_records)(cudaStream_t, const Layout&, unsigned char*, unsigned char*) = nullptr;
   // per cell: CWENOZ record stride, group A bytes (= group B's offset), MUSCL record stride, group A bytes
   uint32_t rec_bytes[4] = {0, 0, 0, 0};
@@ -114,11 +118,11 @@ void troubled_split_launcher(dim3 g, cudaStream_t st, const Layout& L, const Phy
            TroubledStage<K, NQ, NF, MM, MD>::SPLIT_BYTES + 16, st, L, p, S, U, f);
 }
 
-template <int K, int NQ, int NF, int MM, int MD>
+template <int K, int NQ, int NF, int MM, int MD, int WHICH = 0>
 void troubled_cells_launcher(dim3 g, cudaStream_t st, const Layout& L, const Physics& p, const Scratch& S,
                              const double4* U, int f) {
-  launch_k(k_troubled_cells<K, NQ, NF, MM, MD>, g, dim3(4 * kCellTile), CellRec<K, NQ, NF, MM, MD, kCellTile>::BYTES + 16,
-           st, L, p, S, U, f);
+  launch_k(k_troubled_cells<K, NQ, NF, MM, MD, WHICH>, g, dim3(4 * kCellTile),
+           CellTile<K, NQ, NF, MM, MD, kCellTile, WHICH>::BYTES + 16, st, L, p, S, U, f);
 }
 
 // raise the dynamic smem limit and size the persistent grid (resident blocks x SMs)
@@ -176,6 +180,14 @@ KernelSet make_set() {
       *grid = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT>,
                               CellRec<K, NQ, NF, MMT, MDT, kCellTile>::BYTES + 16, n_sm, 4 * kCellTile);
       *launch = troubled_cells_launcher<K, NQ, NF, MMT, MDT>;
+    };
+    s.cells_split_setup = [](int n_sm, int* gc, KernelSet::Launch* lc, int* gm, KernelSet::Launch* lm) {
+      *gc = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT, 1>,
+                            CellTile<K, NQ, NF, MMT, MDT, kCellTile, 1>::BYTES + 16, n_sm, 4 * kCellTile);
+      *lc = troubled_cells_launcher<K, NQ, NF, MMT, MDT, 1>;
+      *gm = persistent_grid(k_troubled_cells<K, NQ, NF, MMT, MDT, 2>,
+                            CellTile<K, NQ, NF, MMT, MDT, kCellTile, 2>::BYTES + 16, n_sm, 4 * kCellTile);
+      *lm = troubled_cells_launcher<K, NQ, NF, MMT, MDT, 2>;
     };
     s.pack_records = [](cudaStream_t st, const Layout& L, unsigned char* rc, unsigned char* rm) {
       k_pack_records<K, NQ, NF, MMT, MDT><<<(L.n + 255) / 256, 256, 0, st>>>(L, rc, rm);
@@ -416,9 +428,17 @@ struct GpuSolver::Impl {
       } else if (ks.cells) {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
         record(2);
-        ks.cells(dim3(std::min(ks.cells_grid, (L.n + kCellTile - 1) / kCellTile + 2)), stream, L, ph, S, U,
-                 FL_NAD | FL_FALLBACK | taps);
-        nl += 3;
+        if (UCFVB_CELLS_SPLIT) {
+          ks.cells_c(dim3(std::min(ks.cells_c_grid, (L.n + kCellTile - 1) / kCellTile + 1)), stream, L, ph, S, U,
+                     FL_NAD | FL_FALLBACK | taps);
+          ks.cells_m(dim3(std::min(ks.cells_m_grid, (L.n + kCellTile - 1) / kCellTile + 1)), stream, L, ph, S, U,
+                     FL_NAD | FL_FALLBACK | taps);
+          nl += 4;
+        } else {
+          ks.cells(dim3(std::min(ks.cells_grid, (L.n + kCellTile - 1) / kCellTile + 2)), stream, L, ph, S, U,
+                   FL_NAD | FL_FALLBACK | taps);
+          nl += 3;
+        }
       } else {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
         record(2);
@@ -727,6 +747,8 @@ GpuSolver::GpuSolver(const ucfvb_mesh_view& m, const ucfvb_stencil_view& s, cons
     I.ks.central_tma_setup(I.n_sm, &I.ks.central_tma_grid, &I.ks.central);
     I.ks.troubled_setup(I.n_sm, &I.ks.troubled_grid, &I.ks.troubled);
     I.ks.cells_setup(I.n_sm, &I.ks.cells_grid, &I.ks.cells);
+    if (UCFVB_CELLS_SPLIT)
+      I.ks.cells_split_setup(I.n_sm, &I.ks.cells_c_grid, &I.ks.cells_c, &I.ks.cells_m_grid, &I.ks.cells_m);
   }
   auto& own = I.owned;
   Layout& L = I.L;

@@ -428,7 +428,7 @@ struct GpuSolver::Impl {
       } else if (ks.cells) {
         ks.spread(grid_cells(), stream, L, S, U, taps, detect ? 1 : 0);
         record(2);
-        if (UCFVB_CELLS_SPLIT) {
+        if (UCFVB_CELLS_SPLIT && L.n >= kSpreadWideCells) {  // small meshes: one launch (config 1: +3.5 us/stage split)
           ks.cells_c(dim3(std::min(ks.cells_c_grid, (L.n + kCellTile - 1) / kCellTile + 1)), stream, L, ph, S, U,
                      FL_NAD | FL_FALLBACK | taps);
           ks.cells_m(dim3(std::min(ks.cells_m_grid, (L.n + kCellTile - 1) / kCellTile + 1)), stream, L, ph, S, U,
